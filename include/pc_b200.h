@@ -1,0 +1,157 @@
+/*
+ * pc_b200.h — C ABI of the B200 training-step library (libpcb200.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `parconv`
+ * (pure Python/numpy, /root/reference/pkg/src/parconv). Each entry point
+ * replaces one reference kernel call made by the step engine
+ * `schemes.column_fwd_bwd` (schemes.py:342-419) or the data-parallel leg of
+ * `schemes.hybrid_step` (schemes.py:540-558); the Python drop-in binds them
+ * with ctypes (paper_1312_5853_b200/_lib.py; INTEGRATION.md shows the stub).
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless noted; sizes are element counts.
+ *  - Activations are NHWC ("channels last"), row = pixel (b, y, x), in the
+ *    storage precision `prec` (PC_FP32 -> float, PC_BF16 -> __nv_bfloat16).
+ *    Master weights, velocities and weight gradients are always float.
+ *  - A channel-blocked activation (the cross-layer concatenation of m column
+ *    slices) stores channel c at  base + (c / cs) * cstride + pixel * cs + c % cs.
+ *    cs == C (cstride ignored) is plain NHWC.
+ *  - Conv weights are stored [N][kh][kw][C] (reference: [N][C][kh][kw]).
+ *  - FC weights are stored [U][D] (reference: [D][U], kernels.py:160-168).
+ *  - Every function is asynchronous on `stream` and returns a status:
+ *      0 ok, 1 shape error, 2 validation error, 3 CUDA error, 4 NCCL error.
+ *    pc_last_error() returns the message of the calling thread's last error.
+ *  - Functions never allocate device memory; callers pass workspaces.
+ *  - Reentrant; the caller selects the device (cudaSetDevice) beforehand.
+ */
+#ifndef PC_B200_H
+#define PC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define PC_API __attribute__((visibility("default")))
+#else
+#define PC_API
+#endif
+
+typedef void* pc_stream_t; /* cudaStream_t */
+
+enum pc_prec { PC_FP32 = 0, PC_BF16 = 1 };
+enum pc_status { PC_OK = 0, PC_ESHAPE = 1, PC_EVALUE = 2, PC_ECUDA = 3, PC_ENCCL = 4 };
+enum pc_conv_flags { PC_RELU = 1, PC_WANT_DX = 2, PC_WANT_DW = 4, PC_MASK_DX = 8 };
+
+/* Conv geometry (reference ConvParams + input shape, kernels.py:37-83). */
+typedef struct {
+  int B, H, W, C;      /* input extents (C = full, possibly concatenated, channels) */
+  int N, k, stride, pad;
+  int Ho, Wo;          /* output extents; must equal (H+2p-k)/s+1 exactly */
+  int cs;              /* channels per input block (== C when not blocked) */
+  long long cstride;   /* elements between input channel blocks */
+} pc_conv_geom;
+
+/* Matrix view: element (r, c) at ptr + (c / cb) * bstride + r * ld + c % cb. */
+typedef struct {
+  void* ptr;
+  long long ld, cb, bstride;
+} pc_mat;
+
+PC_API const char* pc_last_error(void);
+PC_API int pc_version(void);
+/* Number of kernels this library has launched in the process (all devices). */
+PC_API unsigned long long pc_launch_count(void);
+/* 1 when the tcgen05/TMA tensor-core path is compiled in and the device is sm_100. */
+PC_API int pc_has_tcgen05(void);
+
+/* --- conv: replaces kernels.conv2d_forward (kernels.py:104-116) ------------- */
+/* y[pixel][n] = bias[n] + sum_{i,j,c} x[b, oy*s+i-p, ox*s+j-p, c] * w[n][i][j][c]
+ * (PC_RELU: y = max(y, 0)). x may be channel-blocked; y is plain NHWC. */
+PC_API int pc_conv2d_forward(const pc_conv_geom* g, const void* x, const void* w, const float* bias,
+                      void* y, int prec, int flags, pc_stream_t stream);
+
+/* --- conv: replaces kernels.conv2d_backward (kernels.py:119-152) ------------ */
+/* PC_WANT_DX: gx (same blocked layout as x) = conv-transpose of gy;
+ *   PC_MASK_DX: gx = 0 where mask <= 0 (fused ReLU backward of the producer;
+ *   mask has gx's layout, normally the ReLU output that fed this conv).
+ * PC_WANT_DW: gw[n][i][j][c] (float) and gb[n] (float) = weight/bias grads.
+ * workspace: pc_conv2d_backward_workspace() bytes (split-K partials). */
+PC_API size_t pc_conv2d_backward_workspace(const pc_conv_geom* g, int prec);
+PC_API int pc_conv2d_backward(const pc_conv_geom* g, const void* x, const void* w, const void* gy,
+                       void* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                       void* workspace, size_t workspace_bytes, pc_stream_t stream);
+
+/* --- fc: replaces kernels.fc_forward / fc_backward (kernels.py:160-182) ----- */
+/* y[b][u] = bias[u] + sum_d x(b, d) * w[u][d]; x is a pc_mat view (blocked
+ * when the FC consumes a cross concatenation). y is plain [B][U]. */
+PC_API int pc_fc_forward(int B, int D, int U, const pc_mat* x, const void* w, const float* bias,
+                  void* y, int prec, int flags, pc_stream_t stream);
+/* gx(b, d) = sum_u gy[b][u] w[u][d] (written through the pc_mat view, masked
+ * by `mask` viewed identically when PC_MASK_DX); gw[u][d] = sum_b gy[b][u] x(b, d);
+ * gb[u] = sum_b gy[b][u]. */
+PC_API size_t pc_fc_backward_workspace(int B, int D, int U, int prec);
+PC_API int pc_fc_backward(int B, int D, int U, const pc_mat* x, const void* w, const void* gy,
+                   const pc_mat* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                   void* workspace, size_t workspace_bytes, pc_stream_t stream);
+
+/* --- relu: kernels.relu_forward / relu_backward (kernels.py:190-197) -------- */
+PC_API int pc_relu_forward(long long n, const void* x, void* y, int prec, pc_stream_t stream);
+/* gx = g where x > 0 else 0 (x may be the ReLU input or output: same mask). */
+PC_API int pc_relu_backward(long long n, const void* x, const void* g, void* gx, int prec,
+                     pc_stream_t stream);
+
+/* --- maxpool: kernels.maxpool_forward / backward (kernels.py:200-244) ------- */
+/* NHWC; argmax = local window index i*k+j (row-major, first max wins, NaN wins)
+ * stored as uint8. */
+PC_API int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, const void* x, void* y,
+                       uint8_t* argmax, int prec, pc_stream_t stream);
+/* Deterministic gather form of the np.add.at scatter: each input element sums
+ * the windows whose argmax hits it in ascending (oy, ox) order. If mask != NULL
+ * the result is zeroed where mask <= 0 (fused ReLU backward). */
+PC_API int pc_maxpool_backward(int B, int H, int W, int C, int k, int s, const void* gy,
+                        const uint8_t* argmax, const void* mask, void* gx, int prec,
+                        pc_stream_t stream);
+
+/* --- softmax cross-entropy: kernels.softmax_xent_scaled (kernels.py:252-276) */
+/* grad[b][k] = (softmax - onehot) * scale (stored in prec); row_loss[b] =
+ * -scale * log softmax[b][label_b] (double). Out-of-range labels set *bad_label
+ * to 1 (device int; checked at the loss read-back). */
+PC_API int pc_softmax_xent(int B, int K, const void* logits, const int32_t* labels, double scale,
+                    void* grad, double* row_loss, int* bad_label, int prec, pc_stream_t stream);
+/* out[0] = sum_i v[i] in ascending order (one block; deterministic). */
+PC_API int pc_sum_f64(int n, const double* v, double* out, pc_stream_t stream);
+
+/* --- SGD: kernels.sgd_step (kernels.py:319-341), multi-tensor, one launch -- */
+typedef struct {
+  float* p;          /* fp32 master parameters (updated in place) */
+  float* v;          /* fp32 velocity (updated in place) */
+  const float* g;    /* fp32 gradient */
+  void* p_lowp;      /* optional bf16 shadow copy rewritten from p (NULL: none) */
+  long long n;
+} pc_sgd_tensor;
+/* `table` is a DEVICE array of n_tensors descriptors. */
+PC_API int pc_sgd_step(int n_tensors, const pc_sgd_tensor* table, long long max_numel, float lr,
+                float momentum, float weight_decay, pc_stream_t stream);
+
+/* --- layout / reduction helpers used by the engine -------------------------- */
+/* NCHW float (reference layout) -> NHWC prec with C padded to Cp (zeros). */
+PC_API int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* src, void* dst, int prec,
+                    pc_stream_t stream);
+/* dst[i] = sum_{j<k} src[j][i] in ascending j, accumulated in fp32 and rounded
+ * once to prec (k buffers; `src` is a DEVICE array of k device pointers). */
+PC_API int pc_sum_buffers(int k, long long n, const void* const* src, void* dst, int prec,
+                          pc_stream_t stream);
+/* float <-> prec conversions of a flat buffer. */
+PC_API int pc_cast(long long n, const void* src, int src_prec, void* dst, int dst_prec,
+            pc_stream_t stream);
+/* dst = src * alpha (prec storage), used for the shared-head 1/m contribution. */
+PC_API int pc_scale(long long n, const void* src, void* dst, float alpha, int prec, pc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PC_B200_H */

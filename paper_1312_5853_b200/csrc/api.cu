@@ -1,0 +1,226 @@
+// extern "C" entry points for the contractions (conv / FC) and the shared
+// reductions; dispatches PC_FP32 to the exact-fp32 SIMT path and PC_BF16 to
+// the tcgen05 tensor-core path (umma_gemm.cu).
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "gemm_ops.cuh"
+#include "umma.cuh"
+
+namespace pc {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+__global__ void reduce_partials_k(const float* __restrict__ ws, int splits, long long n,
+                                  float* __restrict__ out) {
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n;
+       i += (long long)gridDim.x * blockDim.x * 4) {
+    if (i + 4 <= n && (n & 3) == 0) {
+      float4 a = __ldg(reinterpret_cast<const float4*>(ws + i));
+      for (int z = 1; z < splits; ++z) {
+        float4 b = __ldg(reinterpret_cast<const float4*>(ws + z * n + i));
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      *reinterpret_cast<float4*>(out + i) = a;
+    } else {
+      for (long long j = i; j < n && j < i + 4; ++j) {
+        float a = ws[j];
+        for (int z = 1; z < splits; ++z) a += ws[z * n + j];
+        out[j] = a;
+      }
+    }
+  }
+}
+
+int reduce_partials(const float* ws, int splits, long long n, float* out, cudaStream_t st) {
+  if (n == 0) return PC_OK;
+  long long g = (n / 4 + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  if (g < 1) g = 1;
+  reduce_partials_k<<<(int)g, 256, 0, st>>>(ws, splits, n, out);
+  PC_CUDA_CHECK_LAUNCH("reduce_partials");
+  return PC_OK;
+}
+
+// Bias gradients: pass 1 sums rows [r*RB, (r+1)*RB) per column block; pass 2
+// sums the row-block partials in ascending order. Fixed order => deterministic.
+constexpr int CS_RB = 512;
+long long colsum_ws(long long P, int N) { return ((P + CS_RB - 1) / CS_RB) * (long long)N; }
+
+template <typename T>
+__global__ void colsum1_k(const T* __restrict__ g, long long P, int N, float* __restrict__ part) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  long long r0 = (long long)blockIdx.y * CS_RB, r1 = min(P, r0 + CS_RB);
+  float acc = 0.f;
+  for (long long r = r0; r < r1; ++r) acc += ld(g + r * N + c);
+  part[(long long)blockIdx.y * N + c] = acc;
+}
+__global__ void colsum2_k(const float* __restrict__ part, int R, int N, float* __restrict__ out) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float acc = 0.f;
+  for (int r = 0; r < R; ++r) acc += part[(long long)r * N + c];
+  out[c] = acc;
+}
+
+int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, cudaStream_t st) {
+  if (N == 0) return PC_OK;
+  int R = (int)((P + CS_RB - 1) / CS_RB);
+  if (R == 0) {
+    cudaMemsetAsync(out, 0, sizeof(float) * N, st);
+    return PC_OK;
+  }
+  dim3 g1((N + 127) / 128, R);
+  if (prec == PC_FP32)
+    colsum1_k<float><<<g1, 128, 0, st>>>(static_cast<const float*>(g), P, N, ws);
+  else
+    colsum1_k<__nv_bfloat16><<<g1, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(g), P, N, ws);
+  colsum2_k<<<(N + 127) / 128, 128, 0, st>>>(ws, R, N, out);
+  count_launches(1);
+  PC_CUDA_CHECK_LAUNCH("colsum");
+  return PC_OK;
+}
+
+static int check_geom(const pc_conv_geom* g) {
+  PC_REQUIRE(g != nullptr, PC_EVALUE, "null conv geometry");
+  PC_REQUIRE(g->B >= 0 && g->H > 0 && g->W > 0 && g->C > 0 && g->N > 0 && g->k > 0 && g->stride > 0 &&
+                 g->pad >= 0, PC_ESHAPE, "conv: non-positive extent");
+  int sh = g->H + 2 * g->pad - g->k, sw = g->W + 2 * g->pad - g->k;
+  PC_REQUIRE(sh >= 0 && sw >= 0 && sh % g->stride == 0 && sw % g->stride == 0, PC_EVALUE,
+             "conv geometry does not produce an integer output extent: input %dx%d, kernel %d, "
+             "stride %d, pad %d", g->H, g->W, g->k, g->stride, g->pad);
+  PC_REQUIRE(g->Ho == sh / g->stride + 1 && g->Wo == sw / g->stride + 1, PC_ESHAPE,
+             "conv: output extents %dx%d do not match geometry", g->Ho, g->Wo);
+  PC_REQUIRE(g->cs > 0 && g->C % g->cs == 0, PC_ESHAPE, "conv: channel block %d does not divide %d",
+             g->cs, g->C);
+  PC_REQUIRE(g->k * g->k <= 255, PC_EVALUE, "conv: kernel too large");
+  return PC_OK;
+}
+
+static int check_prec(int prec) {
+  PC_REQUIRE(prec == PC_FP32 || prec == PC_BF16, PC_EVALUE, "unknown precision %d", prec);
+  return PC_OK;
+}
+
+}  // namespace pc
+
+using namespace pc;
+
+extern "C" const char* pc_last_error(void) { return g_err.c_str(); }
+extern "C" int pc_version(void) { return 1; }
+extern "C" unsigned long long pc_launch_count(void) { return g_launches.load(); }
+extern "C" int pc_has_tcgen05(void) { return umma_available() ? 1 : 0; }
+
+extern "C" int pc_conv2d_forward(const pc_conv_geom* g, const void* x, const void* w, const float* bias,
+                                 void* y, int prec, int flags, pc_stream_t st) {
+  int rc = check_geom(g);
+  if (rc || (rc = check_prec(prec))) return rc;
+  if (g->B == 0) return PC_OK;
+  if (prec == PC_BF16) return umma_conv_forward(*g, x, w, bias, y, flags, S(st));
+  return simt_conv_forward(*g, x, w, bias, y, prec, flags, S(st));
+}
+
+extern "C" size_t pc_conv2d_backward_workspace(const pc_conv_geom* g, int prec) {
+  if (check_geom(g)) return 0;
+  long long P = (long long)g->B * g->Ho * g->Wo;
+  long long MN = (long long)g->N * g->k * g->k * g->C;
+  long long splits = prec == PC_BF16 ? umma_wgrad_splits(*g) : simt_splits(g->N, g->k * g->k * g->C, P);
+  long long floats = (splits > 1 ? splits * MN : 0) + colsum_ws(P, g->N);
+  return (size_t)floats * sizeof(float) + umma_conv_extra_ws(*g, prec);
+}
+
+extern "C" int pc_conv2d_backward(const pc_conv_geom* g, const void* x, const void* w, const void* gy,
+                                  void* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                                  void* workspace, size_t ws_bytes, pc_stream_t st) {
+  int rc = check_geom(g);
+  if (rc || (rc = check_prec(prec))) return rc;
+  size_t need = pc_conv2d_backward_workspace(g, prec);
+  PC_REQUIRE(!(flags & PC_WANT_DW) || ws_bytes >= need, PC_EVALUE,
+             "conv2d_backward: workspace %zu B < required %zu B", ws_bytes, need);
+  long long P = (long long)g->B * g->Ho * g->Wo;
+  if (flags & PC_WANT_DX) {
+    if (g->B == 0) return PC_OK;
+    const void* mk = (flags & PC_MASK_DX) ? mask : nullptr;
+    rc = prec == PC_BF16 ? umma_conv_dgrad(*g, w, gy, gx, mk, S(st), workspace, ws_bytes)
+                         : simt_conv_dgrad(*g, w, gy, gx, mk, S(st), prec);
+    if (rc) return rc;
+  }
+  if (flags & PC_WANT_DW) {
+    float* ws = static_cast<float*>(workspace);
+    if (g->B == 0) {
+      cudaMemsetAsync(gw, 0, sizeof(float) * g->N * g->k * g->k * g->C, S(st));
+      cudaMemsetAsync(gb, 0, sizeof(float) * g->N, S(st));
+      return PC_OK;
+    }
+    rc = colsum(gy, P, g->N, prec, gb, ws, S(st));
+    if (rc) return rc;
+    float* part = ws + colsum_ws(P, g->N);
+    if (prec == PC_BF16) {
+      rc = umma_conv_wgrad(*g, x, gy, gw, part, S(st));
+    } else {
+      rc = simt_conv_wgrad(*g, x, gy, gw, part, simt_splits(g->N, g->k * g->k * g->C, P), S(st), prec);
+    }
+    if (rc) return rc;
+  }
+  return PC_OK;
+}
+
+static int check_mat(const pc_mat* m, const char* what) {
+  PC_REQUIRE(m && m->ptr && m->ld > 0 && m->cb > 0, PC_EVALUE, "%s: bad matrix view", what);
+  return PC_OK;
+}
+
+extern "C" int pc_fc_forward(int B, int D, int U, const pc_mat* x, const void* w, const float* bias,
+                             void* y, int prec, int flags, pc_stream_t st) {
+  int rc = check_prec(prec);
+  if (rc) return rc;
+  PC_REQUIRE(B >= 0 && D > 0 && U > 0, PC_ESHAPE, "fc: bad extents B=%d D=%d U=%d", B, D, U);
+  if (B == 0) return PC_OK;
+  if ((rc = check_mat(x, "fc_forward x"))) return rc;
+  if (prec == PC_BF16) return umma_fc_forward(B, D, U, *x, w, bias, y, flags, S(st));
+  return simt_fc_forward(B, D, U, *x, w, bias, y, prec, flags, S(st));
+}
+
+extern "C" size_t pc_fc_backward_workspace(int B, int D, int U, int prec) {
+  return (size_t)colsum_ws(B, U) * sizeof(float) + umma_fc_extra_ws(B, D, U, prec);
+}
+
+extern "C" int pc_fc_backward(int B, int D, int U, const pc_mat* x, const void* w, const void* gy,
+                              const pc_mat* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                              void* workspace, size_t ws_bytes, pc_stream_t st) {
+  int rc = check_prec(prec);
+  if (rc) return rc;
+  PC_REQUIRE(B >= 0 && D > 0 && U > 0, PC_ESHAPE, "fc: bad extents B=%d D=%d U=%d", B, D, U);
+  size_t need = pc_fc_backward_workspace(B, D, U, prec);
+  PC_REQUIRE(ws_bytes >= need, PC_EVALUE, "fc_backward: workspace %zu B < required %zu B", ws_bytes, need);
+  if (flags & PC_WANT_DX) {
+    if ((rc = check_mat(gx, "fc_backward gx"))) return rc;
+    if (B > 0) {
+      const void* mk = (flags & PC_MASK_DX) ? mask : nullptr;
+      rc = prec == PC_BF16 ? umma_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st))
+                           : simt_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st), prec);
+      if (rc) return rc;
+    }
+  }
+  if (flags & PC_WANT_DW) {
+    if ((rc = check_mat(x, "fc_backward x"))) return rc;
+    if (B == 0) {
+      cudaMemsetAsync(gw, 0, sizeof(float) * (size_t)U * D, S(st));
+      cudaMemsetAsync(gb, 0, sizeof(float) * U, S(st));
+      return PC_OK;
+    }
+    float* ws = static_cast<float*>(workspace);
+    rc = colsum(gy, B, U, prec, gb, ws, S(st));
+    if (rc) return rc;
+    rc = prec == PC_BF16 ? umma_fc_wgrad(B, D, U, *x, gy, gw, ws + colsum_ws(B, U), S(st))
+                         : simt_fc_wgrad(B, D, U, *x, gy, gw, S(st), prec);
+    if (rc) return rc;
+  }
+  return PC_OK;
+}

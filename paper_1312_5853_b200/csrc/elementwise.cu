@@ -1,0 +1,457 @@
+// Bandwidth-bound layers of the step: ReLU, max-pool (u8 argmax, gather
+// backward), softmax cross-entropy, multi-tensor momentum SGD and the layout
+// helpers. Every kernel moves 8 elements (16 B of bf16 / 32 B of fp32) per
+// thread where the extents allow, so loads and stores are 128-bit.
+#include "common.cuh"
+
+namespace pc {
+
+// 8-element vector load/store ------------------------------------------------
+template <typename T> struct Vec8;
+template <> struct Vec8<float> {
+  static __device__ __forceinline__ void load(const float* p, float* v) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float* v) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+template <> struct Vec8<__nv_bfloat16> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float* v) {
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x; v[2 * i + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float* v) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+
+static inline int grid_for(long long work, int block) {
+  long long g = (work + block - 1) / block;
+  return (int)(g < 1 ? 1 : (g > (1LL << 30) ? (1LL << 30) : g));
+}
+
+// ReLU -------------------------------------------------------------------------
+template <typename T>
+__global__ void relu_fwd_k(long long n, const T* __restrict__ x, T* __restrict__ y) {
+  long long i8 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8;
+  if (i8 + 8 <= n && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 31) == 0) {
+    float v[8];
+    Vec8<T>::load(x + i8, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = v[j] > 0.f ? v[j] : (v[j] != v[j] ? v[j] : 0.f);
+    Vec8<T>::store(y + i8, v);
+  } else {
+    for (long long i = i8; i < n && i < i8 + 8; ++i) {
+      float a = ld(x + i);
+      y[i] = cvt<T>(a > 0.f ? a : (a != a ? a : 0.f));
+    }
+  }
+}
+
+template <typename T>
+__global__ void relu_bwd_k(long long n, const T* __restrict__ x, const T* __restrict__ g,
+                           T* __restrict__ gx) {
+  long long i8 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 8;
+  if (i8 + 8 <= n &&
+      ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(gx)) & 31) == 0) {
+    float a[8], b[8];
+    Vec8<T>::load(x + i8, a);
+    Vec8<T>::load(g + i8, b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = a[j] > 0.f ? b[j] : 0.f;
+    Vec8<T>::store(gx + i8, b);
+  } else {
+    for (long long i = i8; i < n && i < i8 + 8; ++i) gx[i] = cvt<T>(ld(x + i) > 0.f ? ld(g + i) : 0.f);
+  }
+}
+
+// Max-pool ---------------------------------------------------------------------
+// One thread per (b, oy, ox, 8-channel group) when C % 8 == 0, else per channel.
+template <typename T, int V>
+__global__ void maxpool_fwd_k(int B, int H, int W, int C, int k, int s, int Ho, int Wo,
+                              const T* __restrict__ x, T* __restrict__ y, uint8_t* __restrict__ arg) {
+  long long cg = C / V;
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long total = (long long)B * Ho * Wo * cg;
+  if (t >= total) return;
+  int c0 = (int)(t % cg) * V;
+  long long pix = t / cg;
+  int ox = (int)(pix % Wo);
+  int oy = (int)((pix / Wo) % Ho);
+  int b = (int)(pix / ((long long)Wo * Ho));
+  float best[V];
+  int bi[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) { best[v] = 0.f; bi[v] = -1; }
+  for (int i = 0; i < k; ++i) {
+    const T* row = x + (((long long)b * H + oy * s + i) * W + ox * s) * C + c0;
+    for (int j = 0; j < k; ++j) {
+      float val[V];
+      if constexpr (V == 8) {
+        Vec8<T>::load(row + (long long)j * C, val);
+      } else {
+        val[0] = ld(row + (long long)j * C);
+      }
+      int idx = i * k + j;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        bool nan_v = val[v] != val[v], nan_b = best[v] != best[v];
+        // np.argmax: first maximum wins, the first NaN wins over everything
+        if (bi[v] < 0 || (!nan_b && (val[v] > best[v] || nan_v))) { best[v] = val[v]; bi[v] = idx; }
+      }
+    }
+  }
+  long long o = pix * C + c0;
+  if constexpr (V == 8) {
+    Vec8<T>::store(y + o, best);
+    uint2 packed;
+    uint8_t* pb = reinterpret_cast<uint8_t*>(&packed);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) pb[v] = (uint8_t)bi[v];
+    *reinterpret_cast<uint2*>(arg + o) = packed;
+  } else {
+    y[o] = cvt<T>(best[0]);
+    arg[o] = (uint8_t)bi[0];
+  }
+}
+
+template <typename T, int V>
+__global__ void maxpool_bwd_k(int B, int H, int W, int C, int k, int s, int Ho, int Wo,
+                              const T* __restrict__ gy, const uint8_t* __restrict__ arg,
+                              const T* __restrict__ mask, T* __restrict__ gx) {
+  long long cg = C / V;
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long total = (long long)B * H * W * cg;
+  if (t >= total) return;
+  int c0 = (int)(t % cg) * V;
+  long long pix = t / cg;
+  int x = (int)(pix % W);
+  int y = (int)((pix / W) % H);
+  int b = (int)(pix / ((long long)W * H));
+  // windows oy with oy*s <= y <= oy*s + k - 1
+  int oy_lo = y - k + 1 <= 0 ? 0 : (y - k + 1 + s - 1) / s;
+  int oy_hi = min(y / s, Ho - 1);
+  int ox_lo = x - k + 1 <= 0 ? 0 : (x - k + 1 + s - 1) / s;
+  int ox_hi = min(x / s, Wo - 1);
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  for (int oy = oy_lo; oy <= oy_hi; ++oy) {
+    for (int ox = ox_lo; ox <= ox_hi; ++ox) {
+      int want = (y - oy * s) * k + (x - ox * s);
+      long long o = (((long long)b * Ho + oy) * Wo + ox) * C + c0;
+      if constexpr (V == 8) {
+        uint2 packed = __ldg(reinterpret_cast<const uint2*>(arg + o));
+        const uint8_t* pb = reinterpret_cast<const uint8_t*>(&packed);
+        float g[8];
+        Vec8<T>::load(gy + o, g);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[v] += (pb[v] == want) ? g[v] : 0.f;
+      } else {
+        if (arg[o] == want) acc[0] += ld(gy + o);
+      }
+    }
+  }
+  long long o = pix * C + c0;
+  if (mask) {
+    float mk[V];
+    if constexpr (V == 8) Vec8<T>::load(mask + o, mk); else mk[0] = ld(mask + o);
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = mk[v] > 0.f ? acc[v] : 0.f;
+  }
+  if constexpr (V == 8) Vec8<T>::store(gx + o, acc); else gx[o] = cvt<T>(acc[0]);
+}
+
+// Softmax cross-entropy: one CTA per row ------------------------------------------
+template <int NT>
+__device__ __forceinline__ float block_reduce(float v, bool is_max, float* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, w) : v + w;
+  }
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  v = sh[0];
+  for (int i = 1; i < NT / 32; ++i) v = is_max ? fmaxf(v, sh[i]) : v + sh[i];
+  return v;
+}
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) softmax_xent_k(int K, const T* __restrict__ logits,
+                                                     const int32_t* __restrict__ labels, double scale,
+                                                     T* __restrict__ grad, double* __restrict__ row_loss,
+                                                     int* __restrict__ bad) {
+  __shared__ float sh[NT / 32];
+  int row = blockIdx.x;
+  const T* z = logits + (long long)row * K;
+  float mx = -INFINITY;
+  for (int i = threadIdx.x; i < K; i += NT) mx = fmaxf(mx, ld(z + i));
+  mx = block_reduce<NT>(mx, true, sh);
+  float sum = 0.f;
+  for (int i = threadIdx.x; i < K; i += NT) sum += expf(ld(z + i) - mx);
+  sum = block_reduce<NT>(sum, false, sh);
+  int lab = labels[row];
+  bool ok = lab >= 0 && lab < K;
+  float inv = 1.f / sum, sc = (float)scale;
+  for (int i = threadIdx.x; i < K; i += NT) {
+    float p = expf(ld(z + i) - mx) * inv;
+    grad[(long long)row * K + i] = cvt<T>((p - (i == lab ? 1.f : 0.f)) * sc);
+  }
+  if (threadIdx.x == 0) {
+    if (!ok) { *bad = 1; row_loss[row] = 0.0; return; }
+    double logp = (double)(ld(z + lab) - mx) - log((double)sum);
+    row_loss[row] = -logp * scale;
+  }
+}
+
+__global__ void sum_f64_k(int n, const double* __restrict__ v, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += v[i];
+    out[0] = acc;
+  }
+}
+
+// Multi-tensor momentum SGD: blockIdx.y = tensor --------------------------------------
+__global__ void sgd_k(const pc_sgd_tensor* __restrict__ tab, float lr, float mom, float wd) {
+  pc_sgd_tensor t = tab[blockIdx.y];
+  long long stride = (long long)gridDim.x * blockDim.x * 4;
+  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < t.n; i += stride) {
+    if (i + 4 <= t.n && ((reinterpret_cast<uintptr_t>(t.p) | reinterpret_cast<uintptr_t>(t.v) |
+                          reinterpret_cast<uintptr_t>(t.g)) & 15) == 0) {
+      float4 p = *reinterpret_cast<float4*>(t.p + i);
+      float4 v = *reinterpret_cast<float4*>(t.v + i);
+      float4 g = __ldg(reinterpret_cast<const float4*>(t.g + i));
+      v.x = mom * v.x - lr * (g.x + wd * p.x);
+      v.y = mom * v.y - lr * (g.y + wd * p.y);
+      v.z = mom * v.z - lr * (g.z + wd * p.z);
+      v.w = mom * v.w - lr * (g.w + wd * p.w);
+      p.x += v.x; p.y += v.y; p.z += v.z; p.w += v.w;
+      *reinterpret_cast<float4*>(t.v + i) = v;
+      *reinterpret_cast<float4*>(t.p + i) = p;
+      if (t.p_lowp) {
+        __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(t.p_lowp) + i);
+        q[0] = __floats2bfloat162_rn(p.x, p.y);
+        q[1] = __floats2bfloat162_rn(p.z, p.w);
+      }
+    } else {
+      for (long long j = i; j < t.n && j < i + 4; ++j) {
+        float p = t.p[j], v = t.v[j], g = t.g[j];
+        v = mom * v - lr * (g + wd * p);
+        p += v;
+        t.v[j] = v;
+        t.p[j] = p;
+        if (t.p_lowp) static_cast<__nv_bfloat16*>(t.p_lowp)[j] = __float2bfloat16_rn(p);
+      }
+    }
+  }
+}
+
+// Layout helpers ---------------------------------------------------------------------
+template <typename T>
+__global__ void nchw_to_nhwc_k(int B, int C, int H, int W, int Cp, const float* __restrict__ src,
+                               T* __restrict__ dst) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long total = (long long)B * H * W * Cp;
+  if (t >= total) return;
+  int c = (int)(t % Cp);
+  long long pix = t / Cp;
+  int x = (int)(pix % W);
+  int y = (int)((pix / W) % H);
+  int b = (int)(pix / ((long long)W * H));
+  float v = c < C ? src[(((long long)b * C + c) * H + y) * W + x] : 0.f;
+  dst[t] = cvt<T>(v);
+}
+
+template <typename T>
+__global__ void sum_buffers_k(int k, long long n, const void* const* __restrict__ src,
+                              T* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float acc = ld(static_cast<const T*>(src[0]) + i);
+    for (int j = 1; j < k; ++j) acc += ld(static_cast<const T*>(src[j]) + i);
+    dst[i] = cvt<T>(acc);
+  }
+}
+
+template <typename S, typename D>
+__global__ void cast_k(long long n, const S* __restrict__ src, D* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = cvt<D>(ld(src + i));
+}
+
+template <typename T>
+__global__ void scale_k(long long n, const T* __restrict__ src, T* __restrict__ dst, float a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = cvt<T>(ld(src + i) * a);
+}
+
+}  // namespace pc
+
+using namespace pc;
+
+#define DISPATCH_PREC(prec, T, ...)                                    \
+  do {                                                                 \
+    if ((prec) == PC_FP32) { using T = float; __VA_ARGS__; }           \
+    else if ((prec) == PC_BF16) { using T = __nv_bfloat16; __VA_ARGS__; } \
+    else { pc::set_error("unknown precision"); return PC_EVALUE; }     \
+  } while (0)
+
+extern "C" int pc_relu_forward(long long n, const void* x, void* y, int prec, pc_stream_t st) {
+  PC_REQUIRE(n >= 0, PC_ESHAPE, "relu: negative size");
+  if (n == 0) return PC_OK;
+  DISPATCH_PREC(prec, T, relu_fwd_k<T><<<grid_for((n + 7) / 8, 256), 256, 0, S(st)>>>(
+      n, static_cast<const T*>(x), static_cast<T*>(y)));
+  PC_CUDA_CHECK_LAUNCH("relu_forward");
+  return PC_OK;
+}
+
+extern "C" int pc_relu_backward(long long n, const void* x, const void* g, void* gx, int prec,
+                                pc_stream_t st) {
+  PC_REQUIRE(n >= 0, PC_ESHAPE, "relu: negative size");
+  if (n == 0) return PC_OK;
+  DISPATCH_PREC(prec, T, relu_bwd_k<T><<<grid_for((n + 7) / 8, 256), 256, 0, S(st)>>>(
+      n, static_cast<const T*>(x), static_cast<const T*>(g), static_cast<T*>(gx)));
+  PC_CUDA_CHECK_LAUNCH("relu_backward");
+  return PC_OK;
+}
+
+static int pool_geom(int H, int W, int k, int s, int* Ho, int* Wo) {
+  PC_REQUIRE(k >= 1 && s >= 1 && k <= 16, PC_EVALUE, "maxpool: bad kernel/stride %d/%d", k, s);
+  PC_REQUIRE(H >= k && W >= k && (H - k) % s == 0 && (W - k) % s == 0, PC_EVALUE,
+             "maxpool geometry does not tile: %dx%d k%d s%d", H, W, k, s);
+  *Ho = (H - k) / s + 1;
+  *Wo = (W - k) / s + 1;
+  return PC_OK;
+}
+
+static bool aligned(const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+extern "C" int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, const void* x, void* y,
+                                  uint8_t* argmax, int prec, pc_stream_t st) {
+  int Ho, Wo, rc = pool_geom(H, W, k, s, &Ho, &Wo);
+  if (rc) return rc;
+  if ((long long)B * C == 0) return PC_OK;
+  bool vec = C % 8 == 0 && aligned(x, 32) && aligned(y, 32) && aligned(argmax, 8);
+  long long work = (long long)B * Ho * Wo * (vec ? C / 8 : C);
+  DISPATCH_PREC(prec, T, {
+    if (vec)
+      maxpool_fwd_k<T, 8><<<grid_for(work, 256), 256, 0, S(st)>>>(
+          B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(x), static_cast<T*>(y), argmax);
+    else
+      maxpool_fwd_k<T, 1><<<grid_for(work, 256), 256, 0, S(st)>>>(
+          B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(x), static_cast<T*>(y), argmax);
+  });
+  PC_CUDA_CHECK_LAUNCH("maxpool_forward");
+  return PC_OK;
+}
+
+extern "C" int pc_maxpool_backward(int B, int H, int W, int C, int k, int s, const void* gy,
+                                   const uint8_t* argmax, const void* mask, void* gx, int prec,
+                                   pc_stream_t st) {
+  int Ho, Wo, rc = pool_geom(H, W, k, s, &Ho, &Wo);
+  if (rc) return rc;
+  if ((long long)B * C == 0) return PC_OK;
+  bool vec = C % 8 == 0 && aligned(gy, 32) && aligned(gx, 32) && aligned(argmax, 8) &&
+             (!mask || aligned(mask, 32));
+  long long work = (long long)B * H * W * (vec ? C / 8 : C);
+  DISPATCH_PREC(prec, T, {
+    if (vec)
+      maxpool_bwd_k<T, 8><<<grid_for(work, 256), 256, 0, S(st)>>>(
+          B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(gy), argmax,
+          static_cast<const T*>(mask), static_cast<T*>(gx));
+    else
+      maxpool_bwd_k<T, 1><<<grid_for(work, 256), 256, 0, S(st)>>>(
+          B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(gy), argmax,
+          static_cast<const T*>(mask), static_cast<T*>(gx));
+  });
+  PC_CUDA_CHECK_LAUNCH("maxpool_backward");
+  return PC_OK;
+}
+
+extern "C" int pc_softmax_xent(int B, int K, const void* logits, const int32_t* labels, double scale,
+                               void* grad, double* row_loss, int* bad_label, int prec, pc_stream_t st) {
+  PC_REQUIRE(B >= 0 && K >= 2, PC_ESHAPE, "softmax_xent: bad extents B=%d K=%d", B, K);
+  if (B == 0) return PC_OK;
+  DISPATCH_PREC(prec, T, softmax_xent_k<T, 256><<<B, 256, 0, S(st)>>>(
+      K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label));
+  PC_CUDA_CHECK_LAUNCH("softmax_xent");
+  return PC_OK;
+}
+
+extern "C" int pc_sum_f64(int n, const double* v, double* out, pc_stream_t st) {
+  sum_f64_k<<<1, 32, 0, S(st)>>>(n, v, out);
+  PC_CUDA_CHECK_LAUNCH("sum_f64");
+  return PC_OK;
+}
+
+extern "C" int pc_sgd_step(int n_tensors, const pc_sgd_tensor* table, long long max_numel, float lr,
+                           float momentum, float weight_decay, pc_stream_t st) {
+  PC_REQUIRE(n_tensors >= 0 && n_tensors <= 65535, PC_EVALUE, "sgd: bad tensor count %d", n_tensors);
+  if (n_tensors == 0 || max_numel <= 0) return PC_OK;
+  int gx = grid_for((max_numel + 3) / 4, 256);
+  if (gx > 1184) gx = 1184;  // 8 CTAs per SM on 148 SMs; grid-stride beyond that
+  sgd_k<<<dim3(gx, n_tensors), 256, 0, S(st)>>>(table, lr, momentum, weight_decay);
+  PC_CUDA_CHECK_LAUNCH("sgd_step");
+  return PC_OK;
+}
+
+extern "C" int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* src, void* dst,
+                               int prec, pc_stream_t st) {
+  PC_REQUIRE(Cp >= C, PC_ESHAPE, "nchw_to_nhwc: Cp < C");
+  long long n = (long long)B * H * W * Cp;
+  if (n == 0) return PC_OK;
+  DISPATCH_PREC(prec, T, nchw_to_nhwc_k<T><<<grid_for(n, 256), 256, 0, S(st)>>>(
+      B, C, H, W, Cp, src, static_cast<T*>(dst)));
+  PC_CUDA_CHECK_LAUNCH("nchw_to_nhwc");
+  return PC_OK;
+}
+
+extern "C" int pc_sum_buffers(int k, long long n, const void* const* src, void* dst, int prec,
+                              pc_stream_t st) {
+  PC_REQUIRE(k >= 1, PC_EVALUE, "sum_buffers: k < 1");
+  if (n == 0) return PC_OK;
+  int g = grid_for(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  DISPATCH_PREC(prec, T, sum_buffers_k<T><<<g, 256, 0, S(st)>>>(k, n, src, static_cast<T*>(dst)));
+  PC_CUDA_CHECK_LAUNCH("sum_buffers");
+  return PC_OK;
+}
+
+extern "C" int pc_cast(long long n, const void* src, int sp, void* dst, int dp, pc_stream_t st) {
+  if (n == 0) return PC_OK;
+  int g = grid_for(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  DISPATCH_PREC(sp, TS, DISPATCH_PREC(dp, TD, cast_k<TS, TD><<<g, 256, 0, S(st)>>>(
+      n, static_cast<const TS*>(src), static_cast<TD*>(dst))));
+  PC_CUDA_CHECK_LAUNCH("cast");
+  return PC_OK;
+}
+
+extern "C" int pc_scale(long long n, const void* src, void* dst, float a, int prec, pc_stream_t st) {
+  if (n == 0) return PC_OK;
+  int g = grid_for(n, 256);
+  if (g > 148 * 16) g = 148 * 16;
+  DISPATCH_PREC(prec, T, scale_k<T><<<g, 256, 0, S(st)>>>(n, static_cast<const T*>(src),
+                                                           static_cast<T*>(dst), a));
+  PC_CUDA_CHECK_LAUNCH("scale");
+  return PC_OK;
+}

@@ -1,0 +1,379 @@
+"""Per-worker device engine: the B200 restatement of `schemes.column_fwd_bwd`
+(`pkg/src/parconv/schemes.py:342-419`) plus the worker's slice of the
+data-parallel leg and the SGD update (`schemes.py:540-558`).
+
+Layout in HBM (one worker = one column of one replica):
+  * activations NHWC in the storage precision (bf16 in production, fp32 in
+    the verification mode); a cross layer's input is a channel-blocked
+    concatenation buffer [m][B][H][W][C/m] that the column exchange fills;
+  * parameters, velocity and gradients are single flat fp32 buffers in the
+    reference's canonical order (ascending layer, weights then bias; device
+    weight layouts from ``layout.py``), so the data-parallel all-reduce is
+    one contiguous buffer and the optimizer is one launch; a flat bf16
+    shadow of the parameters feeds the tensor cores and is rewritten by the
+    same SGD launch.
+Fusions: conv/FC + ReLU forward (epilogue), ReLU backward folded into the
+consumer's data-grad epilogue (conv/FC dgrad mask) or the max-pool gather
+backward, softmax loss + gradient in one kernel.
+Every call goes through the C ABI (``_lib``); nothing here computes on the
+host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import layout
+from .errors import ValidationError
+from .netdef import FC, ColumnizedSpec, Conv, MaxPool, ReLU, SoftmaxXent
+
+ALIGN = 32  # elements; every flat-buffer slice starts 128-byte aligned in fp32
+PROFILE: list | None = None  # set to a list to record per-call CUDA events
+
+
+def torch_dtype(prec: int):
+    return torch.bfloat16 if prec == L.PC_BF16 else torch.float32
+
+
+@dataclass
+class LayerState:
+    cl: object
+    kind: str
+    inp: torch.Tensor | None = None      # input activation (concat buffer when cross)
+    in_nhwc: tuple | None = None         # (H, W, C_full) or (D,) per sample
+    in_blocks: int = 1
+    out: torch.Tensor | None = None
+    out_nhwc: tuple | None = None
+    argmax: torch.Tensor | None = None
+    gin: torch.Tensor | None = None      # gradient w.r.t. inp (same layout)
+    gout: torch.Tensor | None = None     # gradient w.r.t. out
+    rs: torch.Tensor | None = None       # cross layers: reduce-scatter target (own slice)
+    relu_fused_fwd: bool = False         # ReLU computed by the producer's epilogue
+    relu_after: bool = False             # conv/FC: next layer is a fused ReLU
+    skip_bwd: bool = False               # ReLU: backward folded into consumer
+    mask_dx: bool = False                # consumer applies the ReLU mask (= inp > 0)
+    w_off: int = -1
+    b_off: int = -1
+    w_shape: tuple = ()
+    cp: int = 0                          # padded input channels (conv)
+    perm: np.ndarray | None = None       # FC row permutation (reference <-> device)
+    geom: object = None
+    row_loss: torch.Tensor | None = None
+
+
+class ColumnEngine:
+    """One worker's buffers and step program on one device."""
+
+    def __init__(self, cs: ColumnizedSpec, wid: int, replica: int, column: int, shard: int,
+                 prec: int, device: torch.device, hyper: tuple):
+        self.cs, self.m = cs, cs.columns
+        self.wid, self.replica, self.column = wid, replica, column
+        self.B, self.prec, self.device = shard, prec, device
+        self.lr, self.mom, self.wd = (float(h) for h in hyper)
+        self.dtype = torch_dtype(prec)
+        self.lib = L.lib()
+        self.layers: list[LayerState] = []
+        self._build_activations()
+        self._build_params()
+        self._build_grads()
+        self.labels = torch.zeros(max(shard, 1), dtype=torch.int32, device=device)
+        self.bad_label = torch.zeros(1, dtype=torch.int32, device=device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+
+    # ------------------------------------------------------------------ setup
+    def _new(self, n, dtype=None):
+        return torch.empty(max(int(n), 1), dtype=dtype or self.dtype, device=self.device)
+
+    def _build_activations(self):
+        cs, B, m = self.cs, self.B, self.m
+        c, h, w = cs.base.input_shape
+        first = cs.col_layers[0]
+        self.in_c = c
+        self.in_cp = c
+        if self.prec == L.PC_BF16 and isinstance(first.layer, Conv) and c % 8:
+            self.in_cp = (c + 7) // 8 * 8
+        self.x = self._new(B * h * w * self.in_cp)
+        prev_out, prev_shape = self.x, (h, w, self.in_cp)
+        n = len(cs.col_layers)
+        for i, cl in enumerate(cs.col_layers):
+            layer = cl.layer
+            kind = {Conv: "conv", FC: "fc", ReLU: "relu", MaxPool: "pool", SoftmaxXent: "softmax"}[type(layer)]
+            st = LayerState(cl, kind)
+            per = math.prod(prev_shape)
+            if cl.cross:
+                st.inp = self._new(m * B * per)
+                st.in_blocks = m
+                st.in_nhwc = (prev_shape[:-1] + (prev_shape[-1] * m,)) if len(prev_shape) == 3 \
+                    else (prev_shape[0] * m,)
+                st.rs = self._new(B * per)
+            else:
+                st.inp, st.in_nhwc = prev_out, prev_shape
+            if kind == "conv":
+                hh, ww, cc = st.in_nhwc
+                ho = (hh + 2 * layer.pad - layer.kernel) // layer.stride + 1
+                wo = (ww + 2 * layer.pad - layer.kernel) // layer.stride + 1
+                nout = cl.out_shape[0]
+                if cc % 8 and self.prec == L.PC_BF16:
+                    raise ValidationError(f"layer {cl.index}: bf16 conv needs C % 8 == 0 (C={cc})")
+                st.cp = cc
+                cs_blk = cc // st.in_blocks
+                st.geom = L.ConvGeom(B, hh, ww, cc, nout, layer.kernel, layer.stride, layer.pad, ho, wo,
+                                     cs_blk, B * hh * ww * cs_blk)
+                st.out_nhwc = (ho, wo, nout)
+                st.out = self._new(B * ho * wo * nout)
+            elif kind == "fc":
+                st.out_nhwc = (cl.out_shape[0],)
+                st.out = self._new(B * cl.out_shape[0])
+                st.perm = layout.fc_row_perm(cl.in_shape, m, cl.cross)
+            elif kind == "relu":
+                prev = self.layers[-1] if self.layers else None
+                st.out_nhwc = st.in_nhwc
+                if prev is not None and prev.kind in ("conv", "fc") and not cl.cross:
+                    st.relu_fused_fwd = True
+                    prev.relu_after = True
+                    st.out = st.inp
+                else:
+                    st.out = self._new(B * per)
+            elif kind == "pool":
+                hh, ww, cc = st.in_nhwc
+                ho = (hh - layer.kernel) // layer.stride + 1
+                wo = (ww - layer.kernel) // layer.stride + 1
+                st.out_nhwc = (ho, wo, cc)
+                st.out = self._new(B * ho * wo * cc)
+                st.argmax = self._new(B * ho * wo * cc, torch.uint8)
+            else:
+                st.out_nhwc = (layer.classes,)
+                st.out = self._new(B * layer.classes)          # gradient of the logits
+                st.row_loss = self._new(B, torch.float64)
+            self.layers.append(st)
+            prev_out, prev_shape = st.out, st.out_nhwc
+        # backward wiring (reverse order so ReLU aliases resolve)
+        for i in range(n - 1, -1, -1):
+            st = self.layers[i]
+            nxt = self.layers[i + 1] if i + 1 < n else None
+            if nxt is not None:
+                st.gout = nxt.rs if nxt.cl.cross else nxt.gin
+            if st.kind == "relu":
+                st.skip_bwd = nxt is not None and nxt.kind in ("conv", "fc", "pool")
+            if i == 0:
+                continue
+            if st.kind == "softmax":
+                st.gin = st.out
+            elif st.kind == "relu" and st.skip_bwd:
+                st.gin = st.gout
+            else:
+                st.gin = self._new(st.inp.numel())
+        for i in range(1, n):
+            st, prv = self.layers[i], self.layers[i - 1]
+            st.mask_dx = st.kind in ("conv", "fc", "pool") and prv.kind == "relu" and prv.skip_bwd
+
+    def _build_params(self):
+        off = 0
+        for st in self.layers:
+            if st.kind not in ("conv", "fc"):
+                continue
+            st.w_shape = layout.device_weight_shape(st.cl, st.cp)
+            st.w_off = off
+            off += -(-layout.numel(st.w_shape) // ALIGN) * ALIGN
+            st.b_off = off
+            off += -(-st.cl.bias_shape[0] // ALIGN) * ALIGN
+        self.n_flat = max(off, ALIGN)
+        self.p32 = torch.zeros(self.n_flat, dtype=torch.float32, device=self.device)
+        self.v32 = torch.zeros_like(self.p32)
+        self.plow = torch.zeros(self.n_flat, dtype=torch.bfloat16, device=self.device) \
+            if self.prec == L.PC_BF16 else None
+        tab = L.SgdTensor(self.p32.data_ptr(), self.v32.data_ptr(), 0,
+                          self.plow.data_ptr() if self.plow is not None else None, self.n_flat)
+        self._sgd_host = tab
+        self._sgd_dev = torch.frombuffer(bytearray(bytes(tab)), dtype=torch.uint8).to(self.device)
+
+    def _build_grads(self):
+        self.g32 = torch.zeros(self.n_flat, dtype=torch.float32, device=self.device)
+        self.set_grad_source(self.g32)
+        ws = 0
+        for st in self.layers:
+            if st.kind == "conv":
+                ws = max(ws, self.lib.raw("pc_conv2d_backward_workspace")(C.byref(st.geom), self.prec))
+            elif st.kind == "fc":
+                d = math.prod(st.in_nhwc)
+                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B, d, st.cl.out_shape[0], self.prec))
+        self.ws_bytes = int(ws)
+        self.ws = torch.empty(max(self.ws_bytes, 16), dtype=torch.uint8, device=self.device)
+
+    def set_grad_source(self, g: torch.Tensor):
+        """Point the SGD launch at a (possibly reduced, shared) gradient buffer."""
+        self._sgd_host.g = g.data_ptr()
+        self._sgd_dev.copy_(torch.frombuffer(bytearray(bytes(self._sgd_host)), dtype=torch.uint8))
+
+    # ------------------------------------------------------ parameter transfer
+    def _w_lowp(self, st):
+        src = self.plow if self.plow is not None else self.p32
+        return src[st.w_off:].data_ptr()
+
+    def load_params(self, col_params: dict, velocity: dict | None = None):
+        """col_params: reference-layout column ParamSet (float64 numpy)."""
+        hp = np.zeros(self.n_flat, dtype=np.float32)
+        hv = np.zeros(self.n_flat, dtype=np.float32)
+        for st in self.layers:
+            if st.w_off < 0:
+                continue
+            idx = st.cl.index
+            for buf, tree in ((hp, col_params), (hv, velocity)):
+                if tree is None:
+                    continue
+                w = tree[idx]["w"]
+                dw = layout.conv_to_device(w, st.cp) if st.kind == "conv" else layout.fc_to_device(w, st.perm)
+                buf[st.w_off:st.w_off + dw.size] = dw.ravel()
+                b = np.asarray(tree[idx]["b"], dtype=np.float32)
+                buf[st.b_off:st.b_off + b.size] = b
+        self.p32.copy_(torch.from_numpy(hp))
+        self.v32.copy_(torch.from_numpy(hv))
+        if self.plow is not None:
+            self.plow.copy_(self.p32)
+
+    def _unflatten(self, flat: np.ndarray) -> dict:
+        out = {}
+        for st in self.layers:
+            if st.w_off < 0:
+                continue
+            n = layout.numel(st.w_shape)
+            wd = flat[st.w_off:st.w_off + n].reshape(st.w_shape)
+            if st.kind == "conv":
+                w = layout.conv_from_device(wd, st.cl.weight_shape[1])
+            else:
+                w = layout.fc_from_device(wd, st.perm)
+            nb = st.cl.bias_shape[0]
+            out[st.cl.index] = {"w": w, "b": flat[st.b_off:st.b_off + nb].astype(np.float64)}
+        return out
+
+    def params_host(self) -> dict:
+        return self._unflatten(self.p32.cpu().numpy())
+
+    def velocity_host(self) -> dict:
+        return self._unflatten(self.v32.cpu().numpy())
+
+    def grads_host(self, g: torch.Tensor | None = None) -> dict:
+        return self._unflatten((self.g32 if g is None else g).cpu().numpy())
+
+    def activation_host(self, i: int, which: str = "out") -> np.ndarray:
+        """Layer i's forward output (or input gradient) back in the reference's
+        NCHW float64 layout, for layer-by-layer parity tests."""
+        st = self.layers[i]
+        t = getattr(st, which)
+        shape = st.out_nhwc if which == "out" else st.in_nhwc
+        blocks = 1 if which == "out" else st.in_blocks
+        a = t[: self.B * math.prod(shape)].float().cpu().numpy().astype(np.float64)
+        if blocks > 1:
+            per = (shape[:-1] + (shape[-1] // blocks,))
+            a = a.reshape((blocks, self.B) + per)
+            a = np.concatenate(list(a), axis=-1)
+        else:
+            a = a.reshape((self.B,) + tuple(shape))
+        if a.ndim == 4:
+            a = a.transpose(0, 3, 1, 2)
+            if st.kind == "conv" and which == "gin" and self.in_cp != self.in_c and i == 0:
+                a = a[:, : self.in_c]
+        return np.ascontiguousarray(a)
+
+    # ------------------------------------------------------------ step program
+    @property
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _call(self, st, name: str, *args):
+        """C-ABI call of one layer pass; with ``PROFILE`` set, bracketed by CUDA
+        events on the launching stream (bench.py's per-kernel roofline)."""
+        if PROFILE is None:
+            return self.lib.call(name, *args)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        self.lib.call(name, *args)
+        b.record()
+        PROFILE.append((self.wid, st.cl.index, st.kind, name, a, b))
+
+    def load_batch(self, x_nchw: torch.Tensor, labels_i32: torch.Tensor):
+        """x_nchw: device float32 (B, C, H, W) slice of the global batch."""
+        c, h, w = self.cs.base.input_shape
+        self.lib.call("pc_nchw_to_nhwc", self.B, c, h, w, self.in_cp, x_nchw.data_ptr(),
+                      self.x.data_ptr(), self.prec, self.stream)
+        self.labels[: self.B].copy_(labels_i32, non_blocking=True)
+
+    def forward(self, i: int, loss_scale: float):
+        st, lib, s = self.layers[i], self.lib, self.stream
+        if st.kind == "conv":
+            flags = L.PC_RELU if st.relu_after else 0
+            self._call(st, "pc_conv2d_forward", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
+                     self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, s)
+        elif st.kind == "fc":
+            d = math.prod(st.in_nhwc)
+            mat = self._in_mat(st)
+            flags = L.PC_RELU if st.relu_after else 0
+            self._call(st, "pc_fc_forward", self.B, d, st.cl.out_shape[0], C.byref(mat), self._w_lowp(st),
+                     self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, s)
+        elif st.kind == "relu":
+            if not st.relu_fused_fwd:
+                self._call(st, "pc_relu_forward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),
+                         st.out.data_ptr(), self.prec, s)
+        elif st.kind == "pool":
+            hh, ww, cc = st.in_nhwc
+            self._call(st, "pc_maxpool_forward", self.B, hh, ww, cc, st.cl.layer.kernel, st.cl.layer.stride,
+                     st.inp.data_ptr(), st.out.data_ptr(), st.argmax.data_ptr(), self.prec, s)
+        else:
+            k = st.cl.layer.classes
+            self._call(st, "pc_softmax_xent", self.B, k, st.inp.data_ptr(), self.labels.data_ptr(),
+                     float(loss_scale), st.out.data_ptr(), st.row_loss.data_ptr(),
+                     self.bad_label.data_ptr(), self.prec, s)
+            self._call(st, "pc_sum_f64", self.B, st.row_loss.data_ptr(), self.loss.data_ptr(), s)
+
+    def _in_mat(self, st) -> L.Mat:
+        d = math.prod(st.in_nhwc)
+        ds = d // st.in_blocks
+        return L.Mat(st.inp.data_ptr(), ds, ds, self.B * ds)
+
+    def backward(self, i: int):
+        st, lib, s = self.layers[i], self.lib, self.stream
+        want_dx = i > 0
+        if st.kind == "conv":
+            flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
+            self._call(st, "pc_conv2d_backward", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
+                     st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
+                     st.inp.data_ptr() if st.mask_dx else None,
+                     self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
+                     self.ws.data_ptr(), self.ws_bytes, s)
+        elif st.kind == "fc":
+            d = math.prod(st.in_nhwc)
+            u = st.cl.out_shape[0]
+            xm = self._in_mat(st)
+            gm = L.Mat(st.gin.data_ptr() if want_dx else st.inp.data_ptr(), xm.ld, xm.cb, xm.bstride)
+            flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
+            self._call(st, "pc_fc_backward", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
+                     C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
+                     self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
+                     self.ws.data_ptr(), self.ws_bytes, s)
+        elif st.kind == "relu":
+            if not st.skip_bwd and want_dx:
+                self._call(st, "pc_relu_backward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),
+                         st.gout.data_ptr(), st.gin.data_ptr(), self.prec, s)
+        elif st.kind == "pool":
+            if want_dx:
+                hh, ww, cc = st.in_nhwc
+                self._call(st, "pc_maxpool_backward", self.B, hh, ww, cc, st.cl.layer.kernel, st.cl.layer.stride,
+                         st.gout.data_ptr(), st.argmax.data_ptr(),
+                         st.inp.data_ptr() if st.mask_dx else None, st.gin.data_ptr(), self.prec, s)
+        if st.cl.cross and st.cl.shared and want_dx and self.m > 1:
+            n = st.gin.numel()
+            self._call(st, "pc_scale", n, st.gin.data_ptr(), st.gin.data_ptr(), 1.0 / self.m, self.prec, s)
+
+    def sgd(self):
+        self.lib.call("pc_sgd_step", 1, self._sgd_dev.data_ptr(), self.n_flat, self.lr, self.mom, self.wd,
+                      self.stream)
+
+    @property
+    def n_layers(self) -> int:
+        return len(self.layers)

@@ -1,0 +1,331 @@
+"""The three schemes on B200: drop-in ``setup_workers`` / ``hybrid_step`` /
+``data_parallel_step`` / ``model_parallel_step`` / ``gather_dense_params`` /
+``evaluation_errors`` / ``reference_step`` with the reference's signatures
+and error behaviour (`pkg/src/parconv/schemes.py:439-645`).
+
+One call of ``hybrid_step`` = one synchronous update of the whole plan:
+contiguous replica shards of the global batch (`schemes.py:516-527`), loss
+scale 1/B_global, the column engines of every local replica run layer by
+layer with the column exchange at cross layers, gradients are summed over
+replicas and every replica applies the identical SGD update (the
+reference's reduce-to-root + root SGD + broadcast, with the broadcast
+replaced by bit-identical local updates; the ledger still books it).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .engine import ColumnEngine
+from .errors import ValidationError
+from .fabric import (Fabric, LocalExchange, LocalReducer, NcclExchange, NcclReducer, book_step)
+from .netdef import ColumnizedSpec, NetworkSpec, columnize, column_footprint_elements
+from .plan import (  # noqa: F401  (re-exported API)
+    CommPhase, CommVolume, ParallelPlan, ParamSet, comm_phases, comm_volume, init_dense_params,
+    lists_as_params, load_plan, merge_params, pack_tree, params_as_lists, parse_plan, plan_columnized,
+    split_params, unpack_tree)
+
+
+@dataclass
+class StepResult:
+    loss: float
+    ledger_bytes: int = 0
+    ledger_messages: int = 0
+    params: dict | None = None
+    sgd: object = None
+    sim_seconds: float | None = None
+
+
+# ----------------------------------------------------------------------------
+# Worker setup
+# ----------------------------------------------------------------------------
+
+
+def setup_workers(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, dense_params: dict, sgd,
+                  meter: bool = True, _velocity: dict | None = None) -> None:
+    if fabric.n != plan.workers:
+        raise ValidationError(f"plan grid {plan.describe()} needs {plan.workers} workers, "
+                              f"fabric has {fabric.n}")
+    m = plan.model_columns
+    fabric._engines.clear()
+    fabric._runner = None
+    fabric._plan, fabric._cs = plan, cs
+    fabric._hyper = (sgd.learning_rate, sgd.momentum, sgd.weight_decay)
+    for wid in range(fabric.n):
+        replica, column = divmod(wid, m)
+        st = fabric._local[wid]
+        dict.clear(st)
+        st.update(replica=replica, column=column, hyper=fabric._hyper, holds_velocity=replica == 0)
+        if wid in fabric.local_wids:
+            # like the reference (schemes.py:486-489) the column velocity starts at
+            # zero; reference_step passes its SgdState velocity through _velocity
+            vel = split_params(_velocity, cs, column) if _velocity is not None else None
+            st.update(host_params=split_params(dense_params, cs, column), host_velocity=vel)
+        if meter:
+            elems = cs.column_param_count * (2 if replica == 0 else 1)
+            st["resident_bytes"] = elems * fabric.device.wire_element_size
+            fabric.meter.alloc(wid, st["resident_bytes"])
+            fabric.meter_assert(wid)
+
+
+class _Runner:
+    """Engines of this process for one (plan, shard) plus the exchange wiring."""
+
+    def __init__(self, fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, shard: int):
+        self.fabric, self.plan, self.cs, self.shard = fabric, plan, cs, shard
+        d, m = plan.data_shards, plan.model_columns
+        dev = fabric.torch_device
+        self.engines = {}
+        with torch.cuda.device(dev):
+            for wid in fabric.local_wids:
+                replica, column = divmod(wid, m)
+                old = fabric._engines.get(wid)
+                eng = ColumnEngine(cs, wid, replica, column, shard, fabric.prec, dev, fabric._hyper)
+                if old is not None:
+                    eng.p32.copy_(old.p32)
+                    eng.v32.copy_(old.v32)
+                    if eng.plow is not None:
+                        eng.plow.copy_(old.plow)
+                else:
+                    st = fabric._local[wid]
+                    eng.load_params(dict.__getitem__(st, "host_params"), dict.get(st, "host_velocity"))
+                self.engines[wid] = eng
+        fabric._engines.update(self.engines)
+        if fabric.dist:
+            col_g, rep_g = fabric.groups(d, m)
+            self.exchange = NcclExchange(col_g) if m > 1 else None
+            self.reducer = NcclReducer(rep_g) if d > 1 else None
+        else:
+            self.exchange = LocalExchange(dev) if m > 1 else None
+            self.reducer = LocalReducer(dev) if d > 1 else None
+        self.replicas = {}
+        self.columns = {}
+        for wid, eng in sorted(self.engines.items()):
+            self.replicas.setdefault(eng.replica, []).append(eng)
+            self.columns.setdefault(eng.column, []).append(eng)
+        self.x_dev = None
+        self.y_dev = None
+
+    def upload(self, batch_x, batch_y):
+        """Host -> device copy of the global batch (float32 NCHW, int32 labels).
+        numpy input is staged through pinned memory; a pinned float32 CPU
+        tensor is copied directly; a CUDA tensor is used in place."""
+        dev = self.fabric.torch_device
+        if isinstance(batch_x, torch.Tensor) and batch_x.is_cuda and batch_x.dtype == torch.float32:
+            xs = batch_x.contiguous()
+        else:
+            xs = None
+            if isinstance(batch_x, torch.Tensor):
+                x = batch_x if batch_x.dtype == torch.float32 else batch_x.float()
+            else:
+                x = torch.as_tensor(np.ascontiguousarray(batch_x, dtype=np.float32))
+        y = torch.as_tensor(np.asarray(batch_y, dtype=np.int32)) if not isinstance(batch_y, torch.Tensor) \
+            else batch_y.to(torch.int32)
+        shape = tuple(xs.shape if xs is not None else x.shape)
+        if self.x_dev is None or tuple(self.x_dev.shape) != shape:
+            self.x_host = torch.empty(shape, dtype=torch.float32).pin_memory()
+            self.y_host = torch.empty(tuple(y.shape), dtype=torch.int32).pin_memory()
+            self.x_dev = torch.empty(shape, dtype=torch.float32, device=dev)
+            self.y_dev = torch.empty(tuple(y.shape), dtype=torch.int32, device=dev)
+        if xs is not None:
+            self.x_dev.copy_(xs)
+        elif x.is_pinned():
+            self.x_dev.copy_(x, non_blocking=True)
+        else:
+            self.x_host.copy_(x)
+            self.x_dev.copy_(self.x_host, non_blocking=True)
+        if y.is_cuda:
+            self.y_dev.copy_(y)
+        else:
+            self.y_host.copy_(y)
+            self.y_dev.copy_(self.y_host, non_blocking=True)
+
+    def program(self, loss_scale: float):
+        """The device step (no host synchronisation inside)."""
+        shard = self.shard
+        for eng in self.engines.values():
+            lo = eng.replica * shard
+            eng.load_batch(self.x_dev[lo:lo + shard], self.y_dev[lo:lo + shard])
+        n = len(self.cs.col_layers)
+        for engines in self.replicas.values():
+            for i in range(n):
+                if self.cs.col_layers[i].cross and self.exchange is not None:
+                    self.exchange.all_gather(i, engines)
+                for e in engines:
+                    e.forward(i, loss_scale)
+            for i in range(n - 1, -1, -1):
+                for e in engines:
+                    e.backward(i)
+                if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
+                    self.exchange.reduce_scatter(i, engines)
+        if self.reducer is not None:
+            self.reducer.reduce(self.columns)
+        for eng in self.engines.values():
+            eng.sgd()
+
+    def loss(self) -> float:
+        """Sum over replicas of column 0's loss (host read-back; raises on bad labels)."""
+        m = self.plan.model_columns
+        parts = [e.loss for e in self.engines.values() if e.column == 0]
+        bad = [e.bad_label for e in self.engines.values()]
+        total = torch.stack(parts).sum() if parts else torch.zeros(1, dtype=torch.float64,
+                                                                    device=self.fabric.torch_device)
+        flag = torch.stack(bad).sum()
+        if self.fabric.dist:
+            buf = torch.cat([total.reshape(1), flag.reshape(1).double()])
+            torch.distributed.all_reduce(buf)
+            total, flag = buf[0], buf[1]
+        host = torch.stack([total.reshape(()).double(), flag.reshape(()).double()]).cpu().numpy()
+        if host[1] != 0:
+            raise ValidationError(f"labels must lie in [0, {self.cs.base.classes})")
+        return float(host[0])
+
+
+def _runner(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, shard: int) -> _Runner:
+    r = getattr(fabric, "_runner", None)
+    if r is None or r.shard != shard or r.cs is not cs:
+        r = _Runner(fabric, plan, cs, shard)
+        fabric._runner = r
+    return r
+
+
+def _meter_step(fabric: Fabric, cs: ColumnizedSpec, shard: int) -> None:
+    _, acts = column_footprint_elements(cs, shard)
+    nbytes = acts * fabric.device.wire_element_size
+    for wid in range(fabric.n):
+        fabric.meter.alloc(wid, nbytes)
+        fabric.meter_assert(wid)
+    for wid in range(fabric.n):
+        fabric.meter.free(wid, nbytes)
+
+
+def hybrid_step(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, batch_x, batch_y,
+                meter: bool = True) -> StepResult:
+    d, m = plan.data_shards, plan.model_columns
+    if fabric.n != plan.workers:
+        raise ValidationError(f"plan grid {plan.describe()} needs {plan.workers} workers, "
+                              f"fabric has {fabric.n}")
+    if cs.columns != m:
+        raise ValidationError("columnized spec does not match the plan's column count")
+    b = int(np.shape(batch_x)[0])
+    if b % d != 0:
+        raise ValidationError(f"batch size {b} not divisible by {d} data shards")
+    labels = batch_y.cpu().numpy().astype(np.int64) if isinstance(batch_y, torch.Tensor) \
+        else np.asarray(batch_y, dtype=np.int64)
+    k = cs.base.classes
+    if labels.size and (labels.min() < 0 or labels.max() >= k):
+        raise ValidationError(f"labels must lie in [0, {k})")
+    if getattr(fabric, "_hyper", None) is None:
+        raise ValidationError("setup_workers must run before hybrid_step")
+    shard = b // d
+    if shard == 0:
+        raise ValidationError("hybrid_step needs a non-empty batch")
+    before_b, before_m = fabric.ledger.total_bytes, fabric.ledger.total_messages
+    if meter:
+        _meter_step(fabric, cs, shard)
+    run = _runner(fabric, plan, cs, shard)
+    with torch.cuda.device(fabric.torch_device):
+        run.upload(batch_x, labels)
+        run.program(1.0 / b)
+        loss = run.loss()
+    book_step(fabric, plan, cs, shard)
+    return StepResult(loss=loss, ledger_bytes=fabric.ledger.total_bytes - before_b,
+                      ledger_messages=fabric.ledger.total_messages - before_m)
+
+
+def data_parallel_step(fabric, plan, cs, batch_x, batch_y, meter: bool = True) -> StepResult:
+    if plan.model_columns != 1:
+        raise ValidationError("data_parallel_step requires a plan with model_columns == 1")
+    return hybrid_step(fabric, plan, cs, batch_x, batch_y, meter=meter)
+
+
+def model_parallel_step(fabric, plan, cs, batch_x, batch_y, meter: bool = True) -> StepResult:
+    if plan.data_shards != 1:
+        raise ValidationError("model_parallel_step requires a plan with data_shards == 1")
+    return hybrid_step(fabric, plan, cs, batch_x, batch_y, meter=meter)
+
+
+def column_params(fabric: Fabric, wid: int) -> dict:
+    """Reference-layout parameters of a hosted worker (device -> host)."""
+    eng = fabric._engines.get(wid)
+    if eng is not None:
+        return eng.params_host()
+    return dict.__getitem__(fabric._local[wid], "host_params")
+
+
+def gather_dense_params(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec) -> dict:
+    m = plan.model_columns
+    if fabric.dist:
+        cols = []
+        for j in range(m):
+            obj = [column_params(fabric, j) if fabric.rank == j else None]
+            torch.distributed.broadcast_object_list(obj, src=j)
+            cols.append(obj[0])
+    else:
+        cols = [column_params(fabric, plan.worker_of(0, j)) for j in range(m)]
+    return merge_params(cols, cs)
+
+
+def evaluation_errors(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, x, labels) -> int:
+    """Misclassifications of replica 0's columns (forward only; ties -> lowest class)."""
+    labels = np.asarray(labels, dtype=np.int64)
+    b = int(np.shape(x)[0])
+    if b == 0:
+        return 0
+    eval_plan = ParallelPlan(1, plan.model_columns, plan.cross_layers)
+    if fabric.dist:
+        raise ValidationError("evaluation_errors under torchrun: gather params and evaluate on rank 0")
+    run = _Runner.__new__(_Runner)
+    run.fabric, run.plan, run.cs, run.shard = fabric, eval_plan, cs, b
+    dev = fabric.torch_device
+    m = plan.model_columns
+    with torch.cuda.device(dev):
+        engines = []
+        for j in range(m):
+            src = fabric._engines.get(j)
+            eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, dev, fabric._hyper)
+            if src is not None:
+                eng.p32.copy_(src.p32)
+                if eng.plow is not None:
+                    eng.plow.copy_(src.plow)
+            else:
+                eng.load_params(dict.__getitem__(fabric._local[j], "host_params"))
+            engines.append(eng)
+        ex = LocalExchange(dev) if m > 1 else None
+        xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+        yd = torch.zeros(b, dtype=torch.int32, device=dev)
+        for e in engines:
+            e.load_batch(xd, yd)
+        n = len(cs.col_layers)
+        for i in range(n - 1):          # stop before the softmax: logits = head output
+            if cs.col_layers[i].cross and ex is not None:
+                ex.all_gather(i, engines)
+            for e in engines:
+                e.forward(i, 1.0)
+        head = engines[0].layers[n - 2]
+        logits = head.out[: b * cs.base.classes].float().reshape(b, cs.base.classes).cpu().numpy()
+    pred = np.argmax(logits, axis=1)
+    return int(np.count_nonzero(pred != labels))
+
+
+def reference_step(net: NetworkSpec, params: dict, batch, sgd, precision: str = "fp32") -> StepResult:
+    """Dense single-worker step on the device (the reference's oracle entry,
+    `schemes.py:439-458`); returns fresh dense params and SgdState."""
+    from .kernels import SgdState
+    from .fabric import spawn
+    x, labels = batch
+    if np.shape(x)[0] < 1:
+        raise ValidationError("reference_step needs a non-empty batch")
+    cs = columnize(net, 1)
+    fab = spawn(1, precision=precision)
+    vel = lists_as_params(list(sgd.velocity), cs) if sgd.velocity else None
+    setup_workers(fab, ParallelPlan(1, 1), cs, params, sgd, meter=False, _velocity=vel)
+    res = hybrid_step(fab, ParallelPlan(1, 1), cs, x, labels, meter=False)
+    eng = fab._engines[0]
+    new_sgd = SgdState(sgd.learning_rate, sgd.momentum, sgd.weight_decay,
+                       params_as_lists(eng.velocity_host(), cs))
+    return StepResult(loss=res.loss, params=eng.params_host(), sgd=new_sgd)

@@ -1,0 +1,180 @@
+"""Kernel-level parity on the B200 through the C ABI (the reference's unit
+tests, `pkg/tests/test_kernels.py`, re-expressed with device tolerances).
+
+fp32 mode: every op vs the reference's golden outputs, <= 1e-5 relative
+(max-normalised). bf16 mode: each op fed bf16-rounded operands vs the float64
+oracle on the same rounded operands, <= 1e-5 before the output rounding,
+i.e. <= 2^-8 relative on bf16-stored outputs. Max-pool argmax
+and label handling are bit-exact in both modes.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import ref_kernels as O
+
+pytestmark = pytest.mark.gpu
+
+KER = np.load(GOLDEN / "kernels.npz")
+FP32_TOL = 1e-5
+BF16_OUT_TOL = 2.0 ** -7   # bf16 storage of the result (8-bit mantissa) plus accumulation
+
+
+@pytest.fixture(autouse=True)
+def fp32_mode():
+    from paper_1312_5853_b200 import kernels as K
+    K.set_precision("fp32")
+    yield
+    K.set_precision("fp32")
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def bf16(a):
+    import torch
+    return torch.as_tensor(np.asarray(a, np.float32)).bfloat16().float().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("gi", range(5))
+def test_conv_fp32(gi):
+    from paper_1312_5853_b200 import kernels as K
+    b, c, h, w, n, k, s, p = KER[f"conv{gi}_geom"]
+    cp = K.ConvParams(KER[f"conv{gi}_w"], KER[f"conv{gi}_b"], int(s), int(p))
+    assert rel(K.conv2d_forward(KER[f"conv{gi}_x"], cp), KER[f"conv{gi}_y"]) < FP32_TOL
+    gx, gw, gb = K.conv2d_backward(KER[f"conv{gi}_x"], cp, KER[f"conv{gi}_gy"])
+    assert rel(gx, KER[f"conv{gi}_gx"]) < FP32_TOL
+    assert rel(gw, KER[f"conv{gi}_gw"]) < FP32_TOL
+    assert rel(gb, KER[f"conv{gi}_gb"]) < FP32_TOL
+
+
+@pytest.mark.parametrize("gi", range(3))
+def test_fc_fp32(gi):
+    from paper_1312_5853_b200 import kernels as K
+    x, w, bias, gy = (KER[f"fc{gi}_{t}"] for t in ("x", "w", "b", "gy"))
+    assert rel(K.fc_forward(x, w, bias), KER[f"fc{gi}_y"]) < FP32_TOL
+    for got, key in zip(K.fc_backward(x, w, gy), ("gx", "gw", "gb")):
+        assert rel(got, KER[f"fc{gi}_{key}"]) < FP32_TOL
+
+
+def test_relu_bit_exact():
+    from paper_1312_5853_b200 import kernels as K
+    assert np.array_equal(K.relu_forward(KER["relu_x"]), KER["relu_y"])
+    assert np.array_equal(K.relu_backward(KER["relu_x"], KER["relu_g"]), KER["relu_gx"])
+
+
+@pytest.mark.parametrize("gi", range(4))
+def test_maxpool_argmax_bit_exact(gi):
+    from paper_1312_5853_b200 import kernels as K
+    x, (k, s), gy = KER[f"pool{gi}_x"], KER[f"pool{gi}_ks"], KER[f"pool{gi}_gy"]
+    y, arg = K.maxpool_forward(x, int(k), int(s))
+    assert np.array_equal(y, KER[f"pool{gi}_y"])
+    assert np.array_equal(arg, KER[f"pool{gi}_arg"])
+    gx = K.maxpool_backward(x, int(k), int(s), gy, arg)
+    assert rel(gx, KER[f"pool{gi}_gx"]) < 1e-6
+
+
+def test_maxpool_ties_and_overlap_kats():
+    from paper_1312_5853_b200 import kernels as K
+    _, arg = K.maxpool_forward(np.full((1, 1, 2, 2), 5.0), 2, 2)
+    assert arg[0, 0, 0, 0] == 0
+    x = np.zeros((1, 1, 5, 5))
+    x[0, 0, 2, 2] = 1.0
+    y, arg = K.maxpool_forward(x, 3, 2)
+    assert K.maxpool_backward(x, 3, 2, np.ones_like(y), arg)[0, 0, 2, 2] == 4.0
+
+
+@pytest.mark.parametrize("gi", range(3))
+def test_softmax_fp32(gi):
+    from paper_1312_5853_b200 import kernels as K
+    loss, grad = K.softmax_xent_scaled(KER[f"sm{gi}_logits"], KER[f"sm{gi}_labels"], float(KER[f"sm{gi}_scale"]))
+    assert abs(loss - float(KER[f"sm{gi}_loss"])) <= 1e-5 * max(1.0, abs(float(KER[f"sm{gi}_loss"])))
+    assert rel(grad, KER[f"sm{gi}_grad"]) < FP32_TOL
+    assert np.all(np.isfinite(grad))
+
+
+def test_softmax_label_errors_and_uniform():
+    from paper_1312_5853_b200 import kernels as K
+    from paper_1312_5853_b200.errors import ValidationError
+    loss, grad = K.softmax_xent(np.zeros((3, 7)), [0, 3, 6])
+    assert abs(loss - np.log(7)) < 1e-6
+    assert np.allclose(grad.sum(axis=1), 0.0, atol=1e-7)
+    with pytest.raises(ValidationError):
+        K.softmax_xent(np.zeros((2, 7)), [1, 7])
+    with pytest.raises(ValidationError):
+        K.softmax_xent(np.zeros((2, 7)), [-1, 0])
+
+
+def test_sgd_matches_reference():
+    from paper_1312_5853_b200 import kernels as K
+    st = K.SgdState(0.01, 0.9, 0.0005, [KER["sgd_v0"], KER["sgd_v1"]])
+    newp, newst = K.sgd_step([KER["sgd_p0"], KER["sgd_p1"]], [KER["sgd_g0"], KER["sgd_g1"]], st)
+    for i in range(2):
+        assert rel(newp[i], KER[f"sgd_np{i}"]) < 1e-6
+        assert rel(newst.velocity[i], KER[f"sgd_nv{i}"]) < 1e-6
+
+
+def test_sgd_two_step_recurrence():
+    from paper_1312_5853_b200 import kernels as K
+    p0, g = np.array([1.0, -2.0]), np.array([0.5, 0.25])
+    st = K.SgdState(0.01, 0.9, 0.0, [np.zeros(2)])
+    p = [p0]
+    for _ in range(2):
+        p, st = K.sgd_step(p, [g], st)
+    assert np.allclose(st.velocity[0], -0.019 * g, rtol=1e-6)
+    assert np.allclose(p[0], p0 - 0.029 * g, rtol=1e-6)
+
+
+# ---------------------------------------------------------------- bf16 mode
+
+@pytest.mark.parametrize("geom", [(2, 8, 9, 9, 16, 3, 1, 1), (2, 16, 13, 13, 32, 3, 1, 1),
+                                  (2, 3, 23, 23, 8, 11, 4, 0), (1, 32, 27, 27, 64, 5, 1, 2),
+                                  (4, 64, 13, 13, 96, 3, 1, 1)])
+def test_conv_bf16_same_operands(geom):
+    from paper_1312_5853_b200 import kernels as K
+    b, c, h, w, n, k, s, p = geom
+    rs = np.random.RandomState(7)
+    x = bf16(rs.randn(b, c, h, w))
+    wt = bf16(rs.randn(n, c, k, k) * 0.2)
+    bias = rs.randn(n).astype(np.float32).astype(np.float64) * 0.1
+    K.set_precision("bf16")
+    cp = K.ConvParams(wt, bias, s, p)
+    y = K.conv2d_forward(x, cp)
+    yr = O.conv2d_forward(x, wt, bias, s, p)
+    assert rel(y, yr) < BF16_OUT_TOL
+    gy = bf16(rs.randn(*yr.shape))
+    gx, gw, gb = K.conv2d_backward(x, cp, gy)
+    rgx, rgw, rgb = O.conv2d_backward(x, wt, gy, s, p)
+    assert rel(gx, rgx) < BF16_OUT_TOL
+    assert rel(gw, rgw) < 1e-5        # fp32 weight gradients from bf16 operands
+    assert rel(gb, rgb) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(8, 64, 32), (32, 512, 96), (256, 1024, 1000)])
+def test_fc_bf16_same_operands(shape):
+    from paper_1312_5853_b200 import kernels as K
+    b, d, u = shape
+    rs = np.random.RandomState(3)
+    x, w = bf16(rs.randn(b, d)), bf16(rs.randn(d, u) * 0.05)
+    bias = rs.randn(u).astype(np.float32).astype(np.float64)
+    gy = bf16(rs.randn(b, u))
+    K.set_precision("bf16")
+    assert rel(K.fc_forward(x, w, bias), O.fc_forward(x, w, bias)) < BF16_OUT_TOL
+    gx, gw, gb = K.fc_backward(x, w, gy)
+    rgx, rgw, rgb = O.fc_backward(x, w, gy)
+    assert rel(gx, rgx) < BF16_OUT_TOL
+    assert rel(gw, rgw) < 1e-5
+    assert rel(gb, rgb) < 1e-5
+
+
+def test_maxpool_bf16_argmax_bit_exact():
+    from paper_1312_5853_b200 import kernels as K
+    rs = np.random.RandomState(5)
+    x = bf16(np.round(rs.randn(2, 16, 13, 13) * 4) / 4)   # many ties
+    K.set_precision("bf16")
+    y, arg = K.maxpool_forward(x, 3, 2)
+    ry, rarg = O.maxpool_forward(x, 3, 2)
+    assert np.array_equal(arg, rarg)
+    assert np.array_equal(y, ry)
