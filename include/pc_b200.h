@@ -65,6 +65,10 @@ PC_API const char* pc_last_error(void);
 PC_API int pc_version(void);
 /* Number of kernels this library has launched in the process (all devices). */
 PC_API unsigned long long pc_launch_count(void);
+/* bf16 contraction launches by engine: tcgen05 tensor-core kernels vs the
+ * CUDA-core kernel used only for extents the tensor-core path cannot tile
+ * (e.g. a 10-class head: rows not 16-byte aligned). */
+PC_API void pc_contraction_counts(unsigned long long* tensor_core, unsigned long long* simt);
 /* 1 when the tcgen05/TMA tensor-core path is compiled in and the device is sm_100. */
 PC_API int pc_has_tcgen05(void);
 

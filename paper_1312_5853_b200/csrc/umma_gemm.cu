@@ -1,39 +1,738 @@
-// bf16 contraction entry points. BRING-UP STAGE: routed through the SIMT
-// implicit GEMM with bf16 storage until the tcgen05 kernel lands.
+// bf16 tensor-core contractions for sm_100a: tcgen05.mma with the fp32
+// accumulator in TMEM, operands staged in 128B-swizzled shared memory by TMA
+// (dense / channel-blocked views, K-major or MN-major) or by an im2col gather
+// (cp.async, 16 B = 8 channels per request, zero-fill for padding) for the
+// convolution operand, and a fused epilogue (bias, ReLU, ReLU-mask of the
+// producer, bf16 / fp32 / transposed-fp32 stores, split-K partials).
+//
+// One CTA computes one BM x BN output tile over a K range (grid.z = split-K):
+//   warps 0-3  epilogue: tcgen05.ld 32 lanes x 16 columns at a time
+//   warp  4    TMEM allocator + single-thread MMA issuer
+//   warp  5    TMA producer
+//   warps 6-9  im2col gather producers (conv operand only)
+// A STAGES-deep full/empty mbarrier ring connects producers and the MMA
+// issuer; tcgen05.commit frees a stage and finally signals the epilogue.
+//
+// GEMM shapes per pass (M x N x K):
+//   conv fwd   pixels x Cout x (kh*kw*Cin)      A = im2col(x)   B = w [Cout][K]     (K-major)
+//   conv dgrad pixels x Cin  x (kh*kw*Cout)     A = im2col(gy)  B = w^T [Cin][K]    (K-major)
+//   conv wgrad (kh*kw*Cin) x Cout x pixels      A = im2col(x)^T (MN)  B = gy (MN)   -> gw^T store
+//   fc fwd     B x U x D     A = x (K)   B = W [U][D] (K)
+//   fc dgrad   B x D x U     A = gy (K)  B = W (MN)
+//   fc wgrad   U x D x B     A = gy (MN) B = x (MN)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
 #include "gemm_ops.cuh"
 #include "umma.cuh"
 
 namespace pc {
+namespace umma {
 
-bool umma_available() { return false; }
+enum AMode { A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FWD = 2, A_GATHER_DGRAD = 3, A_GATHER_WGRAD = 4 };
+enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
+enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2 };
+
+constexpr int BM = 128, BK = 64;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+
+struct alignas(64) Params {
+  CUtensorMap tma_a;
+  CUtensorMap tma_b;
+  int M, N, K;
+  int num_kb;        // k-blocks in total
+  int kb_per_split;  // k-blocks per grid.z slice
+  long long a_cb, b_cb;  // channel-block widths of the TMA views (k or mn index -> (idx % cb, idx / cb))
+  const __nv_bfloat16* gsrc;
+  pc_conv_geom g;
+  void* out;
+  long long o_ld, o_cb, o_bstride;
+  long long split_stride;
+  const float* bias;
+  const __nv_bfloat16* mask;
+  int relu;
+};
+
+// ----------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a pipeline bug traps (a launch error the host reports) instead
+// of hanging the device forever.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++spins == (1u << 28)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, uint32_t dst, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor, 128B swizzle (sm100 version bit 46 = 1).
+__device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__host__ __device__ constexpr uint32_t make_idesc() {
+  return (1u << 4)                  // D = f32
+         | (1u << 7) | (1u << 10)   // A, B = bf16
+         | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16)
+         | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+template <int BN>
+constexpr int tmem_cols() {
+  return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+}
+
+template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD; }
+template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD; }
+
+template <int BN, int STAGES>
+constexpr int smem_bytes() {
+  return 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
+}
+
+// ------------------------------------------------------------------- kernel
+template <int AM, int BMODE, int EPI, int BN, int STAGES>
+__global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
+    umma_gemm_k(const __grid_constant__ Params p) {
+  constexpr bool GATHER = a_is_gather<AM>();
+  constexpr bool A_MN = a_is_mn<AM>();
+  constexpr bool B_MN = BMODE == B_TMA_MN;
+  constexpr int B_STAGE_BYTES = BN * BK * 2;
+  constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN>();
+  constexpr int TCOLS = tmem_cols<BN>();
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kb_begin = blockIdx.z * p.kb_per_split;
+  const int kb_end = min(p.num_kb, kb_begin + p.kb_per_split);
+  const int nkb = max(kb_end - kb_begin, 0);
+
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1 + (GATHER ? 128 : 0));
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(tmem_full, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 5 && lane == 0) {
+    prefetch_tmap(&p.tma_b);
+    if constexpr (!GATHER) prefetch_tmap(&p.tma_a);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 5) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        const int kb = kb_begin + it;
+        mbar_arrive_expect_tx(&full[s], B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES));
+        const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
+        if constexpr (B_MN) {
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c) {
+            long long n = n0 + 64 * c;
+            tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), (int)(n % p.b_cb), kb * BK, (int)(n / p.b_cb));
+          }
+        } else {
+          long long k = (long long)kb * BK;
+          tma_load_3d(&p.tma_b, &full[s], dB, (int)(k % p.b_cb), n0, (int)(k / p.b_cb));
+        }
+        if constexpr (!GATHER) {
+          const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES);
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) {
+              long long m = m0 + 64 * c;
+              tma_load_3d(&p.tma_a, &full[s], dA + c * (64 * BK * 2), (int)(m % p.a_cb), kb * BK,
+                          (int)(m / p.a_cb));
+            }
+          } else {
+            long long k = (long long)kb * BK;
+            tma_load_3d(&p.tma_a, &full[s], dA, (int)(k % p.a_cb), m0, (int)(k / p.a_cb));
+          }
+        }
+      }
+    }
+  } else if (warp >= 6) {
+    // ----------------------------------------------------- im2col gather producer
+    if constexpr (GATHER) {
+      const int gt = threadIdx.x - 192;
+      const pc_conv_geom& g = p.g;
+      if constexpr (AM == A_GATHER_FWD || AM == A_GATHER_DGRAD) {
+        // K-major rows = pixels; thread owns 16B chunk q of rows rb + 16*it
+        const int q = gt & 7, rb = gt >> 3;
+        int rb_b[8], ry[8], rx[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          int m = m0 + rb + 16 * it;
+          int W_ = AM == A_GATHER_FWD ? g.Wo : g.W, H_ = AM == A_GATHER_FWD ? g.Ho : g.H;
+          if (m < p.M) {
+            int x = m % W_, t = m / W_;
+            int y = t % H_;
+            rb_b[it] = t / H_;
+            if constexpr (AM == A_GATHER_FWD) {
+              ry[it] = y * g.stride - g.pad;
+              rx[it] = x * g.stride - g.pad;
+            } else {
+              ry[it] = y + g.pad;
+              rx[it] = x + g.pad;
+            }
+          } else {
+            rb_b[it] = 0;
+            ry[it] = -(1 << 28);
+            rx[it] = -(1 << 28);
+          }
+        }
+        for (int it = 0; it < nkb; ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const long long k = (long long)(kb_begin + it) * BK + q * 8;
+          const bool kvalid = k < p.K;
+          const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES);
+          if constexpr (AM == A_GATHER_FWD) {
+            int c = kvalid ? (int)(k % g.C) : 0;
+            int ij = kvalid ? (int)(k / g.C) : 0;
+            int i = ij / g.k, j = ij - (ij / g.k) * g.k;
+            int blk = c / g.cs, coff = c - blk * g.cs;
+            const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
+#pragma unroll
+            for (int r8 = 0; r8 < 8; ++r8) {
+              int r = rb + 16 * r8;
+              int iy = ry[r8] + i, ix = rx[r8] + j;
+              bool ok = kvalid && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
+              const __nv_bfloat16* src = ok ? src0 + ((long long)(rb_b[r8] * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
+              cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), src, ok);
+            }
+          } else {
+            int n = kvalid ? (int)(k % g.N) : 0;
+            int ij = kvalid ? (int)(k / g.N) : 0;
+            int i = ij / g.k, j = ij - (ij / g.k) * g.k;
+            const __nv_bfloat16* src0 = p.gsrc + n;
+#pragma unroll
+            for (int r8 = 0; r8 < 8; ++r8) {
+              int r = rb + 16 * r8;
+              int ny = ry[r8] - i, nx = rx[r8] - j;
+              bool ok = kvalid && ny >= 0 && nx >= 0;
+              int oy = 0, ox = 0;
+              if (g.stride == 1) {
+                oy = ny; ox = nx;
+              } else {
+                ok = ok && (ny % g.stride == 0) && (nx % g.stride == 0);
+                oy = ny / g.stride; ox = nx / g.stride;
+              }
+              ok = ok && oy < g.Ho && ox < g.Wo;
+              const __nv_bfloat16* src = ok ? src0 + ((long long)(rb_b[r8] * g.Ho + oy) * g.Wo + ox) * g.N : p.gsrc;
+              cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), src, ok);
+            }
+          }
+          cp_async_arrive_noinc(&full[s]);
+        }
+      } else {
+        // A_GATHER_WGRAD: MN-major rows = pixels (K), chunk q = 8 consecutive (i,j,c) of this M tile
+        const int q = gt & 15, rb = gt >> 4;
+        const long long kc = (long long)m0 + q * 8;
+        const bool mvalid = kc < p.M;
+        int c = mvalid ? (int)(kc % g.C) : 0;
+        int ij = mvalid ? (int)(kc / g.C) : 0;
+        int i = ij / g.k, j = ij - (ij / g.k) * g.k;
+        int blk = c / g.cs, coff = c - blk * g.cs;
+        const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
+        const int hw = g.Ho * g.Wo;
+        const uint32_t cofs = (q >> 3) * (64 * BK * 2);
+        for (int it = 0; it < nkb; ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES) + cofs;
+          const long long pbase = (long long)(kb_begin + it) * BK;
+#pragma unroll
+          for (int r8 = 0; r8 < 8; ++r8) {
+            int r = rb + 8 * r8;
+            long long pix = pbase + r;
+            bool ok = mvalid && pix < p.K;
+            int b = 0, oy = 0, ox = 0;
+            if (ok) {
+              b = (int)(pix / hw);
+              int rem = (int)(pix - (long long)b * hw);
+              oy = rem / g.Wo;
+              ox = rem - oy * g.Wo;
+            }
+            int iy = oy * g.stride + i - g.pad, ix = ox * g.stride + j - g.pad;
+            ok = ok && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
+            const __nv_bfloat16* src = ok ? src0 + ((long long)(b * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
+            cp_async16(base + r * 128 + (((q & 7) ^ (r & 7)) << 4), src, ok);
+          }
+          cp_async_arrive_noinc(&full[s]);
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // --------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t aBase = smem_u32(sA + s * A_STAGE_BYTES);
+        const uint32_t bBase = smem_u32(sB + s * B_STAGE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          uint64_t ad = A_MN ? make_desc(aBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(aBase + kk * 32, 16, 1024);
+          uint64_t bd = B_MN ? make_desc(bBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(bBase + kk * 32, 16, 1024);
+          tc_mma(tmem, ad, bd, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&empty[s]);
+      }
+      tc_commit(tmem_full);
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int row = warp * 32 + lane;
+    const long long m = (long long)m0 + row;
+    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      if (nkb > 0) {
+        tmem_ld16(tbase + c0, v);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v[t] = 0.f;
+      }
+      const long long n = (long long)n0 + c0;
+      if (m >= p.M || n >= p.N) continue;
+      if constexpr (EPI == EPI_BF16) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          long long nn = n + 8 * h;
+          if (nn >= p.N) break;
+          float o[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            float val = v[8 * h + t];
+            if (p.bias) val += __ldg(p.bias + nn + t);
+            if (p.relu) val = val > 0.f ? val : 0.f;
+            o[t] = val;
+          }
+          long long blk = nn / p.o_cb;
+          long long idx = blk * p.o_bstride + m * p.o_ld + (nn - blk * p.o_cb);
+          if (p.mask) {
+            uint4 mk = *reinterpret_cast<const uint4*>(p.mask + idx);
+            const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) o[t] = __bfloat162float(mb[t]) > 0.f ? o[t] : 0.f;
+          }
+          uint4 u;
+          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) hh[t] = __floats2bfloat162_rn(o[2 * t], o[2 * t + 1]);
+          *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + idx) = u;
+        }
+      } else if constexpr (EPI == EPI_F32) {
+        float* o = static_cast<float*>(p.out) + blockIdx.z * p.split_stride + m * p.o_ld + n;
+        if (n + 16 <= p.N) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            reinterpret_cast<float4*>(o)[t] = make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
+        } else {
+          for (int t = 0; t < 16 && n + t < p.N; ++t) o[t] = v[t];
+        }
+      } else {
+        float* o = static_cast<float*>(p.out) + blockIdx.z * p.split_stride + m;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (n + t < p.N) o[(n + t) * p.o_ld] = v[t];
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+  }
+}
+
+// --------------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// 3-D bf16 view {inner, rows, blocks} with strides (ld, bstride) elements; box {64, box_rows, 1}.
+static int make_map(CUtensorMap* map, const void* ptr, long long inner, long long rows, long long blocks,
+                    long long ld, long long bstride, int box_rows) {
+  PC_REQUIRE(get_encode(), PC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  PC_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && ld % 8 == 0 && (blocks == 1 || bstride % 8 == 0),
+             PC_EVALUE, "TMA view not 16-byte aligned (ld=%lld bstride=%lld)", ld, bstride);
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)blocks};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)(blocks > 1 ? bstride : ld * rows) * 2};
+  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  PC_REQUIRE(r == CUDA_SUCCESS, PC_ECUDA, "cuTensorMapEncodeTiled failed (%d): inner=%lld rows=%lld blocks=%lld",
+             (int)r, inner, rows, blocks);
+  return PC_OK;
+}
+
+static std::atomic<unsigned long long> g_tc_launches{0}, g_simt_launches{0};
+
+template <int AM, int BMODE, int EPI, int BN, int STAGES>
+static int launch(const Params& p, int splits, cudaStream_t st) {
+  auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES>;
+  constexpr int smem = smem_bytes<BN, STAGES>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  dim3 grid(ceil_div(p.N, BN), ceil_div(p.M, BM), splits);
+  constexpr int threads = a_is_gather<AM>() ? 320 : 192;
+  kern<<<grid, threads, smem, st>>>(p);
+  g_tc_launches.fetch_add(1, std::memory_order_relaxed);
+  PC_CUDA_CHECK_LAUNCH("umma_gemm");
+  return PC_OK;
+}
+
+// Tile N for a K-major B operand (the TMA box height must equal the tile).
+static int bn_for(int N) { return N <= 64 ? 64 : N <= 96 ? 96 : N <= 128 ? 128 : N % 192 == 0 ? 192 : 256; }
+
+template <int AM, int EPI>
+static int launch_kb(const Params& p, int splits, cudaStream_t st) {
+  switch (bn_for(p.N)) {
+    case 64: return launch<AM, B_TMA_K, EPI, 64, 6>(p, splits, st);
+    case 96: return launch<AM, B_TMA_K, EPI, 96, 6>(p, splits, st);
+    case 128: return launch<AM, B_TMA_K, EPI, 128, 5>(p, splits, st);
+    case 192: return launch<AM, B_TMA_K, EPI, 192, 4>(p, splits, st);
+    default: return launch<AM, B_TMA_K, EPI, 256, 4>(p, splits, st);
+  }
+}
+template <int AM, int EPI>
+static int launch_mn(const Params& p, int splits, cudaStream_t st) {
+  if (p.N <= 64) return launch<AM, B_TMA_MN, EPI, 64, 6>(p, splits, st);
+  if (p.N <= 128) return launch<AM, B_TMA_MN, EPI, 128, 5>(p, splits, st);
+  return launch<AM, B_TMA_MN, EPI, 256, 4>(p, splits, st);
+}
+
+static Params base_params(int M, int N, int K) {
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.num_kb = ceil_div(K, BK);
+  p.kb_per_split = p.num_kb;
+  p.a_cb = p.b_cb = 1LL << 40;
+  p.o_cb = 1LL << 40;
+  return p;
+}
+
+}  // namespace umma
+
+using namespace umma;
+
+bool umma_available() {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major == 10 && minor == 0 && get_encode();
+}
+
+static bool conv_tc_shape(const pc_conv_geom& g) {
+  return g.C % 8 == 0 && g.cs % 8 == 0 && g.N % 8 == 0 && (g.C == g.cs || g.cstride % 8 == 0);
+}
 
 int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const float* bias, void* y,
                       int flags, cudaStream_t st) {
-  return simt_conv_forward(g, x, w, bias, y, PC_BF16, flags, st);
+  if (!conv_tc_shape(g)) {
+    g_simt_launches++;
+    return simt_conv_forward(g, x, w, bias, y, PC_BF16, flags, st);
+  }
+  int M = g.B * g.Ho * g.Wo, K = g.k * g.k * g.C;
+  Params p = base_params(M, g.N, K);
+  int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, bn_for(g.N));
+  if (rc) return rc;
+  p.b_cb = K;
+  p.gsrc = static_cast<const __nv_bfloat16*>(x);
+  p.g = g;
+  p.out = y;
+  p.o_ld = g.N;
+  p.bias = bias;
+  p.relu = (flags & PC_RELU) != 0;
+  return launch_kb<A_GATHER_FWD, EPI_BF16>(p, 1, st);
 }
+
+__global__ void transpose_w_k(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt, int N, int KK,
+                              int C) {
+  // wt[c][ij][n] = w[n][ij][c]
+  long long total = (long long)N * KK * C;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    int n = (int)(t % N);
+    long long r = t / N;
+    int ij = (int)(r % KK);
+    int c = (int)(r / KK);
+    wt[t] = w[((long long)n * KK + ij) * C + c];
+  }
+}
+
+size_t umma_conv_extra_ws(const pc_conv_geom& g, int prec) {
+  return prec == PC_BF16 ? (size_t)g.N * g.k * g.k * g.C * 2 + 256 : 0;
+}
+
 int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* gx, const void* mask,
-                    cudaStream_t st, void*, size_t) {
-  return simt_conv_dgrad(g, w, gy, gx, mask, st, PC_BF16);
+                    cudaStream_t st, void* ws, size_t ws_bytes) {
+  if (!conv_tc_shape(g)) {
+    g_simt_launches++;
+    return simt_conv_dgrad(g, w, gy, gx, mask, st, PC_BF16);
+  }
+  const int KK = g.k * g.k;
+  size_t need = (size_t)g.N * KK * g.C * 2;
+  PC_REQUIRE(ws != nullptr && ws_bytes >= need, PC_EVALUE, "conv dgrad: workspace too small");
+  // the transposed weights live at the END of the workspace (wgrad partials use the front)
+  __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(
+      (reinterpret_cast<uintptr_t>(ws) + ws_bytes - need) & ~uintptr_t(127));
+  long long total = (long long)g.N * KK * g.C;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C);
+  PC_CUDA_CHECK_LAUNCH("transpose_w");
+  int M = g.B * g.H * g.W, K = KK * g.N;
+  Params p = base_params(M, g.C, K);
+  int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, bn_for(g.C));
+  if (rc) return rc;
+  p.b_cb = K;
+  p.gsrc = static_cast<const __nv_bfloat16*>(gy);
+  p.g = g;
+  p.out = gx;
+  p.o_ld = g.cs;
+  p.o_cb = g.cs;
+  p.o_bstride = g.cstride;
+  p.mask = static_cast<const __nv_bfloat16*>(mask);
+  return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, 1, st);
 }
+
 long long umma_wgrad_splits(const pc_conv_geom& g) {
-  return simt_splits(g.N, g.k * g.k * g.C, (long long)g.B * g.Ho * g.Wo);
+  long long Kc = (long long)g.k * g.k * g.C;
+  long long P = (long long)g.B * g.Ho * g.Wo;
+  int bn = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
+  long long tiles = ((Kc + BM - 1) / BM) * ((g.N + bn - 1) / bn);
+  long long kbs = (P + BK - 1) / BK;
+  long long want = (2 * 148 + tiles - 1) / tiles;
+  long long cap = kbs / 8;  // keep >= 8 k-blocks per split
+  if (want > cap) want = cap;
+  if (want > 64) want = 64;
+  return want < 1 ? 1 : want;
 }
+
 int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float* gw, float* part,
                     cudaStream_t st) {
-  return simt_conv_wgrad(g, x, gy, gw, part, (int)umma_wgrad_splits(g), st, PC_BF16);
+  if (!conv_tc_shape(g)) {
+    g_simt_launches++;
+    long long P = (long long)g.B * g.Ho * g.Wo;
+    return simt_conv_wgrad(g, x, gy, gw, part, simt_splits(g.N, g.k * g.k * g.C, P), st, PC_BF16);
+  }
+  int Kc = g.k * g.k * g.C;
+  long long P = (long long)g.B * g.Ho * g.Wo;
+  Params p = base_params(Kc, g.N, (int)P);
+  int splits = (int)umma_wgrad_splits(g);
+  p.kb_per_split = ceil_div(p.num_kb, splits);
+  splits = ceil_div(p.num_kb, p.kb_per_split);
+  int rc = make_map(&p.tma_b, gy, g.N, P, 1, g.N, 0, 64);
+  if (rc) return rc;
+  p.b_cb = 1LL << 40;
+  p.gsrc = static_cast<const __nv_bfloat16*>(x);
+  p.g = g;
+  p.o_ld = Kc;
+  if (splits > 1) {
+    p.out = part;
+    p.split_stride = (long long)g.N * Kc;
+    rc = launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, splits, st);
+    if (rc) return rc;
+    return reduce_partials(part, splits, (long long)g.N * Kc, gw, st);
+  }
+  p.out = gw;
+  return launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, 1, st);
 }
-size_t umma_conv_extra_ws(const pc_conv_geom&, int) { return 0; }
-int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const float* bias, void* y,
-                    int flags, cudaStream_t st) {
-  return simt_fc_forward(B, D, U, x, w, bias, y, PC_BF16, flags, st);
+
+static bool tma_view_ok(const pc_mat& v, long long inner_total) {
+  bool blocked = v.cb < inner_total;
+  return v.ld % 8 == 0 && (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0 &&
+         (!blocked || (v.cb % 64 == 0 && v.bstride % 8 == 0));
 }
+
+int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const float* bias, void* y, int flags,
+                    cudaStream_t st) {
+  if (!(tma_view_ok(x, D) && D % 8 == 0 && U % 8 == 0)) {
+    g_simt_launches++;
+    return simt_fc_forward(B, D, U, x, w, bias, y, PC_BF16, flags, st);
+  }
+  Params p = base_params(B, U, D);
+  long long cb = x.cb < D ? x.cb : D;
+  int rc = make_map(&p.tma_a, x.ptr, cb, B, D / cb, x.ld, x.bstride, BM);
+  if (rc) return rc;
+  p.a_cb = cb;
+  if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, bn_for(U)))) return rc;
+  p.b_cb = D;
+  p.out = y;
+  p.o_ld = U;
+  p.bias = bias;
+  p.relu = (flags & PC_RELU) != 0;
+  return launch_kb<A_TMA_K, EPI_BF16>(p, 1, st);
+}
+
 int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_mat& gx, const void* mask,
                   cudaStream_t st) {
-  return simt_fc_dgrad(B, D, U, w, gy, gx, mask, st, PC_BF16);
+  if (!(D % 8 == 0 && U % 8 == 0 && gx.ld % 8 == 0 && (gx.cb >= D || gx.cb % 8 == 0))) {
+    g_simt_launches++;
+    return simt_fc_dgrad(B, D, U, w, gy, gx, mask, st, PC_BF16);
+  }
+  Params p = base_params(B, D, U);
+  int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, BM);
+  if (rc) return rc;
+  p.a_cb = U;
+  if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, 64))) return rc;
+  p.b_cb = D;
+  p.out = gx.ptr;
+  p.o_ld = gx.ld;
+  p.o_cb = gx.cb;
+  p.o_bstride = gx.bstride;
+  p.mask = static_cast<const __nv_bfloat16*>(mask);
+  return launch_mn<A_TMA_K, EPI_BF16>(p, 1, st);
 }
+
 int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* gw, float*, cudaStream_t st) {
-  return simt_fc_wgrad(B, D, U, x, gy, gw, st, PC_BF16);
+  if (!(tma_view_ok(x, D) && D % 8 == 0 && U % 8 == 0)) {
+    g_simt_launches++;
+    return simt_fc_wgrad(B, D, U, x, gy, gw, st, PC_BF16);
+  }
+  Params p = base_params(U, D, B);
+  int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, 64);
+  if (rc) return rc;
+  p.a_cb = 1LL << 40;
+  long long cb = x.cb < D ? x.cb : D;
+  if ((rc = make_map(&p.tma_b, x.ptr, cb, B, D / cb, x.ld, x.bstride, 64))) return rc;
+  p.b_cb = cb;
+  p.out = gw;
+  p.o_ld = D;
+  return launch_mn<A_TMA_MN, EPI_F32>(p, 1, st);
 }
+
 size_t umma_fc_extra_ws(int, int, int, int) { return 0; }
 
 }  // namespace pc
+
+extern "C" PC_API void pc_contraction_counts(unsigned long long* tensor_core, unsigned long long* simt) {
+  if (tensor_core) *tensor_core = pc::umma::g_tc_launches.load();
+  if (simt) *simt = pc::umma::g_simt_launches.load();
+}

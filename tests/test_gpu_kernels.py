@@ -178,3 +178,58 @@ def test_maxpool_bf16_argmax_bit_exact():
     ry, rarg = O.maxpool_forward(x, 3, 2)
     assert np.array_equal(arg, rarg)
     assert np.array_equal(y, ry)
+
+
+# ------------------------------------------- tensor-core path coverage (bf16)
+
+def _tc_counts():
+    import ctypes
+    from paper_1312_5853_b200._lib import lib
+    a, b = ctypes.c_ulonglong(0), ctypes.c_ulonglong(0)
+    lib().dll.pc_contraction_counts(ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
+
+
+@pytest.mark.parametrize("geom", [(2, 96, 27, 27, 256, 5, 1, 2), (2, 256, 13, 13, 384, 3, 1, 1),
+                                  (2, 384, 13, 13, 256, 3, 1, 1), (1, 8, 67, 67, 96, 11, 4, 0),
+                                  (3, 16, 10, 10, 24, 3, 1, 1)])
+def test_conv_bf16_alexnet_shapes_on_tensor_cores(geom):
+    from paper_1312_5853_b200 import kernels as K
+    b, c, h, w, n, k, s, p = geom
+    rs = np.random.RandomState(11)
+    x = bf16(rs.randn(b, c, h, w))
+    wt = bf16(rs.randn(n, c, k, k) * (2.0 / (c * k * k)) ** 0.5)
+    bias = rs.randn(n).astype(np.float32).astype(np.float64) * 0.1
+    K.set_precision("bf16")
+    tc0, simt0 = _tc_counts()
+    cp = K.ConvParams(wt, bias, s, p)
+    y = K.conv2d_forward(x, cp)
+    yr = O.conv2d_forward(x, wt, bias, s, p)
+    assert rel(y, yr) < BF16_OUT_TOL
+    gy = bf16(rs.randn(*yr.shape))
+    gx, gw, gb = K.conv2d_backward(x, cp, gy)
+    rgx, rgw, rgb = O.conv2d_backward(x, wt, gy, s, p)
+    assert rel(gx, rgx) < BF16_OUT_TOL
+    assert rel(gw, rgw) < 1e-5
+    assert rel(gb, rgb) < 1e-5
+    tc1, simt1 = _tc_counts()
+    assert simt1 == simt0 and tc1 - tc0 >= 3      # fwd, dgrad, wgrad all on tcgen05
+
+
+@pytest.mark.parametrize("shape", [(256, 9216, 4096), (200, 4096, 1000), (64, 512, 128)])
+def test_fc_bf16_on_tensor_cores(shape):
+    from paper_1312_5853_b200 import kernels as K
+    b, d, u = shape
+    rs = np.random.RandomState(13)
+    x, w = bf16(rs.randn(b, d)), bf16(rs.randn(d, u) * d ** -0.5)
+    bias = rs.randn(u).astype(np.float32).astype(np.float64)
+    gy = bf16(rs.randn(b, u))
+    K.set_precision("bf16")
+    tc0, simt0 = _tc_counts()
+    assert rel(K.fc_forward(x, w, bias), O.fc_forward(x, w, bias)) < BF16_OUT_TOL
+    gx, gw, gb = K.fc_backward(x, w, gy)
+    rgx, rgw, rgb = O.fc_backward(x, w, gy)
+    assert rel(gx, rgx) < BF16_OUT_TOL
+    assert rel(gw, rgw) < 1e-5
+    tc1, simt1 = _tc_counts()
+    assert simt1 == simt0 and tc1 - tc0 == 3
