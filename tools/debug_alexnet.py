@@ -1,0 +1,39 @@
+"""Layer-by-layer error report of the device step vs the float64 oracle (AlexNet-227)."""
+import sys
+import numpy as np
+sys.path.insert(0, __file__.rsplit("/tools", 1)[0])
+import paper_1312_5853_b200 as P
+from oracle.ref_engine import OracleFabric
+from paper_1312_5853_b200.plan import plan_columnized
+
+prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+std = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+net = P.load_network("configs/alexnet.net")
+plan = P.ParallelPlan(1, 1)
+cs = plan_columnized(net, plan)
+init = P.init_dense_params(net, 0, std=std if std > 0 else None)
+dense = {i: {k: v.astype(np.float32).astype(np.float64) for k, v in t.items()} for i, t in init.items()}
+tr, _ = P.gen_synthetic(2, (B + 1) // 2, net.input_shape, seed=0)
+x, y = tr.images[:B], np.arange(B) * 7 % 1000
+trace = {}
+of = OracleFabric(net, plan, dense)
+ol = of.step(x, y, trace=trace)
+fab = P.spawn(1, precision=prec)
+P.setup_workers(fab, plan, cs, dense, P.SgdState())
+res = P.hybrid_step(fab, plan, cs, x, y)
+print(f"loss dev {res.loss:.8f} oracle {ol:.8f} rel {abs(res.loss-ol)/abs(ol):.2e}")
+eng = fab._engines[0]
+def rel(a, b): return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+def rl2(a, b): return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+for i, cl in enumerate(cs.col_layers):
+    st = eng.layers[i]
+    if st.kind == "softmax" or (st.kind == "relu" and st.relu_fused_fwd):
+        continue
+    ref = trace["fwd"][cl.index + 1 if st.relu_after else cl.index][0]
+    got = eng.activation_host(i, "out")
+    print(f"fwd L{cl.index:2d} {st.kind:5s} maxrel {rel(got, ref):.2e} relL2 {rl2(got, ref):.2e}")
+g = eng.grads_host()
+for i in sorted(g):
+    for k in ("w", "b"):
+        print(f"grad L{i:2d} {k} maxrel {rel(g[i][k], trace['grads'][0][i][k]):.2e} relL2 {rl2(g[i][k], trace['grads'][0][i][k]):.2e}")
