@@ -34,8 +34,13 @@ from paper_1312_5853_b200.plan import (
 from . import ref_kernels as K
 
 
-def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None):
-    """All m columns of one replica; returns (per-column losses, per-column grads)."""
+def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argmax=None):
+    """All m columns of one replica; returns (per-column losses, per-column grads).
+
+    ``force_argmax`` ({layer: [per-column argmax]}) replays another engine's
+    max-pool decisions ("teacher forcing"): where a window holds a near-tie
+    that float32 and float64 rank differently, the checker then measures the
+    arithmetic of the rest of the step instead of the tie's routing."""
     m = cs.columns
     acts = [np.asarray(x, dtype=np.float64)] * m
     caches = []
@@ -58,6 +63,8 @@ def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None):
                 o = K.relu_forward(a)
             elif isinstance(L, MaxPool):
                 o, cache[j]["arg"] = K.maxpool_forward(a, L.kernel, L.stride)
+                if force_argmax is not None and cl.index in force_argmax:
+                    cache[j]["arg"] = np.asarray(force_argmax[cl.index][j], dtype=np.int64)
             else:
                 losses[j], glog[j] = K.softmax_xent_scaled(a.reshape(a.shape[0], -1), labels, loss_scale)
                 o = glog[j]
@@ -133,7 +140,8 @@ class OracleFabric:
                          for j in range(m)]
         self.hyper = (lr, momentum, weight_decay)
 
-    def step(self, x, y, trace=None):
+    def step(self, x, y, trace=None, force_argmax=None):
+        """force_argmax: {layer: [replica][column] argmax arrays} (see column_fwd_bwd)."""
         d, m = self.plan.data_shards, self.plan.model_columns
         b = x.shape[0]
         if b % d:
@@ -144,8 +152,9 @@ class OracleFabric:
         total = 0.0
         for r in range(d):
             lo, hi = r * shard, (r + 1) * shard
+            fa = None if force_argmax is None else {k: v[r] for k, v in force_argmax.items()}
             losses, grads = column_fwd_bwd(self.cs, self.params, x[lo:hi], labels[lo:hi], scale,
-                                           trace=trace if r == 0 else None)
+                                           trace=trace if r == 0 else None, force_argmax=fa)
             per_replica.append(grads)
             total += losses[0]
         for j in range(m):

@@ -281,6 +281,16 @@ class ColumnEngine:
                 a = a[:, : self.in_c]
         return np.ascontiguousarray(a)
 
+    def pool_argmax_host(self) -> dict:
+        """{layer index: int64 NCHW local-window argmax} of the last forward pass."""
+        out = {}
+        for st in self.layers:
+            if st.kind == "pool":
+                ho, wo, c = st.out_nhwc
+                a = st.argmax[: self.B * ho * wo * c].cpu().numpy().reshape(self.B, ho, wo, c)
+                out[st.cl.index] = np.ascontiguousarray(a.transpose(0, 3, 1, 2)).astype(np.int64)
+        return out
+
     # ------------------------------------------------------------ step program
     @property
     def stream(self):
