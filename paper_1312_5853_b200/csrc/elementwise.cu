@@ -279,6 +279,26 @@ __global__ void nchw_to_nhwc_k(int B, int C, int H, int W, int Cp, const float* 
   dst[t] = cvt<T>(v);
 }
 
+// One CTA per image row (b, y): coalesced read of the C planes of that row into
+// shared memory, coalesced write of the W x Cp channels-last row.
+template <typename T>
+__global__ void nchw_to_nhwc_row_k(int C, int H, int W, int Cp, const float* __restrict__ src,
+                                   T* __restrict__ dst) {
+  extern __shared__ float row[];  // [C][W]
+  const int by = blockIdx.x;
+  const int b = by / H, y = by - b * H;
+  for (int t = threadIdx.x; t < C * W; t += blockDim.x) {
+    int c = t / W, x = t - c * W;
+    row[t] = src[(((long long)b * C + c) * H + y) * W + x];
+  }
+  __syncthreads();
+  T* out = dst + (long long)by * W * Cp;
+  for (int t = threadIdx.x; t < W * Cp; t += blockDim.x) {
+    int x = t / Cp, c = t - x * Cp;
+    out[t] = cvt<T>(c < C ? row[c * W + x] : 0.f);
+  }
+}
+
 template <typename T>
 __global__ void sum_buffers_k(int k, long long n, const void* const* __restrict__ src,
                               T* __restrict__ dst) {
@@ -419,8 +439,14 @@ extern "C" int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* 
   PC_REQUIRE(Cp >= C, PC_ESHAPE, "nchw_to_nhwc: Cp < C");
   long long n = (long long)B * H * W * Cp;
   if (n == 0) return PC_OK;
-  DISPATCH_PREC(prec, T, nchw_to_nhwc_k<T><<<grid_for(n, 256), 256, 0, S(st)>>>(
-      B, C, H, W, Cp, src, static_cast<T*>(dst)));
+  size_t row_bytes = sizeof(float) * (size_t)C * W;
+  if (row_bytes <= 48 * 1024) {
+    DISPATCH_PREC(prec, T, nchw_to_nhwc_row_k<T><<<B * H, 256, row_bytes, S(st)>>>(
+        C, H, W, Cp, src, static_cast<T*>(dst)));
+  } else {
+    DISPATCH_PREC(prec, T, nchw_to_nhwc_k<T><<<grid_for(n, 256), 256, 0, S(st)>>>(
+        B, C, H, W, Cp, src, static_cast<T*>(dst)));
+  }
   PC_CUDA_CHECK_LAUNCH("nchw_to_nhwc");
   return PC_OK;
 }

@@ -47,7 +47,7 @@ struct alignas(64) Params {
   int M, N, K;
   int num_kb;        // k-blocks in total
   int kb_per_split;  // k-blocks per grid.z slice
-  long long a_cb, b_cb;  // channel-block widths of the TMA views (k or mn index -> (idx % cb, idx / cb))
+  int a_cb, b_cb;  // channel-block width of a blocked TMA view (idx -> (idx % cb, idx / cb)); 0 = unblocked
   const __nv_bfloat16* gsrc;
   pc_conv_geom g;
   void* out;
@@ -132,6 +132,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+__device__ __forceinline__ int blk_off(int idx, int cb) { return cb ? (int)((unsigned)idx % (unsigned)cb) : idx; }
+__device__ __forceinline__ int blk_idx(int idx, int cb) { return cb ? (int)((unsigned)idx / (unsigned)cb) : 0; }
 
 // Shared-memory matrix descriptor, 128B swizzle (sm100 version bit 46 = 1).
 __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -222,25 +225,25 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
         if constexpr (B_MN) {
 #pragma unroll
           for (int c = 0; c < BN / 64; ++c) {
-            long long n = n0 + 64 * c;
-            tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), (int)(n % p.b_cb), kb * BK, (int)(n / p.b_cb));
+            int n = n0 + 64 * c;
+            tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK, blk_idx(n, p.b_cb));
           }
         } else {
-          long long k = (long long)kb * BK;
-          tma_load_3d(&p.tma_b, &full[s], dB, (int)(k % p.b_cb), n0, (int)(k / p.b_cb));
+          int k = kb * BK;
+          tma_load_3d(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
         }
         if constexpr (!GATHER) {
           const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES);
           if constexpr (A_MN) {
 #pragma unroll
             for (int c = 0; c < BM / 64; ++c) {
-              long long m = m0 + 64 * c;
-              tma_load_3d(&p.tma_a, &full[s], dA + c * (64 * BK * 2), (int)(m % p.a_cb), kb * BK,
-                          (int)(m / p.a_cb));
+              int m = m0 + 64 * c;
+              tma_load_3d(&p.tma_a, &full[s], dA + c * (64 * BK * 2), blk_off(m, p.a_cb), kb * BK,
+                          blk_idx(m, p.a_cb));
             }
           } else {
-            long long k = (long long)kb * BK;
-            tma_load_3d(&p.tma_a, &full[s], dA, (int)(k % p.a_cb), m0, (int)(k / p.a_cb));
+            int k = kb * BK;
+            tma_load_3d(&p.tma_a, &full[s], dA, blk_off(k, p.a_cb), m0, blk_idx(k, p.a_cb));
           }
         }
       }
@@ -279,12 +282,13 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          const long long k = (long long)(kb_begin + it) * BK + q * 8;
+          // 32-bit index math: 64-bit integer division is emulated (~100 instructions)
+          const int k = (kb_begin + it) * BK + q * 8;
           const bool kvalid = k < p.K;
           const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES);
           if constexpr (AM == A_GATHER_FWD) {
-            int c = kvalid ? (int)(k % g.C) : 0;
-            int ij = kvalid ? (int)(k / g.C) : 0;
+            int c = kvalid ? (int)((unsigned)k % (unsigned)g.C) : 0;
+            int ij = kvalid ? (int)((unsigned)k / (unsigned)g.C) : 0;
             int i = ij / g.k, j = ij - (ij / g.k) * g.k;
             int blk = c / g.cs, coff = c - blk * g.cs;
             const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
@@ -297,8 +301,8 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
               cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), src, ok);
             }
           } else {
-            int n = kvalid ? (int)(k % g.N) : 0;
-            int ij = kvalid ? (int)(k / g.N) : 0;
+            int n = kvalid ? (int)((unsigned)k % (unsigned)g.N) : 0;
+            int ij = kvalid ? (int)((unsigned)k / (unsigned)g.N) : 0;
             int i = ij / g.k, j = ij - (ij / g.k) * g.k;
             const __nv_bfloat16* src0 = p.gsrc + n;
 #pragma unroll
@@ -323,37 +327,39 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
       } else {
         // A_GATHER_WGRAD: MN-major rows = pixels (K), chunk q = 8 consecutive (i,j,c) of this M tile
         const int q = gt & 15, rb = gt >> 4;
-        const long long kc = (long long)m0 + q * 8;
+        const int kc = m0 + q * 8;
         const bool mvalid = kc < p.M;
-        int c = mvalid ? (int)(kc % g.C) : 0;
-        int ij = mvalid ? (int)(kc / g.C) : 0;
+        int c = mvalid ? (int)((unsigned)kc % (unsigned)g.C) : 0;
+        int ij = mvalid ? (int)((unsigned)kc / (unsigned)g.C) : 0;
         int i = ij / g.k, j = ij - (ij / g.k) * g.k;
         int blk = c / g.cs, coff = c - blk * g.cs;
         const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
-        const int hw = g.Ho * g.Wo;
+        const unsigned hw = (unsigned)(g.Ho * g.Wo);
         const uint32_t cofs = (q >> 3) * (64 * BK * 2);
         for (int it = 0; it < nkb; ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES) + cofs;
-          const long long pbase = (long long)(kb_begin + it) * BK;
+          // pixel of row rb (32-bit divides once per k-block), then step 8 pixels per row
+          const unsigned pix0 = (unsigned)((kb_begin + it) * BK + rb);
+          int b = (int)(pix0 / hw);
+          int rem = (int)(pix0 - (unsigned)b * hw);
+          int oy = rem / g.Wo;
+          int ox = rem - oy * g.Wo;
 #pragma unroll
           for (int r8 = 0; r8 < 8; ++r8) {
             int r = rb + 8 * r8;
-            long long pix = pbase + r;
-            bool ok = mvalid && pix < p.K;
-            int b = 0, oy = 0, ox = 0;
-            if (ok) {
-              b = (int)(pix / hw);
-              int rem = (int)(pix - (long long)b * hw);
-              oy = rem / g.Wo;
-              ox = rem - oy * g.Wo;
-            }
+            bool ok = mvalid && (int)pix0 + 8 * r8 < p.K;
             int iy = oy * g.stride + i - g.pad, ix = ox * g.stride + j - g.pad;
             ok = ok && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
             const __nv_bfloat16* src = ok ? src0 + ((long long)(b * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
             cp_async16(base + r * 128 + (((q & 7) ^ (r & 7)) << 4), src, ok);
+            ox += 8;
+            while (ox >= g.Wo) {
+              ox -= g.Wo;
+              if (++oy == g.Ho) { oy = 0; ++b; }
+            }
           }
           cp_async_arrive_noinc(&full[s]);
         }
@@ -532,7 +538,7 @@ static Params base_params(int M, int N, int K) {
   p.K = K;
   p.num_kb = ceil_div(K, BK);
   p.kb_per_split = p.num_kb;
-  p.a_cb = p.b_cb = 1LL << 40;
+  p.a_cb = p.b_cb = 0;
   p.o_cb = 1LL << 40;
   return p;
 }
@@ -563,7 +569,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   Params p = base_params(M, g.N, K);
   int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, bn_for(g.N));
   if (rc) return rc;
-  p.b_cb = K;
+  p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
   p.g = g;
   p.out = y;
@@ -611,7 +617,7 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
   Params p = base_params(M, g.C, K);
   int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, bn_for(g.C));
   if (rc) return rc;
-  p.b_cb = K;
+  p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(gy);
   p.g = g;
   p.out = gx;
@@ -650,7 +656,7 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   splits = ceil_div(p.num_kb, p.kb_per_split);
   int rc = make_map(&p.tma_b, gy, g.N, P, 1, g.N, 0, 64);
   if (rc) return rc;
-  p.b_cb = 1LL << 40;
+  p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
   p.g = g;
   p.o_ld = Kc;
@@ -681,9 +687,9 @@ int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const f
   long long cb = x.cb < D ? x.cb : D;
   int rc = make_map(&p.tma_a, x.ptr, cb, B, D / cb, x.ld, x.bstride, BM);
   if (rc) return rc;
-  p.a_cb = cb;
+  p.a_cb = cb < D ? (int)cb : 0;
   if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, bn_for(U)))) return rc;
-  p.b_cb = D;
+  p.b_cb = 0;
   p.out = y;
   p.o_ld = U;
   p.bias = bias;
@@ -700,9 +706,9 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
   Params p = base_params(B, D, U);
   int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, BM);
   if (rc) return rc;
-  p.a_cb = U;
+  p.a_cb = 0;
   if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, 64))) return rc;
-  p.b_cb = D;
+  p.b_cb = 0;
   p.out = gx.ptr;
   p.o_ld = gx.ld;
   p.o_cb = gx.cb;
@@ -719,10 +725,10 @@ int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* g
   Params p = base_params(U, D, B);
   int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, 64);
   if (rc) return rc;
-  p.a_cb = 1LL << 40;
+  p.a_cb = 0;
   long long cb = x.cb < D ? x.cb : D;
   if ((rc = make_map(&p.tma_b, x.ptr, cb, B, D / cb, x.ld, x.bstride, 64))) return rc;
-  p.b_cb = cb;
+  p.b_cb = cb < D ? (int)cb : 0;
   p.out = gw;
   p.o_ld = D;
   return launch_mn<A_TMA_MN, EPI_F32>(p, 1, st);
