@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -34,7 +35,13 @@
 namespace pc {
 namespace umma {
 
-enum AMode { A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FWD = 2, A_GATHER_DGRAD = 3, A_GATHER_WGRAD = 4 };
+// A operand sources: TMA tiled views, TMA im2col-mode loads (the hardware
+// walks output pixels across rows / images and zero-fills the padding), or the
+// cp.async gather kept for geometries the im2col box cannot express.
+enum AMode {
+  A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FWD = 2, A_GATHER_DGRAD = 3, A_GATHER_WGRAD = 4,
+  A_IM2COL_K = 5, A_IM2COL_MN = 6
+};
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2 };
 
@@ -56,6 +63,9 @@ struct alignas(64) Params {
   const float* bias;
   const __nv_bfloat16* mask;
   int relu;
+  // im2col-mode A: K index = (i, j, c) over i2c_C channels in blocks of i2c_cs,
+  // output-pixel walk over (i2c_Ho, i2c_Wo) with stride i2c_s from corner (lw, lh)
+  int i2c_C, i2c_cs, i2c_k, i2c_s, i2c_lw, i2c_lh, i2c_Wo, i2c_Ho;
 };
 
 // ----------------------------------------------------------------- PTX helpers
@@ -101,6 +111,17 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// im2col mode: {c, w, h, d, n} = (channel offset, pixel-walk start, batch, block),
+// im2col offsets {w, h, d} = filter tap (j, i, 0).
+__device__ __forceinline__ void tma_im2col_5d(const CUtensorMap* map, uint64_t* bar, uint32_t dst, int c, int w,
+                                              int h, int d, int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], {%8, %9, %10};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(d), "r"(n),
+      "h"(ow), "h"(oh), "h"((uint16_t)0)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -155,8 +176,8 @@ constexpr int tmem_cols() {
   return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
 }
 
-template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD; }
-template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD; }
+template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM <= A_GATHER_WGRAD; }
+template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN; }
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
@@ -215,6 +236,13 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
   if (warp == 5) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      int t_b = 0, t_oy = 0, t_ox = 0;  // first output pixel of this M tile (im2col K-major)
+      if constexpr (AM == A_IM2COL_K) {
+        t_ox = m0 % p.i2c_Wo;
+        const int t = m0 / p.i2c_Wo;
+        t_oy = t % p.i2c_Ho;
+        t_b = t / p.i2c_Ho;
+      }
       for (int it = 0; it < nkb; ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
@@ -232,7 +260,30 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
           int k = kb * BK;
           tma_load_3d(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
         }
-        if constexpr (!GATHER) {
+        if constexpr (AM == A_IM2COL_K) {
+          // 128 output pixels from the tile's first pixel; K block = 64 channels of tap (i, j)
+          const int k = kb * BK;
+          const int c = (int)((unsigned)k % (unsigned)p.i2c_C), ij = (int)((unsigned)k / (unsigned)p.i2c_C);
+          const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
+          const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
+          tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), coff, t_ox * p.i2c_s + p.i2c_lw,
+                        t_oy * p.i2c_s + p.i2c_lh, t_b, blk, (uint16_t)j, (uint16_t)i);
+        } else if constexpr (AM == A_IM2COL_MN) {
+          // K block = 64 consecutive pixels; M = (i, j, c): two 64-channel chunks
+          const unsigned pix0 = (unsigned)(kb * BK), hw = (unsigned)(p.i2c_Ho * p.i2c_Wo);
+          const int b = (int)(pix0 / hw), rem = (int)(pix0 - (unsigned)b * hw);
+          const int oy = rem / p.i2c_Wo, ox = rem - (rem / p.i2c_Wo) * p.i2c_Wo;
+#pragma unroll
+          for (int cch = 0; cch < BM / 64; ++cch) {
+            int kc = m0 + 64 * cch;
+            if (kc >= p.M) kc = m0;  // rows past M are discarded by the epilogue
+            const int c = (int)((unsigned)kc % (unsigned)p.i2c_C), ij = (int)((unsigned)kc / (unsigned)p.i2c_C);
+            const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
+            const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
+            tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES) + cch * (64 * BK * 2), coff,
+                          ox * p.i2c_s + p.i2c_lw, oy * p.i2c_s + p.i2c_lh, b, blk, (uint16_t)j, (uint16_t)i);
+          }
+        } else if constexpr (!GATHER) {
           const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES);
           if constexpr (A_MN) {
 #pragma unroll
@@ -490,6 +541,35 @@ static int make_map(CUtensorMap* map, const void* ptr, long long inner, long lon
   return PC_OK;
 }
 
+static PFN_cuTensorMapEncodeIm2col_v12000 g_encode_i2c = nullptr;
+static std::once_flag g_encode_i2c_once;
+
+// im2col view of a channel-blocked NHWC activation: dims {cs, W, H, B, nblk};
+// each load = `pixels` walked output positions x 64 channels (128 B rows, 128B swizzle).
+static int make_im2col_map(CUtensorMap* map, const void* ptr, int cs, int W, int H, int B, int nblk,
+                           long long cstride, int pixels, int lw, int lh, int uw, int uh, int stride) {
+  std::call_once(g_encode_i2c_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode_i2c = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(fn);
+  });
+  PC_REQUIRE(g_encode_i2c != nullptr, PC_ECUDA, "cuTensorMapEncodeIm2col unavailable");
+  PC_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && cs % 64 == 0, PC_EVALUE, "im2col view misaligned");
+  cuuint64_t dims[5] = {(cuuint64_t)cs, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)nblk};
+  cuuint64_t strides[4] = {(cuuint64_t)cs * 2, (cuuint64_t)W * cs * 2, (cuuint64_t)H * W * cs * 2,
+                           (cuuint64_t)(nblk > 1 ? cstride : (long long)B * H * W * cs) * 2};
+  int lower[3] = {lw, lh, 0}, upper[3] = {uw, uh, 0};
+  cuuint32_t estr[5] = {1u, (cuuint32_t)stride, (cuuint32_t)stride, 1u, 1u};
+  CUresult r = g_encode_i2c(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, lower,
+                            upper, 64u, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  PC_REQUIRE(r == CUDA_SUCCESS, PC_ECUDA, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
+  return PC_OK;
+}
+
 static std::atomic<unsigned long long> g_tc_launches{0}, g_simt_launches{0};
 
 template <int AM, int BMODE, int EPI, int BN, int STAGES>
@@ -555,6 +635,25 @@ bool umma_available() {
   return major == 10 && minor == 0 && get_encode();
 }
 
+// TMA im2col needs 64-channel (128 B) pixel rows within one channel block.
+static bool im2col_ok(int cs, int C, long long cstride) {
+  static const int enabled = [] {
+    const char* e = getenv("PC_IM2COL");
+    return e ? atoi(e) : 1;
+  }();
+  return enabled && cs % 64 == 0 && C % cs == 0 && (C == cs || cstride % 8 == 0);
+}
+
+static void set_i2c(Params& p, int C, int cs, int k, int s, int lo, int Wo, int Ho) {
+  p.i2c_C = C;
+  p.i2c_cs = cs;
+  p.i2c_k = k;
+  p.i2c_s = s;
+  p.i2c_lw = p.i2c_lh = lo;
+  p.i2c_Wo = Wo;
+  p.i2c_Ho = Ho;
+}
+
 static bool conv_tc_shape(const pc_conv_geom& g) {
   return g.C % 8 == 0 && g.cs % 8 == 0 && g.N % 8 == 0 && (g.C == g.cs || g.cstride % 8 == 0);
 }
@@ -576,12 +675,19 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   p.o_ld = g.N;
   p.bias = bias;
   p.relu = (flags & PC_RELU) != 0;
+  if (im2col_ok(g.cs, g.C, g.cstride)) {
+    rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, BM, -g.pad, -g.pad,
+                         g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
+    if (rc) return rc;
+    set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
+    return launch_kb<A_IM2COL_K, EPI_BF16>(p, 1, st);
+  }
   return launch_kb<A_GATHER_FWD, EPI_BF16>(p, 1, st);
 }
 
 __global__ void transpose_w_k(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt, int N, int KK,
-                              int C) {
-  // wt[c][ij][n] = w[n][ij][c]
+                              int C, int flip) {
+  // wt[c][ij][n] = w[n][ij][c]; flip: wt[c][ij][n] = w[n][KK-1-ij][c] (180-degree filter rotation)
   long long total = (long long)N * KK * C;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -589,7 +695,7 @@ __global__ void transpose_w_k(const __nv_bfloat16* __restrict__ w, __nv_bfloat16
     long long r = t / N;
     int ij = (int)(r % KK);
     int c = (int)(r / KK);
-    wt[t] = w[((long long)n * KK + ij) * C + c];
+    wt[t] = w[((long long)n * KK + (flip ? KK - 1 - ij : ij)) * C + c];
   }
 }
 
@@ -611,7 +717,8 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
       (reinterpret_cast<uintptr_t>(ws) + ws_bytes - need) & ~uintptr_t(127));
   long long total = (long long)g.N * KK * g.C;
   int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
-  transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C);
+  const bool i2c = g.stride == 1 && im2col_ok(g.N, g.N, 0) && g.H + 2 * g.pad - g.k + 1 == g.Ho;
+  transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C, i2c ? 1 : 0);
   PC_CUDA_CHECK_LAUNCH("transpose_w");
   int M = g.B * g.H * g.W, K = KK * g.N;
   Params p = base_params(M, g.C, K);
@@ -625,6 +732,15 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
   p.o_cb = g.cs;
   p.o_bstride = g.cstride;
   p.mask = static_cast<const __nv_bfloat16*>(mask);
+  if (i2c) {
+    // dgrad = forward conv of gy with the rotated filter, corner p-(k-1), walking dx's H x W
+    const int lo = g.pad - (g.k - 1);
+    rc = make_im2col_map(&p.tma_a, gy, g.N, g.Wo, g.Ho, g.B, 1, 0, BM, lo, lo, lo + g.W - g.Wo,
+                         lo + g.H - g.Ho, 1);
+    if (rc) return rc;
+    set_i2c(p, g.N, g.N, g.k, 1, lo, g.W, g.H);
+    return launch_kb<A_IM2COL_K, EPI_BF16>(p, 1, st);
+  }
   return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, 1, st);
 }
 
@@ -660,15 +776,18 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
   p.g = g;
   p.o_ld = Kc;
-  if (splits > 1) {
-    p.out = part;
-    p.split_stride = (long long)g.N * Kc;
-    rc = launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, splits, st);
+  const bool i2c = im2col_ok(g.cs, g.C, g.cstride);
+  if (i2c) {
+    rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, 64, -g.pad, -g.pad,
+                         g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
     if (rc) return rc;
-    return reduce_partials(part, splits, (long long)g.N * Kc, gw, st);
+    set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
   }
-  p.out = gw;
-  return launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, 1, st);
+  p.out = splits > 1 ? static_cast<void*>(part) : static_cast<void*>(gw);
+  p.split_stride = splits > 1 ? (long long)g.N * Kc : 0;
+  rc = i2c ? launch_mn<A_IM2COL_MN, EPI_F32_T>(p, splits, st) : launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, splits, st);
+  if (rc || splits == 1) return rc;
+  return reduce_partials(part, splits, (long long)g.N * Kc, gw, st);
 }
 
 static bool tma_view_ok(const pc_mat& v, long long inner_total) {
