@@ -61,12 +61,21 @@ __global__ void colsum1_k(const T* __restrict__ g, long long P, int N, float* __
   for (long long r = r0; r < r1; ++r) acc += ld(g + r * N + c);
   part[(long long)blockIdx.y * N + c] = acc;
 }
+// 32 columns x 8 row lanes per CTA; lanes combine in a fixed order (deterministic).
 __global__ void colsum2_k(const float* __restrict__ part, int R, int N, float* __restrict__ out) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
+  __shared__ float sh[8][33];
+  const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cx;
   float acc = 0.f;
-  for (int r = 0; r < R; ++r) acc += part[(long long)r * N + c];
-  out[c] = acc;
+  if (c < N)
+    for (int r = ry; r < R; r += 8) acc += part[(long long)r * N + c];
+  sh[ry][cx] = acc;
+  __syncthreads();
+  if (ry == 0 && c < N) {
+    float t = sh[0][cx];
+    for (int k = 1; k < 8; ++k) t += sh[k][cx];
+    out[c] = t;
+  }
 }
 
 int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, cudaStream_t st) {
@@ -81,7 +90,7 @@ int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, c
     colsum1_k<float><<<g1, 128, 0, st>>>(static_cast<const float*>(g), P, N, ws);
   else
     colsum1_k<__nv_bfloat16><<<g1, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(g), P, N, ws);
-  colsum2_k<<<(N + 127) / 128, 128, 0, st>>>(ws, R, N, out);
+  colsum2_k<<<(N + 31) / 32, 256, 0, st>>>(ws, R, N, out);
   count_launches(1);
   PC_CUDA_CHECK_LAUNCH("colsum");
   return PC_OK;

@@ -279,6 +279,43 @@ __global__ void nchw_to_nhwc_k(int B, int C, int H, int W, int Cp, const float* 
   dst[t] = cvt<T>(v);
 }
 
+// Explicit im2col for the network's input layer: col[pixel][(c*k + i)*k + j]
+// (the reference's K order, kernels.py:94-100) = x[b][c][oy*s+i-p][ox*s+j-p],
+// zero-padded to Kp columns, straight from the float32 NCHW batch. One CTA per
+// output row (b, oy): the C*k input rows it needs are staged in shared memory,
+// then the Wo x Kp output rows are written with 16-byte stores.
+__global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, int Wo, int Kp,
+                              const float* __restrict__ x, __nv_bfloat16* __restrict__ col) {
+  extern __shared__ float rows[];  // [C][k][W]
+  const int bo = blockIdx.x;
+  const int b = bo / Ho, oy = bo - b * Ho;
+  for (int t = threadIdx.x; t < C * k * W; t += blockDim.x) {
+    int xw = t % W, r = t / W;
+    int i = r % k, c = r / k;
+    int iy = oy * s + i - p;
+    rows[t] = (iy >= 0 && iy < H) ? x[(((long long)b * C + c) * H + iy) * W + xw] : 0.f;
+  }
+  __syncthreads();
+  const int K = C * k * k, chunks = Kp / 8;
+  __nv_bfloat16* out = col + (long long)bo * Wo * Kp;
+  for (int t = threadIdx.x; t < Wo * chunks; t += blockDim.x) {
+    int ox = t / chunks, q = t - ox * chunks;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      int kk = q * 8 + e;
+      float val = 0.f;
+      if (kk < K) {
+        int j = kk % k, r = kk / k;  // r = c*k + i
+        int ix = ox * s + j - p;
+        if (ix >= 0 && ix < W) val = rows[r * W + ix];
+      }
+      v[e] = val;
+    }
+    Vec8<__nv_bfloat16>::store(out + (long long)ox * Kp + q * 8, v);
+  }
+}
+
 // One CTA per image row (b, y): coalesced read of the C planes of that row into
 // shared memory, coalesced write of the W x Cp channels-last row.
 template <typename T>
@@ -448,6 +485,23 @@ extern "C" int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* 
         B, C, H, W, Cp, src, static_cast<T*>(dst)));
   }
   PC_CUDA_CHECK_LAUNCH("nchw_to_nhwc");
+  return PC_OK;
+}
+
+extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const float* src, void* dst,
+                         pc_stream_t st) {
+  PC_REQUIRE(B >= 0 && C > 0 && k > 0 && s > 0 && p >= 0 && Kp % 8 == 0 && Kp >= C * k * k, PC_EVALUE,
+             "im2col: bad arguments (Kp must be a multiple of 8 and >= C*k*k)");
+  int sh = H + 2 * p - k, sw = W + 2 * p - k;
+  PC_REQUIRE(sh >= 0 && sw >= 0 && sh % s == 0 && sw % s == 0, PC_EVALUE, "im2col: geometry does not tile");
+  int Ho = sh / s + 1, Wo = sw / s + 1;
+  size_t smem = sizeof(float) * (size_t)C * k * W;
+  PC_REQUIRE(smem <= 200 * 1024, PC_EVALUE, "im2col: input rows do not fit shared memory");
+  if (B == 0) return PC_OK;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(im2col_rows_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  im2col_rows_k<<<B * Ho, 256, smem, S(st)>>>(C, H, W, k, s, p, Ho, Wo, Kp, src,
+                                              static_cast<__nv_bfloat16*>(dst));
+  PC_CUDA_CHECK_LAUNCH("im2col");
   return PC_OK;
 }
 

@@ -836,7 +836,19 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
   return launch_mn<A_TMA_K, EPI_BF16>(p, 1, st);
 }
 
-int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* gw, float*, cudaStream_t st) {
+// Split-K for the weight gradient when the reduction (the batch, or the pixel
+// count of an explicit-im2col convolution) is long and the output tiles few.
+static int fc_wgrad_splits(int B, int D, int U) {
+  long long tiles = (long long)ceil_div(U, BM) * ceil_div(D, D <= 64 ? 64 : D <= 128 ? 128 : 256);
+  long long kbs = (B + BK - 1) / BK;
+  long long want = (2 * 148 + tiles - 1) / tiles;
+  long long cap = kbs / 8;
+  if (want > cap) want = cap;
+  if (want > 64) want = 64;
+  return (int)(want < 1 ? 1 : want);
+}
+
+int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* gw, float* part, cudaStream_t st) {
   if (!(tma_view_ok(x, D) && D % 8 == 0 && U % 8 == 0)) {
     g_simt_launches++;
     return simt_fc_wgrad(B, D, U, x, gy, gw, st, PC_BF16);
@@ -848,12 +860,27 @@ int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* g
   long long cb = x.cb < D ? x.cb : D;
   if ((rc = make_map(&p.tma_b, x.ptr, cb, B, D / cb, x.ld, x.bstride, 64))) return rc;
   p.b_cb = cb < D ? (int)cb : 0;
-  p.out = gw;
   p.o_ld = D;
-  return launch_mn<A_TMA_MN, EPI_F32>(p, 1, st);
+  int splits = fc_wgrad_splits(B, D, U);
+  p.kb_per_split = ceil_div(p.num_kb, splits);
+  splits = ceil_div(p.num_kb, p.kb_per_split);
+  if (splits == 1 || part == nullptr) {
+    p.kb_per_split = p.num_kb;
+    p.out = gw;
+    return launch_mn<A_TMA_MN, EPI_F32>(p, 1, st);
+  }
+  p.out = part;
+  p.split_stride = (long long)U * D;
+  rc = launch_mn<A_TMA_MN, EPI_F32>(p, splits, st);
+  if (rc) return rc;
+  return reduce_partials(part, splits, (long long)U * D, gw, st);
 }
 
-size_t umma_fc_extra_ws(int, int, int, int) { return 0; }
+size_t umma_fc_extra_ws(int B, int D, int U, int prec) {
+  if (prec != PC_BF16) return 0;
+  int s = fc_wgrad_splits(B, D, U);
+  return s > 1 ? (size_t)s * U * D * sizeof(float) : 0;
+}
 
 }  // namespace pc
 

@@ -65,6 +65,7 @@ class LayerState:
     perm: np.ndarray | None = None       # FC row permutation (reference <-> device)
     geom: object = None
     row_loss: torch.Tensor | None = None
+    col: int = 0                         # explicit-im2col input conv: padded K (0 = implicit GEMM)
 
 
 class ColumnEngine:
@@ -96,9 +97,17 @@ class ColumnEngine:
         first = cs.col_layers[0]
         self.in_c = c
         self.in_cp = c
-        if self.prec == L.PC_BF16 and isinstance(first.layer, Conv) and c % 8:
-            self.in_cp = (c + 7) // 8 * 8
-        self.x = self._new(B * h * w * self.in_cp)
+        # bf16 input conv with channels too narrow for 128-byte im2col rows (AlexNet:
+        # 3): materialise its columns once per step (pc_im2col) and run it as a
+        # dense GEMM over pixels; col_kp = padded K (reference (c, i, j) order).
+        self.col_kp = 0
+        if self.prec == L.PC_BF16 and isinstance(first.layer, Conv) and c % 64:
+            k0 = first.layer.kernel
+            self.col_kp = (c * k0 * k0 + 7) // 8 * 8
+            ho0, wo0 = first.out_shape[1], first.out_shape[2]
+            self.x = self._new(B * ho0 * wo0 * self.col_kp)
+        else:
+            self.x = self._new(B * h * w * self.in_cp)
         prev_out, prev_shape = self.x, (h, w, self.in_cp)
         n = len(cs.col_layers)
         for i, cl in enumerate(cs.col_layers):
@@ -119,7 +128,9 @@ class ColumnEngine:
                 ho = (hh + 2 * layer.pad - layer.kernel) // layer.stride + 1
                 wo = (ww + 2 * layer.pad - layer.kernel) // layer.stride + 1
                 nout = cl.out_shape[0]
-                if cc % 8 and self.prec == L.PC_BF16:
+                if i == 0 and self.col_kp:
+                    st.col = self.col_kp
+                elif cc % 8 and self.prec == L.PC_BF16:
                     raise ValidationError(f"layer {cl.index}: bf16 conv needs C % 8 == 0 (C={cc})")
                 st.cp = cc
                 cs_blk = cc // st.in_blocks
@@ -178,7 +189,7 @@ class ColumnEngine:
         for st in self.layers:
             if st.kind not in ("conv", "fc"):
                 continue
-            st.w_shape = layout.device_weight_shape(st.cl, st.cp)
+            st.w_shape = (st.cl.weight_shape[0], st.col) if st.col else layout.device_weight_shape(st.cl, st.cp)
             st.w_off = off
             off += -(-layout.numel(st.w_shape) // ALIGN) * ALIGN
             st.b_off = off
@@ -198,7 +209,10 @@ class ColumnEngine:
         self.set_grad_source(self.g32)
         ws = 0
         for st in self.layers:
-            if st.kind == "conv":
+            if st.kind == "conv" and st.col:
+                g = st.geom
+                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B * g.Ho * g.Wo, st.col, g.N, self.prec))
+            elif st.kind == "conv":
                 ws = max(ws, self.lib.raw("pc_conv2d_backward_workspace")(C.byref(st.geom), self.prec))
             elif st.kind == "fc":
                 d = math.prod(st.in_nhwc)
@@ -228,7 +242,13 @@ class ColumnEngine:
                 if tree is None:
                     continue
                 w = tree[idx]["w"]
-                dw = layout.conv_to_device(w, st.cp) if st.kind == "conv" else layout.fc_to_device(w, st.perm)
+                if st.col:
+                    dw = np.zeros(st.w_shape, dtype=np.float32)
+                    dw[:, : w[0].size] = w.reshape(w.shape[0], -1)
+                elif st.kind == "conv":
+                    dw = layout.conv_to_device(w, st.cp)
+                else:
+                    dw = layout.fc_to_device(w, st.perm)
                 buf[st.w_off:st.w_off + dw.size] = dw.ravel()
                 b = np.asarray(tree[idx]["b"], dtype=np.float32)
                 buf[st.b_off:st.b_off + b.size] = b
@@ -244,7 +264,9 @@ class ColumnEngine:
                 continue
             n = layout.numel(st.w_shape)
             wd = flat[st.w_off:st.w_off + n].reshape(st.w_shape)
-            if st.kind == "conv":
+            if st.col:
+                w = wd[:, : math.prod(st.cl.weight_shape[1:])].reshape(st.cl.weight_shape).astype(np.float64)
+            elif st.kind == "conv":
                 w = layout.conv_from_device(wd, st.cl.weight_shape[1])
             else:
                 w = layout.fc_from_device(wd, st.perm)
@@ -310,13 +332,24 @@ class ColumnEngine:
     def load_batch(self, x_nchw: torch.Tensor, labels_i32: torch.Tensor):
         """x_nchw: device float32 (B, C, H, W) slice of the global batch."""
         c, h, w = self.cs.base.input_shape
-        self.lib.call("pc_nchw_to_nhwc", self.B, c, h, w, self.in_cp, x_nchw.data_ptr(),
-                      self.x.data_ptr(), self.prec, self.stream)
+        if self.col_kp:
+            lay = self.cs.col_layers[0].layer
+            self.lib.call("pc_im2col", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
+                          x_nchw.data_ptr(), self.x.data_ptr(), self.stream)
+        else:
+            self.lib.call("pc_nchw_to_nhwc", self.B, c, h, w, self.in_cp, x_nchw.data_ptr(),
+                          self.x.data_ptr(), self.prec, self.stream)
         self.labels[: self.B].copy_(labels_i32, non_blocking=True)
 
     def forward(self, i: int, loss_scale: float):
         st, lib, s = self.layers[i], self.lib, self.stream
-        if st.kind == "conv":
+        if st.kind == "conv" and st.col:
+            g = st.geom
+            mat = L.Mat(st.inp.data_ptr(), st.col, st.col, 0)
+            self._call(st, "pc_fc_forward", self.B * g.Ho * g.Wo, st.col, g.N, C.byref(mat), self._w_lowp(st),
+                       self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec,
+                       L.PC_RELU if st.relu_after else 0, s)
+        elif st.kind == "conv":
             flags = L.PC_RELU if st.relu_after else 0
             self._call(st, "pc_conv2d_forward", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
                      self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, s)
@@ -349,7 +382,14 @@ class ColumnEngine:
     def backward(self, i: int):
         st, lib, s = self.layers[i], self.lib, self.stream
         want_dx = i > 0
-        if st.kind == "conv":
+        if st.kind == "conv" and st.col:      # input layer: weight / bias gradients only
+            g = st.geom
+            mat = L.Mat(st.inp.data_ptr(), st.col, st.col, 0)
+            self._call(st, "pc_fc_backward", self.B * g.Ho * g.Wo, st.col, g.N, C.byref(mat), self._w_lowp(st),
+                       st.gout.data_ptr(), C.byref(mat), None, self.g32[st.w_off:].data_ptr(),
+                       self.g32[st.b_off:].data_ptr(), self.prec, L.PC_WANT_DW, self.ws.data_ptr(),
+                       self.ws_bytes, s)
+        elif st.kind == "conv":
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             self._call(st, "pc_conv2d_backward", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
                      st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
