@@ -53,7 +53,8 @@ struct alignas(64) Params {
   CUtensorMap tma_b;
   int M, N, K;
   int num_kb;        // k-blocks in total
-  int kb_per_split;  // k-blocks per grid.z slice
+  int kb_per_split;  // k-blocks per split-K slice
+  int tiles;         // split slices x M tiles x N tiles (persistent walk)
   int a_cb, b_cb;  // channel-block width of a blocked TMA view (idx -> (idx % cb, idx / cb)); 0 = unblocked
   const __nv_bfloat16* gsrc;
   pc_conv_geom g;
@@ -181,10 +182,37 @@ template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GA
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-  return 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
+  return 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
 }
 
 // ------------------------------------------------------------------- kernel
+// Persistent: each CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
+// (tile order: split-K slice, then M, then N fastest). The smem stage ring runs
+// continuously across tiles, and with two TMEM accumulators the epilogue of
+// tile t overlaps the mainloop of tile t+1.
+template <int BN>
+constexpr int acc_count() { return 2 * tmem_cols<BN>() <= 512 ? 2 : 1; }
+
+struct TileCoord {
+  int m0, n0, z, kb_begin, nkb;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const Params& p, int t, int bn) {
+  const int tn = (p.N + bn - 1) / bn, tm = (p.M + BM - 1) / BM;
+  TileCoord c;
+  c.z = t / (tm * tn);
+  const int r = t - c.z * (tm * tn);
+  c.m0 = (r / tn) * BM;
+  c.n0 = (r - (r / tn) * tn) * bn;
+  c.kb_begin = c.z * p.kb_per_split;
+  c.nkb = max(min(p.num_kb, c.kb_begin + p.kb_per_split) - c.kb_begin, 0);
+  return c;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <int AM, int BMODE, int EPI, int BN, int STAGES>
 __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
     umma_gemm_k(const __grid_constant__ Params p) {
@@ -194,6 +222,7 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
   constexpr int B_STAGE_BYTES = BN * BK * 2;
   constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN>();
   constexpr int TCOLS = tmem_cols<BN>();
+  constexpr int ACC = acc_count<BN>();
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -201,14 +230,12 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;  // [ACC]
+  uint64_t* tempty = tfull + 2;      // [ACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int kb_begin = blockIdx.z * p.kb_per_split;
-  const int kb_end = min(p.num_kb, kb_begin + p.kb_per_split);
-  const int nkb = max(kb_end - kb_begin, 0);
+  const int total = p.tiles;
 
   if (warp == 4) {
     if (lane == 0) {
@@ -216,12 +243,15 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
         mbar_init(&full[s], 1 + (GATHER ? 128 : 0));
         mbar_init(&empty[s], 1);
       }
-      mbar_init(tmem_full, 1);
+      for (int a = 0; a < ACC; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], 4);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TCOLS));
+                 "r"(TCOLS * ACC));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (warp == 5 && lane == 0) {
@@ -236,65 +266,73 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
   if (warp == 5) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int t_b = 0, t_oy = 0, t_ox = 0;  // first output pixel of this M tile (im2col K-major)
-      if constexpr (AM == A_IM2COL_K) {
-        t_ox = m0 % p.i2c_Wo;
-        const int t = m0 / p.i2c_Wo;
-        t_oy = t % p.i2c_Ho;
-        t_b = t / p.i2c_Ho;
-      }
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        const int kb = kb_begin + it;
-        mbar_arrive_expect_tx(&full[s], B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES));
-        const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
-        if constexpr (B_MN) {
-#pragma unroll
-          for (int c = 0; c < BN / 64; ++c) {
-            int n = n0 + 64 * c;
-            tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK, blk_idx(n, p.b_cb));
-          }
-        } else {
-          int k = kb * BK;
-          tma_load_3d(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
-        }
+      int git = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord tc = tile_coord(p, t, BN);
+        const int m0 = tc.m0, n0 = tc.n0;
+        int t_b = 0, t_oy = 0, t_ox = 0;  // first output pixel of this M tile (im2col K-major)
         if constexpr (AM == A_IM2COL_K) {
-          // 128 output pixels from the tile's first pixel; K block = 64 channels of tap (i, j)
-          const int k = kb * BK;
-          const int c = (int)((unsigned)k % (unsigned)p.i2c_C), ij = (int)((unsigned)k / (unsigned)p.i2c_C);
-          const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
-          const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
-          tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), coff, t_ox * p.i2c_s + p.i2c_lw,
-                        t_oy * p.i2c_s + p.i2c_lh, t_b, blk, (uint16_t)j, (uint16_t)i);
-        } else if constexpr (AM == A_IM2COL_MN) {
-          // K block = 64 consecutive pixels; M = (i, j, c): two 64-channel chunks
-          const unsigned pix0 = (unsigned)(kb * BK), hw = (unsigned)(p.i2c_Ho * p.i2c_Wo);
-          const int b = (int)(pix0 / hw), rem = (int)(pix0 - (unsigned)b * hw);
-          const int oy = rem / p.i2c_Wo, ox = rem - (rem / p.i2c_Wo) * p.i2c_Wo;
+          t_ox = m0 % p.i2c_Wo;
+          const int q = m0 / p.i2c_Wo;
+          t_oy = q % p.i2c_Ho;
+          t_b = q / p.i2c_Ho;
+        }
+        for (int it = 0; it < tc.nkb; ++it, ++git) {
+          const int s = git % STAGES;
+          const uint32_t ph = (git / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const int kb = tc.kb_begin + it;
+          mbar_arrive_expect_tx(&full[s], B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES));
+          const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
+          if constexpr (B_MN) {
 #pragma unroll
-          for (int cch = 0; cch < BM / 64; ++cch) {
-            int kc = m0 + 64 * cch;
-            if (kc >= p.M) kc = m0;  // rows past M are discarded by the epilogue
-            const int c = (int)((unsigned)kc % (unsigned)p.i2c_C), ij = (int)((unsigned)kc / (unsigned)p.i2c_C);
-            const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
-            const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
-            tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES) + cch * (64 * BK * 2), coff,
-                          ox * p.i2c_s + p.i2c_lw, oy * p.i2c_s + p.i2c_lh, b, blk, (uint16_t)j, (uint16_t)i);
-          }
-        } else if constexpr (!GATHER) {
-          const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES);
-          if constexpr (A_MN) {
-#pragma unroll
-            for (int c = 0; c < BM / 64; ++c) {
-              int m = m0 + 64 * c;
-              tma_load_3d(&p.tma_a, &full[s], dA + c * (64 * BK * 2), blk_off(m, p.a_cb), kb * BK,
-                          blk_idx(m, p.a_cb));
+            for (int c = 0; c < BN / 64; ++c) {
+              int n = n0 + 64 * c;
+              tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK,
+                          blk_idx(n, p.b_cb));
             }
           } else {
             int k = kb * BK;
-            tma_load_3d(&p.tma_a, &full[s], dA, blk_off(k, p.a_cb), m0, blk_idx(k, p.a_cb));
+            tma_load_3d(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
+          }
+          if constexpr (AM == A_IM2COL_K) {
+            // 128 output pixels from the tile's first pixel; K block = 64 channels of tap (i, j)
+            const int k = kb * BK;
+            const int c = (int)((unsigned)k % (unsigned)p.i2c_C), ij = (int)((unsigned)k / (unsigned)p.i2c_C);
+            const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
+            const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
+            tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), coff,
+                          t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, blk, (uint16_t)j,
+                          (uint16_t)i);
+          } else if constexpr (AM == A_IM2COL_MN) {
+            // K block = 64 consecutive pixels; M = (i, j, c): two 64-channel chunks
+            const unsigned pix0 = (unsigned)(kb * BK), hw = (unsigned)(p.i2c_Ho * p.i2c_Wo);
+            const int b = (int)(pix0 / hw), rem = (int)(pix0 - (unsigned)b * hw);
+            const int oy = rem / p.i2c_Wo, ox = rem - (rem / p.i2c_Wo) * p.i2c_Wo;
+#pragma unroll
+            for (int cch = 0; cch < BM / 64; ++cch) {
+              int kc = m0 + 64 * cch;
+              if (kc >= p.M) kc = m0;  // rows past M are discarded by the epilogue
+              const int c = (int)((unsigned)kc % (unsigned)p.i2c_C),
+                        ij = (int)((unsigned)kc / (unsigned)p.i2c_C);
+              const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
+              const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
+              tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES) + cch * (64 * BK * 2), coff,
+                            ox * p.i2c_s + p.i2c_lw, oy * p.i2c_s + p.i2c_lh, b, blk, (uint16_t)j, (uint16_t)i);
+            }
+          } else if constexpr (!GATHER) {
+            const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES);
+            if constexpr (A_MN) {
+#pragma unroll
+              for (int c = 0; c < BM / 64; ++c) {
+                int m = m0 + 64 * c;
+                tma_load_3d(&p.tma_a, &full[s], dA + c * (64 * BK * 2), blk_off(m, p.a_cb), kb * BK,
+                            blk_idx(m, p.a_cb));
+              }
+            } else {
+              int k = kb * BK;
+              tma_load_3d(&p.tma_a, &full[s], dA, blk_off(k, p.a_cb), m0, blk_idx(k, p.a_cb));
+            }
           }
         }
       }
@@ -304,199 +342,224 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
     if constexpr (GATHER) {
       const int gt = threadIdx.x - 192;
       const pc_conv_geom& g = p.g;
-      if constexpr (AM == A_GATHER_FWD || AM == A_GATHER_DGRAD) {
-        // K-major rows = pixels; thread owns 16B chunk q of rows rb + 16*it
-        const int q = gt & 7, rb = gt >> 3;
-        int rb_b[8], ry[8], rx[8];
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          int m = m0 + rb + 16 * it;
-          int W_ = AM == A_GATHER_FWD ? g.Wo : g.W, H_ = AM == A_GATHER_FWD ? g.Ho : g.H;
-          if (m < p.M) {
-            int x = m % W_, t = m / W_;
-            int y = t % H_;
-            rb_b[it] = t / H_;
-            if constexpr (AM == A_GATHER_FWD) {
-              ry[it] = y * g.stride - g.pad;
-              rx[it] = x * g.stride - g.pad;
-            } else {
-              ry[it] = y + g.pad;
-              rx[it] = x + g.pad;
-            }
-          } else {
-            rb_b[it] = 0;
-            ry[it] = -(1 << 28);
-            rx[it] = -(1 << 28);
-          }
-        }
-        for (int it = 0; it < nkb; ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          // 32-bit index math: 64-bit integer division is emulated (~100 instructions)
-          const int k = (kb_begin + it) * BK + q * 8;
-          const bool kvalid = k < p.K;
-          const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES);
-          if constexpr (AM == A_GATHER_FWD) {
-            int c = kvalid ? (int)((unsigned)k % (unsigned)g.C) : 0;
-            int ij = kvalid ? (int)((unsigned)k / (unsigned)g.C) : 0;
-            int i = ij / g.k, j = ij - (ij / g.k) * g.k;
-            int blk = c / g.cs, coff = c - blk * g.cs;
-            const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
-#pragma unroll
-            for (int r8 = 0; r8 < 8; ++r8) {
-              int r = rb + 16 * r8;
-              int iy = ry[r8] + i, ix = rx[r8] + j;
-              bool ok = kvalid && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
-              const __nv_bfloat16* src = ok ? src0 + ((long long)(rb_b[r8] * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
-              cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), src, ok);
-            }
-          } else {
-            int n = kvalid ? (int)((unsigned)k % (unsigned)g.N) : 0;
-            int ij = kvalid ? (int)((unsigned)k / (unsigned)g.N) : 0;
-            int i = ij / g.k, j = ij - (ij / g.k) * g.k;
-            const __nv_bfloat16* src0 = p.gsrc + n;
-#pragma unroll
-            for (int r8 = 0; r8 < 8; ++r8) {
-              int r = rb + 16 * r8;
-              int ny = ry[r8] - i, nx = rx[r8] - j;
-              bool ok = kvalid && ny >= 0 && nx >= 0;
-              int oy = 0, ox = 0;
-              if (g.stride == 1) {
-                oy = ny; ox = nx;
-              } else {
-                ok = ok && (ny % g.stride == 0) && (nx % g.stride == 0);
-                oy = ny / g.stride; ox = nx / g.stride;
-              }
-              ok = ok && oy < g.Ho && ox < g.Wo;
-              const __nv_bfloat16* src = ok ? src0 + ((long long)(rb_b[r8] * g.Ho + oy) * g.Wo + ox) * g.N : p.gsrc;
-              cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), src, ok);
-            }
-          }
-          cp_async_arrive_noinc(&full[s]);
-        }
-      } else {
-        // A_GATHER_WGRAD: MN-major rows = pixels (K), chunk q = 8 consecutive (i,j,c) of this M tile
-        const int q = gt & 15, rb = gt >> 4;
-        const int kc = m0 + q * 8;
-        const bool mvalid = kc < p.M;
-        int c = mvalid ? (int)((unsigned)kc % (unsigned)g.C) : 0;
-        int ij = mvalid ? (int)((unsigned)kc / (unsigned)g.C) : 0;
-        int i = ij / g.k, j = ij - (ij / g.k) * g.k;
-        int blk = c / g.cs, coff = c - blk * g.cs;
-        const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
-        const unsigned hw = (unsigned)(g.Ho * g.Wo);
-        const uint32_t cofs = (q >> 3) * (64 * BK * 2);
-        for (int it = 0; it < nkb; ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES) + cofs;
-          // pixel of row rb (32-bit divides once per k-block), then step 8 pixels per row
-          const unsigned pix0 = (unsigned)((kb_begin + it) * BK + rb);
-          int b = (int)(pix0 / hw);
-          int rem = (int)(pix0 - (unsigned)b * hw);
-          int oy = rem / g.Wo;
-          int ox = rem - oy * g.Wo;
+      int git = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord tc = tile_coord(p, t, BN);
+        const int m0 = tc.m0;
+        if constexpr (AM == A_GATHER_FWD || AM == A_GATHER_DGRAD) {
+          // K-major rows = pixels; thread owns 16B chunk q of rows rb + 16*r8
+          const int q = gt & 7, rb = gt >> 3;
+          int rb_b[8], ry[8], rx[8];
 #pragma unroll
           for (int r8 = 0; r8 < 8; ++r8) {
-            int r = rb + 8 * r8;
-            bool ok = mvalid && (int)pix0 + 8 * r8 < p.K;
-            int iy = oy * g.stride + i - g.pad, ix = ox * g.stride + j - g.pad;
-            ok = ok && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
-            const __nv_bfloat16* src = ok ? src0 + ((long long)(b * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
-            cp_async16(base + r * 128 + (((q & 7) ^ (r & 7)) << 4), src, ok);
-            ox += 8;
-            while (ox >= g.Wo) {
-              ox -= g.Wo;
-              if (++oy == g.Ho) { oy = 0; ++b; }
+            int m = m0 + rb + 16 * r8;
+            int W_ = AM == A_GATHER_FWD ? g.Wo : g.W, H_ = AM == A_GATHER_FWD ? g.Ho : g.H;
+            if (m < p.M) {
+              int x = m % W_, q2 = m / W_;
+              int y = q2 % H_;
+              rb_b[r8] = q2 / H_;
+              if constexpr (AM == A_GATHER_FWD) {
+                ry[r8] = y * g.stride - g.pad;
+                rx[r8] = x * g.stride - g.pad;
+              } else {
+                ry[r8] = y + g.pad;
+                rx[r8] = x + g.pad;
+              }
+            } else {
+              rb_b[r8] = 0;
+              ry[r8] = -(1 << 28);
+              rx[r8] = -(1 << 28);
             }
           }
-          cp_async_arrive_noinc(&full[s]);
+          for (int it = 0; it < tc.nkb; ++it, ++git) {
+            const int s = git % STAGES;
+            const uint32_t ph = (git / STAGES) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            // 32-bit index math: 64-bit integer division is emulated (~100 instructions)
+            const int k = (tc.kb_begin + it) * BK + q * 8;
+            const bool kvalid = k < p.K;
+            const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES);
+            if constexpr (AM == A_GATHER_FWD) {
+              int c = kvalid ? (int)((unsigned)k % (unsigned)g.C) : 0;
+              int ij = kvalid ? (int)((unsigned)k / (unsigned)g.C) : 0;
+              int i = ij / g.k, j = ij - (ij / g.k) * g.k;
+              int blk = c / g.cs, coff = c - blk * g.cs;
+              const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
+#pragma unroll
+              for (int r8 = 0; r8 < 8; ++r8) {
+                int r = rb + 16 * r8;
+                int iy = ry[r8] + i, ix = rx[r8] + j;
+                bool ok = kvalid && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
+                const __nv_bfloat16* src =
+                    ok ? src0 + ((long long)(rb_b[r8] * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
+                cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), src, ok);
+              }
+            } else {
+              int n = kvalid ? (int)((unsigned)k % (unsigned)g.N) : 0;
+              int ij = kvalid ? (int)((unsigned)k / (unsigned)g.N) : 0;
+              int i = ij / g.k, j = ij - (ij / g.k) * g.k;
+              const __nv_bfloat16* src0 = p.gsrc + n;
+#pragma unroll
+              for (int r8 = 0; r8 < 8; ++r8) {
+                int r = rb + 16 * r8;
+                int ny = ry[r8] - i, nx = rx[r8] - j;
+                bool ok = kvalid && ny >= 0 && nx >= 0;
+                int oy = 0, ox = 0;
+                if (g.stride == 1) {
+                  oy = ny; ox = nx;
+                } else {
+                  ok = ok && (ny % g.stride == 0) && (nx % g.stride == 0);
+                  oy = ny / g.stride; ox = nx / g.stride;
+                }
+                ok = ok && oy < g.Ho && ox < g.Wo;
+                const __nv_bfloat16* src =
+                    ok ? src0 + ((long long)(rb_b[r8] * g.Ho + oy) * g.Wo + ox) * g.N : p.gsrc;
+                cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), src, ok);
+              }
+            }
+            cp_async_arrive_noinc(&full[s]);
+          }
+        } else {
+          // A_GATHER_WGRAD: MN-major rows = pixels (K), chunk q = 8 consecutive (i,j,c) of this M tile
+          const int q = gt & 15, rb = gt >> 4;
+          const int kc = m0 + q * 8;
+          const bool mvalid = kc < p.M;
+          int c = mvalid ? (int)((unsigned)kc % (unsigned)g.C) : 0;
+          int ij = mvalid ? (int)((unsigned)kc / (unsigned)g.C) : 0;
+          int i = ij / g.k, j = ij - (ij / g.k) * g.k;
+          int blk = c / g.cs, coff = c - blk * g.cs;
+          const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
+          const unsigned hw = (unsigned)(g.Ho * g.Wo);
+          const uint32_t cofs = (q >> 3) * (64 * BK * 2);
+          for (int it = 0; it < tc.nkb; ++it, ++git) {
+            const int s = git % STAGES;
+            const uint32_t ph = (git / STAGES) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t base = smem_u32(sA + s * A_STAGE_BYTES) + cofs;
+            // pixel of row rb (32-bit divides once per k-block), then step 8 pixels per row
+            const unsigned pix0 = (unsigned)((tc.kb_begin + it) * BK + rb);
+            int b = (int)(pix0 / hw);
+            int rem = (int)(pix0 - (unsigned)b * hw);
+            int oy = rem / g.Wo;
+            int ox = rem - oy * g.Wo;
+#pragma unroll
+            for (int r8 = 0; r8 < 8; ++r8) {
+              int r = rb + 8 * r8;
+              bool ok = mvalid && (int)pix0 + 8 * r8 < p.K;
+              int iy = oy * g.stride + i - g.pad, ix = ox * g.stride + j - g.pad;
+              ok = ok && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
+              const __nv_bfloat16* src = ok ? src0 + ((long long)(b * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
+              cp_async16(base + r * 128 + (((q & 7) ^ (r & 7)) << 4), src, ok);
+              ox += 8;
+              while (ox >= g.Wo) {
+                ox -= g.Wo;
+                if (++oy == g.Ho) { oy = 0; ++b; }
+              }
+            }
+            cp_async_arrive_noinc(&full[s]);
+          }
         }
       }
     }
   } else if (warp == 4) {
     // --------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int git = 0, lt = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+        const TileCoord tc = tile_coord(p, t, BN);
+        const int acc = lt % ACC;
+        const uint32_t aph = (lt / ACC) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t aBase = smem_u32(sA + s * A_STAGE_BYTES);
-        const uint32_t bBase = smem_u32(sB + s * B_STAGE_BYTES);
+        const uint32_t tacc = tmem + acc * TCOLS;
+        for (int it = 0; it < tc.nkb; ++it, ++git) {
+          const int s = git % STAGES;
+          const uint32_t ph = (git / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const uint32_t aBase = smem_u32(sA + s * A_STAGE_BYTES);
+          const uint32_t bBase = smem_u32(sB + s * B_STAGE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          uint64_t ad = A_MN ? make_desc(aBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(aBase + kk * 32, 16, 1024);
-          uint64_t bd = B_MN ? make_desc(bBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(bBase + kk * 32, 16, 1024);
-          tc_mma(tmem, ad, bd, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            uint64_t ad = A_MN ? make_desc(aBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(aBase + kk * 32, 16, 1024);
+            uint64_t bd = B_MN ? make_desc(bBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(bBase + kk * 32, 16, 1024);
+            tc_mma(tacc, ad, bd, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[s]);
         }
-        tc_commit(&empty[s]);
+        tc_commit(&tfull[acc]);
       }
-      tc_commit(tmem_full);
     }
   } else {
     // ------------------------------------------------------------------ epilogue
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
     const int row = warp * 32 + lane;
-    const long long m = (long long)m0 + row;
-    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+    int lt = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      const TileCoord tc = tile_coord(p, t, BN);
+      const int acc = lt % ACC;
+      mbar_wait(&tfull[acc], (lt / ACC) & 1);
+      tc_fence_after();
+      const long long m = (long long)tc.m0 + row;
+      const uint32_t tbase = tmem + acc * TCOLS + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      if (nkb > 0) {
-        tmem_ld16(tbase + c0, v);
-      } else {
-#pragma unroll
-        for (int t = 0; t < 16; ++t) v[t] = 0.f;
-      }
-      const long long n = (long long)n0 + c0;
-      if (m >= p.M || n >= p.N) continue;
-      if constexpr (EPI == EPI_BF16) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          long long nn = n + 8 * h;
-          if (nn >= p.N) break;
-          float o[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            float val = v[8 * h + t];
-            if (p.bias) val += __ldg(p.bias + nn + t);
-            if (p.relu) val = val > 0.f ? val : 0.f;
-            o[t] = val;
-          }
-          long long blk = nn / p.o_cb;
-          long long idx = blk * p.o_bstride + m * p.o_ld + (nn - blk * p.o_cb);
-          if (p.mask) {
-            uint4 mk = *reinterpret_cast<const uint4*>(p.mask + idx);
-            const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
-#pragma unroll
-            for (int t = 0; t < 8; ++t) o[t] = __bfloat162float(mb[t]) > 0.f ? o[t] : 0.f;
-          }
-          uint4 u;
-          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) hh[t] = __floats2bfloat162_rn(o[2 * t], o[2 * t + 1]);
-          *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + idx) = u;
-        }
-      } else if constexpr (EPI == EPI_F32) {
-        float* o = static_cast<float*>(p.out) + blockIdx.z * p.split_stride + m * p.o_ld + n;
-        if (n + 16 <= p.N) {
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            reinterpret_cast<float4*>(o)[t] = make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        if (tc.nkb > 0) {
+          tmem_ld16(tbase + c0, v);
         } else {
-          for (int t = 0; t < 16 && n + t < p.N; ++t) o[t] = v[t];
-        }
-      } else {
-        float* o = static_cast<float*>(p.out) + blockIdx.z * p.split_stride + m;
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-          if (n + t < p.N) o[(n + t) * p.o_ld] = v[t];
+          for (int q = 0; q < 16; ++q) v[q] = 0.f;
+        }
+        const long long n = (long long)tc.n0 + c0;
+        if (m >= p.M || n >= p.N) continue;
+        if constexpr (EPI == EPI_BF16) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            long long nn = n + 8 * h;
+            if (nn >= p.N) break;
+            float o[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float val = v[8 * h + q];
+              if (p.bias) val += __ldg(p.bias + nn + q);
+              if (p.relu) val = val > 0.f ? val : 0.f;
+              o[q] = val;
+            }
+            long long blk = nn / p.o_cb;
+            long long idx = blk * p.o_bstride + m * p.o_ld + (nn - blk * p.o_cb);
+            if (p.mask) {
+              uint4 mk = *reinterpret_cast<const uint4*>(p.mask + idx);
+              const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] = __bfloat162float(mb[q]) > 0.f ? o[q] : 0.f;
+            }
+            uint4 u;
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) hh[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
+            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + idx) = u;
+          }
+        } else if constexpr (EPI == EPI_F32) {
+          float* o = static_cast<float*>(p.out) + tc.z * p.split_stride + m * p.o_ld + n;
+          if (n + 16 <= p.N) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+            for (int q = 0; q < 16 && n + q < p.N; ++q) o[q] = v[q];
+          }
+        } else {
+          float* o = static_cast<float*>(p.out) + tc.z * p.split_stride + m;
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (n + q < p.N) o[(n + q) * p.o_ld] = v[q];
+        }
       }
+      // accumulator drained: let the MMA warp reuse it
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
 
@@ -504,7 +567,7 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS * ACC));
   }
 }
 
@@ -576,15 +639,23 @@ template <int AM, int BMODE, int EPI, int BN, int STAGES>
 static int launch(const Params& p, int splits, cudaStream_t st) {
   auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES>;
   constexpr int smem = smem_bytes<BN, STAGES>();
-  static bool configured = false;
-  if (!configured) {
+  constexpr int threads = a_is_gather<AM>() ? 320 : 192;
+  static int resident = 0;  // persistent CTAs the device holds at once
+  if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-    configured = true;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    const int tmem_cap = 512 / (tmem_cols<BN>() * acc_count<BN>());
+    per_sm = std::max(1, std::min(per_sm, tmem_cap));
+    resident = sms * per_sm;
   }
-  dim3 grid(ceil_div(p.N, BN), ceil_div(p.M, BM), splits);
-  constexpr int threads = a_is_gather<AM>() ? 320 : 192;
-  kern<<<grid, threads, smem, st>>>(p);
+  Params q = p;
+  q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, BM) * splits;
+  dim3 grid(std::min(q.tiles, resident));
+  kern<<<grid, threads, smem, st>>>(q);
   g_tc_launches.fetch_add(1, std::memory_order_relaxed);
   PC_CUDA_CHECK_LAUNCH("umma_gemm");
   return PC_OK;
