@@ -83,27 +83,29 @@ __global__ void relu_bwd_k(long long n, const T* __restrict__ x, const T* __rest
 template <typename T, int V>
 __global__ void maxpool_fwd_k(int B, int H, int W, int C, int k, int s, int Ho, int Wo,
                               const T* __restrict__ x, T* __restrict__ y, uint8_t* __restrict__ arg) {
-  long long cg = C / V;
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long total = (long long)B * Ho * Wo * cg;
+  // 32-bit index math (the host guarantees < 2^31 work items): 64-bit division is emulated
+  const unsigned cg = (unsigned)(C / V);
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned total = (unsigned)B * Ho * Wo * cg;
   if (t >= total) return;
-  int c0 = (int)(t % cg) * V;
-  long long pix = t / cg;
-  int ox = (int)(pix % Wo);
-  int oy = (int)((pix / Wo) % Ho);
-  int b = (int)(pix / ((long long)Wo * Ho));
+  const unsigned pix = t / cg;
+  const int c0 = (int)(t - pix * cg) * V;
+  const unsigned row = pix / (unsigned)Wo;
+  const int ox = (int)(pix - row * Wo);
+  const int b = (int)(row / (unsigned)Ho);
+  const int oy = (int)(row - (unsigned)b * Ho);
   float best[V];
   int bi[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) { best[v] = 0.f; bi[v] = -1; }
   for (int i = 0; i < k; ++i) {
-    const T* row = x + (((long long)b * H + oy * s + i) * W + ox * s) * C + c0;
+    const T* xr = x + (((long long)b * H + oy * s + i) * W + ox * s) * C + c0;
     for (int j = 0; j < k; ++j) {
       float val[V];
       if constexpr (V == 8) {
-        Vec8<T>::load(row + (long long)j * C, val);
+        Vec8<T>::load(xr + (long long)j * C, val);
       } else {
-        val[0] = ld(row + (long long)j * C);
+        val[0] = ld(xr + (long long)j * C);
       }
       int idx = i * k + j;
 #pragma unroll
@@ -114,7 +116,7 @@ __global__ void maxpool_fwd_k(int B, int H, int W, int C, int k, int s, int Ho, 
       }
     }
   }
-  long long o = pix * C + c0;
+  long long o = (long long)pix * C + c0;
   if constexpr (V == 8) {
     Vec8<T>::store(y + o, best);
     uint2 packed;
@@ -132,15 +134,16 @@ template <typename T, int V>
 __global__ void maxpool_bwd_k(int B, int H, int W, int C, int k, int s, int Ho, int Wo,
                               const T* __restrict__ gy, const uint8_t* __restrict__ arg,
                               const T* __restrict__ mask, T* __restrict__ gx) {
-  long long cg = C / V;
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long total = (long long)B * H * W * cg;
+  const unsigned cg = (unsigned)(C / V);
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned total = (unsigned)B * H * W * cg;
   if (t >= total) return;
-  int c0 = (int)(t % cg) * V;
-  long long pix = t / cg;
-  int x = (int)(pix % W);
-  int y = (int)((pix / W) % H);
-  int b = (int)(pix / ((long long)W * H));
+  const unsigned pix = t / cg;
+  const int c0 = (int)(t - pix * cg) * V;
+  const unsigned row = pix / (unsigned)W;
+  const int x = (int)(pix - row * W);
+  const int b = (int)(row / (unsigned)H);
+  const int y = (int)(row - (unsigned)b * H);
   // windows oy with oy*s <= y <= oy*s + k - 1
   int oy_lo = y - k + 1 <= 0 ? 0 : (y - k + 1 + s - 1) / s;
   int oy_hi = min(y / s, Ho - 1);
@@ -165,7 +168,7 @@ __global__ void maxpool_bwd_k(int B, int H, int W, int C, int k, int s, int Ho, 
       }
     }
   }
-  long long o = pix * C + c0;
+  long long o = (long long)pix * C + c0;
   if (mask) {
     float mk[V];
     if constexpr (V == 8) Vec8<T>::load(mask + o, mk); else mk[0] = ld(mask + o);
@@ -409,6 +412,7 @@ extern "C" int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, cons
   if ((long long)B * C == 0) return PC_OK;
   bool vec = C % 8 == 0 && aligned(x, 32) && aligned(y, 32) && aligned(argmax, 8);
   long long work = (long long)B * Ho * Wo * (vec ? C / 8 : C);
+  PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
   DISPATCH_PREC(prec, T, {
     if (vec)
       maxpool_fwd_k<T, 8><<<grid_for(work, 256), 256, 0, S(st)>>>(
@@ -430,6 +434,7 @@ extern "C" int pc_maxpool_backward(int B, int H, int W, int C, int k, int s, con
   bool vec = C % 8 == 0 && aligned(gy, 32) && aligned(gx, 32) && aligned(argmax, 8) &&
              (!mask || aligned(mask, 32));
   long long work = (long long)B * H * W * (vec ? C / 8 : C);
+  PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
   DISPATCH_PREC(prec, T, {
     if (vec)
       maxpool_bwd_k<T, 8><<<grid_for(work, 256), 256, 0, S(st)>>>(

@@ -661,12 +661,26 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
   return PC_OK;
 }
 
-// Tile N for a K-major B operand (the TMA box height must equal the tile).
-static int bn_for(int N) { return N <= 64 ? 64 : N <= 96 ? 96 : N <= 128 ? 128 : N % 192 == 0 ? 192 : 256; }
+// Tile N. Wide tiles halve the A-operand traffic per MMA; when the grid would
+// leave SMs idle (small-M FC layers: M = batch), narrower tiles buy parallelism.
+// For a K-major B the TMA box height equals the tile (bn_for is also used to
+// encode that box); an MN-major B is loaded in 64-column chunks.
+static int bn_for(int N, int M = 1 << 30) {
+  int bn = N <= 64 ? 64 : N <= 96 ? 96 : N <= 128 ? 128 : N % 192 == 0 ? 192 : 256;
+  const long long tm = (M + BM - 1) / BM;
+  while (bn > 64 && tm * ((N + bn - 1) / bn) < 148) bn = bn > 128 ? 128 : 64;
+  return bn;
+}
+static int bn_for_mn(int N, int M = 1 << 30) {
+  int bn = N <= 64 ? 64 : N <= 128 ? 128 : N % 192 == 0 ? 192 : 256;
+  const long long tm = (M + BM - 1) / BM;
+  while (bn > 64 && tm * ((N + bn - 1) / bn) < 148) bn = bn > 128 ? 128 : 64;
+  return bn;
+}
 
 template <int AM, int EPI>
 static int launch_kb(const Params& p, int splits, cudaStream_t st) {
-  switch (bn_for(p.N)) {
+  switch (bn_for(p.N, p.M)) {
     case 64: return launch<AM, B_TMA_K, EPI, 64, 6>(p, splits, st);
     case 96: return launch<AM, B_TMA_K, EPI, 96, 6>(p, splits, st);
     case 128: return launch<AM, B_TMA_K, EPI, 128, 5>(p, splits, st);
@@ -676,9 +690,12 @@ static int launch_kb(const Params& p, int splits, cudaStream_t st) {
 }
 template <int AM, int EPI>
 static int launch_mn(const Params& p, int splits, cudaStream_t st) {
-  if (p.N <= 64) return launch<AM, B_TMA_MN, EPI, 64, 6>(p, splits, st);
-  if (p.N <= 128) return launch<AM, B_TMA_MN, EPI, 128, 5>(p, splits, st);
-  return launch<AM, B_TMA_MN, EPI, 256, 4>(p, splits, st);
+  switch (bn_for_mn(p.N, splits > 1 ? 1 << 30 : p.M)) {
+    case 64: return launch<AM, B_TMA_MN, EPI, 64, 6>(p, splits, st);
+    case 128: return launch<AM, B_TMA_MN, EPI, 128, 5>(p, splits, st);
+    case 192: return launch<AM, B_TMA_MN, EPI, 192, 4>(p, splits, st);
+    default: return launch<AM, B_TMA_MN, EPI, 256, 4>(p, splits, st);
+  }
 }
 
 static Params base_params(int M, int N, int K) {
@@ -737,7 +754,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   }
   int M = g.B * g.Ho * g.Wo, K = g.k * g.k * g.C;
   Params p = base_params(M, g.N, K);
-  int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, bn_for(g.N));
+  int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, bn_for(g.N, M));
   if (rc) return rc;
   p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
@@ -793,7 +810,7 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
   PC_CUDA_CHECK_LAUNCH("transpose_w");
   int M = g.B * g.H * g.W, K = KK * g.N;
   Params p = base_params(M, g.C, K);
-  int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, bn_for(g.C));
+  int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, bn_for(g.C, M));
   if (rc) return rc;
   p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(gy);
@@ -818,7 +835,7 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
 long long umma_wgrad_splits(const pc_conv_geom& g) {
   long long Kc = (long long)g.k * g.k * g.C;
   long long P = (long long)g.B * g.Ho * g.Wo;
-  int bn = g.N <= 64 ? 64 : g.N <= 128 ? 128 : 256;
+  int bn = bn_for_mn(g.N);
   long long tiles = ((Kc + BM - 1) / BM) * ((g.N + bn - 1) / bn);
   long long kbs = (P + BK - 1) / BK;
   long long want = (2 * 148 + tiles - 1) / tiles;
@@ -878,7 +895,7 @@ int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const f
   int rc = make_map(&p.tma_a, x.ptr, cb, B, D / cb, x.ld, x.bstride, BM);
   if (rc) return rc;
   p.a_cb = cb < D ? (int)cb : 0;
-  if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, bn_for(U)))) return rc;
+  if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, bn_for(U, B)))) return rc;
   p.b_cb = 0;
   p.out = y;
   p.o_ld = U;
@@ -910,7 +927,7 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
 // Split-K for the weight gradient when the reduction (the batch, or the pixel
 // count of an explicit-im2col convolution) is long and the output tiles few.
 static int fc_wgrad_splits(int B, int D, int U) {
-  long long tiles = (long long)ceil_div(U, BM) * ceil_div(D, D <= 64 ? 64 : D <= 128 ? 128 : 256);
+  long long tiles = (long long)ceil_div(U, BM) * ceil_div(D, bn_for_mn(D));
   long long kbs = (B + BK - 1) / BK;
   long long want = (2 * 148 + tiles - 1) / tiles;
   long long cap = kbs / 8;
