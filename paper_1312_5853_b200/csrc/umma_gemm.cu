@@ -64,6 +64,8 @@ struct alignas(64) Params {
   const float* bias;
   const __nv_bfloat16* mask;
   int relu;
+  int b_chunked;  // MN-major B encoded as a chunked 4-D view: one TMA op per stage
+  int bn_hint;    // tile N fixed by the B view (0: launch picks)
   // im2col-mode A: K index = (i, j, c) over i2c_C channels in blocks of i2c_cs,
   // output-pixel walk over (i2c_Ho, i2c_Wo) with stride i2c_s from corner (lw, lh)
   int i2c_C, i2c_cs, i2c_k, i2c_s, i2c_lw, i2c_lh, i2c_Wo, i2c_Ho;
@@ -112,6 +114,14 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, uint32_t dst, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 // im2col mode: {c, w, h, d, n} = (channel offset, pixel-walk start, batch, block),
@@ -285,11 +295,15 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
           mbar_arrive_expect_tx(&full[s], B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES));
           const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
           if constexpr (B_MN) {
+            if (p.b_chunked) {  // one op: {64 cols, BK rows, BN/64 chunks} of the chunked view
+              tma_load_4d(&p.tma_b, &full[s], dB, 0, kb * BK, blk_off(n0, p.b_cb) >> 6, blk_idx(n0, p.b_cb));
+            } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) {
-              int n = n0 + 64 * c;
-              tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK,
-                          blk_idx(n, p.b_cb));
+              for (int c = 0; c < BN / 64; ++c) {
+                int n = n0 + 64 * c;
+                tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK,
+                            blk_idx(n, p.b_cb));
+              }
             }
           } else {
             int k = kb * BK;
@@ -604,6 +618,23 @@ static int make_map(CUtensorMap* map, const void* ptr, long long inner, long lon
   return PC_OK;
 }
 
+// MN-major operand as a chunked view {64 cols, rows, cols/64 chunks, blocks}: a
+// box {64, 64, n_chunks, 1} lands as [chunk][row][128 B], the MN-major UMMA layout,
+// so a whole BN-wide stage is one TMA op. Returns false when not expressible.
+static bool make_mn_chunked_map(CUtensorMap* map, const void* ptr, long long cb, long long rows, long long blocks,
+                                long long ld, long long bstride, int n_chunks) {
+  if (!get_encode() || cb % 64 || ld % 8 || (reinterpret_cast<uintptr_t>(ptr) & 15) ||
+      (blocks > 1 && bstride % 8) || n_chunks < 1 || n_chunks > 4)
+    return false;
+  cuuint64_t dims[4] = {64u, (cuuint64_t)rows, (cuuint64_t)(cb / 64), (cuuint64_t)blocks};
+  cuuint64_t strides[3] = {(cuuint64_t)ld * 2, 128u, (cuuint64_t)(blocks > 1 ? bstride : ld * rows) * 2};
+  cuuint32_t box[4] = {64u, (cuuint32_t)BK, (cuuint32_t)n_chunks, 1u};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  return g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static PFN_cuTensorMapEncodeIm2col_v12000 g_encode_i2c = nullptr;
 static std::once_flag g_encode_i2c_once;
 
@@ -690,12 +721,24 @@ static int launch_kb(const Params& p, int splits, cudaStream_t st) {
 }
 template <int AM, int EPI>
 static int launch_mn(const Params& p, int splits, cudaStream_t st) {
-  switch (bn_for_mn(p.N, splits > 1 ? 1 << 30 : p.M)) {
+  switch (p.bn_hint ? p.bn_hint : bn_for_mn(p.N, splits > 1 ? 1 << 30 : p.M)) {
     case 64: return launch<AM, B_TMA_MN, EPI, 64, 6>(p, splits, st);
     case 128: return launch<AM, B_TMA_MN, EPI, 128, 5>(p, splits, st);
     case 192: return launch<AM, B_TMA_MN, EPI, 192, 4>(p, splits, st);
     default: return launch<AM, B_TMA_MN, EPI, 256, 4>(p, splits, st);
   }
+}
+
+// MN-major B: prefer the chunked single-op view for the tile width launch_mn will
+// pick (p.M / p.N must be set); fall back to one 3-D load per 64-column chunk.
+static int setup_mn_b(Params& p, const void* ptr, long long cb, long long rows, long long blocks, long long ld,
+                      long long bstride, int splits) {
+  const int bn = bn_for_mn(p.N, splits > 1 ? 1 << 30 : p.M);
+  p.bn_hint = bn;
+  p.b_chunked = (blocks == 1 || cb % bn == 0) &&
+                make_mn_chunked_map(&p.tma_b, ptr, cb, rows, blocks, ld, bstride, bn / 64);
+  if (p.b_chunked) return PC_OK;
+  return make_map(&p.tma_b, ptr, cb, rows, blocks, ld, bstride, 64);
 }
 
 static Params base_params(int M, int N, int K) {
@@ -858,7 +901,7 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   int splits = (int)umma_wgrad_splits(g);
   p.kb_per_split = ceil_div(p.num_kb, splits);
   splits = ceil_div(p.num_kb, p.kb_per_split);
-  int rc = make_map(&p.tma_b, gy, g.N, P, 1, g.N, 0, 64);
+  int rc = setup_mn_b(p, gy, g.N, P, 1, g.N, 0, splits);
   if (rc) return rc;
   p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
@@ -914,7 +957,7 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
   int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, BM);
   if (rc) return rc;
   p.a_cb = 0;
-  if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, 64))) return rc;
+  if ((rc = setup_mn_b(p, w, D, U, 1, D, 0, 1))) return rc;
   p.b_cb = 0;
   p.out = gx.ptr;
   p.o_ld = gx.ld;
@@ -946,7 +989,7 @@ int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* g
   if (rc) return rc;
   p.a_cb = 0;
   long long cb = x.cb < D ? x.cb : D;
-  if ((rc = make_map(&p.tma_b, x.ptr, cb, B, D / cb, x.ld, x.bstride, 64))) return rc;
+  if ((rc = setup_mn_b(p, x.ptr, cb, B, D / cb, x.ld, x.bstride, fc_wgrad_splits(B, D, U)))) return rc;
   p.b_cb = cb < D ? (int)cb : 0;
   p.o_ld = D;
   int splits = fc_wgrad_splits(B, D, U);
