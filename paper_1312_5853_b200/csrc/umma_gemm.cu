@@ -875,17 +875,33 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
   return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, 1, st);
 }
 
+// Split-K count for a long reduction: the persistent grid runs ceil(units/148)
+// waves of ceil(kbs/s) k-blocks each (plus ~4 k-blocks of per-unit fill/drain),
+// and every extra slice costs a partial tile write + read in the reduction.
+// Pick the s with the smallest modelled time (wave quantisation matters:
+// 297 units on 148 SMs is three waves, 296 is two).
+static long long choose_splits(long long tiles, long long kbs, int bn) {
+  long long best = 1;
+  double best_cost = 1e30;
+  const double tile_bytes = (double)BM * bn * 4 * 2;  // partial write + reduce read
+  const double kb_bytes = (double)(BM + bn) * BK * 2;  // operand bytes per k-block
+  for (long long sp = 1; sp <= 64; ++sp) {
+    if (sp > 1 && kbs / sp < 8) break;
+    const long long units = tiles * sp, kb_per = (kbs + sp - 1) / sp;
+    const long long waves = (units + 147) / 148;
+    double cost = (double)waves * (kb_per + 4);
+    if (sp > 1) cost += (double)units * tile_bytes / (148.0 * kb_bytes);
+    if (cost < best_cost * 0.999) best_cost = cost, best = sp;
+  }
+  return best;
+}
+
 long long umma_wgrad_splits(const pc_conv_geom& g) {
   long long Kc = (long long)g.k * g.k * g.C;
   long long P = (long long)g.B * g.Ho * g.Wo;
   int bn = bn_for_mn(g.N);
   long long tiles = ((Kc + BM - 1) / BM) * ((g.N + bn - 1) / bn);
-  long long kbs = (P + BK - 1) / BK;
-  long long want = (2 * 148 + tiles - 1) / tiles;
-  long long cap = kbs / 8;  // keep >= 8 k-blocks per split
-  if (want > cap) want = cap;
-  if (want > 64) want = 64;
-  return want < 1 ? 1 : want;
+  return choose_splits(tiles, (P + BK - 1) / BK, bn);
 }
 
 int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float* gw, float* part,
@@ -970,13 +986,9 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
 // Split-K for the weight gradient when the reduction (the batch, or the pixel
 // count of an explicit-im2col convolution) is long and the output tiles few.
 static int fc_wgrad_splits(int B, int D, int U) {
-  long long tiles = (long long)ceil_div(U, BM) * ceil_div(D, bn_for_mn(D));
-  long long kbs = (B + BK - 1) / BK;
-  long long want = (2 * 148 + tiles - 1) / tiles;
-  long long cap = kbs / 8;
-  if (want > cap) want = cap;
-  if (want > 64) want = 64;
-  return (int)(want < 1 ? 1 : want);
+  const int bn = bn_for_mn(D);
+  long long tiles = (long long)ceil_div(U, BM) * ceil_div(D, bn);
+  return (int)choose_splits(tiles, (B + BK - 1) / BK, bn);
 }
 
 int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* gw, float* part, cudaStream_t st) {
