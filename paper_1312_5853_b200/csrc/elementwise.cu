@@ -178,6 +178,67 @@ __global__ void maxpool_bwd_k(int B, int H, int W, int C, int k, int s, int Ho, 
   if constexpr (V == 8) Vec8<T>::store(gx + o, acc); else gx[o] = cvt<T>(acc[0]);
 }
 
+// k=3, s=2 (every AlexNet pool): one thread per 2x2 input block (Y, X) and 8
+// channels. The block is covered exactly by windows {Y-1, Y} x {X-1, X}, so the
+// thread reads those <= 4 windows' gradient + argmax once and writes 4 pixels
+// (a 4x cut in loads per output vs the per-pixel gather). Contributions are
+// still added in ascending (oy, ox) order per pixel, as in pc_maxpool_backward.
+template <typename T>
+__global__ void maxpool_bwd_k3s2_k(int B, int H, int W, int C, int Ho, int Wo, const T* __restrict__ gy,
+                                   const uint8_t* __restrict__ arg, const T* __restrict__ mask,
+                                   T* __restrict__ gx) {
+  const int H2 = (H + 1) >> 1, W2 = (W + 1) >> 1;
+  const unsigned cg = (unsigned)(C >> 3);
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (unsigned)B * H2 * W2 * cg) return;
+  const unsigned blk = t / cg;
+  const int c0 = (int)(t - blk * cg) * 8;
+  const unsigned r = blk / (unsigned)W2;
+  const int X = (int)(blk - r * W2);
+  const int b = (int)(r / (unsigned)H2);
+  const int Y = (int)(r - (unsigned)b * H2);
+  float acc[4][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[q][v] = 0.f;
+#pragma unroll
+  for (int dy = -1; dy <= 0; ++dy) {
+    const int oy = Y + dy;
+    if (oy < 0 || oy >= Ho) continue;
+#pragma unroll
+    for (int dx = -1; dx <= 0; ++dx) {
+      const int ox = X + dx;
+      if (ox < 0 || ox >= Wo) continue;
+      const long long o = (((long long)b * Ho + oy) * Wo + ox) * C + c0;
+      uint2 packed = __ldg(reinterpret_cast<const uint2*>(arg + o));
+      const uint8_t* pb = reinterpret_cast<const uint8_t*>(&packed);
+      float g[8];
+      Vec8<T>::load(gy + o, g);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // pixel (2Y + q/2, 2X + q%2): local index in window (oy, ox)
+        const int li = 2 * Y + (q >> 1) - 2 * oy, lj = 2 * X + (q & 1) - 2 * ox;
+        const int want = (li <= 2 && lj <= 2) ? li * 3 + lj : 255;  // 255: pixel outside this window
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[q][v] += (pb[v] == want) ? g[v] : 0.f;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int y = 2 * Y + (q >> 1), x = 2 * X + (q & 1);
+    if (y >= H || x >= W) continue;
+    const long long o = (((long long)b * H + y) * W + x) * C + c0;
+    if (mask) {
+      float mk[8];
+      Vec8<T>::load(mask + o, mk);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[q][v] = mk[v] > 0.f ? acc[q][v] : 0.f;
+    }
+    Vec8<T>::store(gx + o, acc[q]);
+  }
+}
+
 // Softmax cross-entropy: one CTA per row ------------------------------------------
 template <int NT>
 __device__ __forceinline__ float block_reduce(float v, bool is_max, float* sh) {
@@ -435,8 +496,13 @@ extern "C" int pc_maxpool_backward(int B, int H, int W, int C, int k, int s, con
              (!mask || aligned(mask, 32));
   long long work = (long long)B * H * W * (vec ? C / 8 : C);
   PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
+  const long long work22 = (long long)B * ((H + 1) / 2) * ((W + 1) / 2) * (C / 8);
   DISPATCH_PREC(prec, T, {
-    if (vec)
+    if (vec && k == 3 && s == 2)
+      maxpool_bwd_k3s2_k<T><<<grid_for(work22, 256), 256, 0, S(st)>>>(
+          B, H, W, C, Ho, Wo, static_cast<const T*>(gy), argmax, static_cast<const T*>(mask),
+          static_cast<T*>(gx));
+    else if (vec)
       maxpool_bwd_k<T, 8><<<grid_for(work, 256), 256, 0, S(st)>>>(
           B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(gy), argmax,
           static_cast<const T*>(mask), static_cast<T*>(gx));

@@ -233,3 +233,20 @@ def test_fc_bf16_on_tensor_cores(shape):
     assert rel(gw, rgw) < 1e-5
     tc1, simt1 = _tc_counts()
     assert simt1 == simt0 and tc1 - tc0 == 3
+
+
+@pytest.mark.parametrize("shape", [(2, 16, 13, 13), (1, 32, 27, 27), (2, 8, 12, 14), (1, 24, 7, 9)])
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_maxpool_k3s2_vectorised_backward(shape, prec):
+    """The 2x2-block k=3/s=2 backward (C % 8 == 0) against the oracle's scatter."""
+    from paper_1312_5853_b200 import kernels as K
+    rs = np.random.RandomState(17)
+    x = bf16(np.round(rs.randn(*shape) * 3) / 3)     # quantised: plenty of ties
+    K.set_precision(prec)
+    y, arg = K.maxpool_forward(x, 3, 2)
+    ry, rarg = O.maxpool_forward(x, 3, 2)
+    assert np.array_equal(arg, rarg)
+    gy = bf16(rs.randn(*ry.shape))
+    gx = K.maxpool_backward(x, 3, 2, gy, arg)
+    rgx = O.maxpool_backward(x.shape, 3, 2, gy, rarg)
+    assert rel(gx, rgx) < (1e-6 if prec == "fp32" else BF16_OUT_TOL)
