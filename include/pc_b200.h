@@ -142,13 +142,13 @@ PC_API int pc_sgd_step(int n_tensors, const pc_sgd_tensor* table, long long max_
                 float momentum, float weight_decay, pc_stream_t stream);
 
 /* --- layout / reduction helpers used by the engine -------------------------- */
-/* Explicit im2col of the float32 NCHW network input (bf16 out):
+/* Explicit im2col of the NCHW network input (float32 or bf16 in, bf16 out):
  * col[(b*Ho + oy)*Wo + ox][(c*k + i)*k + j] = x[b][c][oy*s+i-p][ox*s+j-p] (0 outside),
  * columns zero-padded to Kp (multiple of 8). Used for the input layer, whose
  * 3 channels are too narrow for 16-byte im2col rows; the conv then runs as
  * pc_fc_forward / pc_fc_backward over pixels with weights [N][Kp]. */
-PC_API int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const float* src, void* dst,
-                     pc_stream_t stream);
+PC_API int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const void* src, int src_prec,
+                     void* dst, pc_stream_t stream);
 /* NCHW float (reference layout) -> NHWC prec with C padded to Cp (zeros). */
 PC_API int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* src, void* dst, int prec,
                     pc_stream_t stream);

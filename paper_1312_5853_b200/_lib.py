@@ -56,7 +56,7 @@ SIGNATURES = {
     "pc_sum_f64": (_i, [_i, _vp, _vp, _vp]),
     "pc_sgd_step": (_i, [_i, _vp, _ll, _f, _f, _f, _vp]),
     "pc_nchw_to_nhwc": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i, _vp]),
-    "pc_im2col": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "pc_im2col": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "pc_sum_buffers": (_i, [_i, _ll, _vp, _vp, _i, _vp]),
     "pc_cast": (_i, [_ll, _vp, _i, _vp, _i, _vp]),
     "pc_scale": (_i, [_ll, _vp, _vp, _f, _i, _vp]),

@@ -348,8 +348,9 @@ __global__ void nchw_to_nhwc_k(int B, int C, int H, int W, int Cp, const float* 
 // zero-padded to Kp columns, straight from the float32 NCHW batch. One CTA per
 // output row (b, oy): the C*k input rows it needs are staged in shared memory,
 // then the Wo x Kp output rows are written with 16-byte stores.
+template <typename TS>
 __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, int Wo, int Kp,
-                              const float* __restrict__ x, __nv_bfloat16* __restrict__ col) {
+                              const TS* __restrict__ x, __nv_bfloat16* __restrict__ col) {
   extern __shared__ float rows[];  // [C][k][W]
   const int bo = blockIdx.x;
   const int b = bo / Ho, oy = bo - b * Ho;
@@ -357,7 +358,7 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
     int xw = t % W, r = t / W;
     int i = r % k, c = r / k;
     int iy = oy * s + i - p;
-    rows[t] = (iy >= 0 && iy < H) ? x[(((long long)b * C + c) * H + iy) * W + xw] : 0.f;
+    rows[t] = (iy >= 0 && iy < H) ? ld(x + (((long long)b * C + c) * H + iy) * W + xw) : 0.f;
   }
   __syncthreads();
   const int K = C * k * k, chunks = Kp / 8;
@@ -559,8 +560,8 @@ extern "C" int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* 
   return PC_OK;
 }
 
-extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const float* src, void* dst,
-                         pc_stream_t st) {
+extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const void* src, int src_prec,
+                         void* dst, pc_stream_t st) {
   PC_REQUIRE(B >= 0 && C > 0 && k > 0 && s > 0 && p >= 0 && Kp % 8 == 0 && Kp >= C * k * k, PC_EVALUE,
              "im2col: bad arguments (Kp must be a multiple of 8 and >= C*k*k)");
   int sh = H + 2 * p - k, sw = W + 2 * p - k;
@@ -569,9 +570,12 @@ extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp
   size_t smem = sizeof(float) * (size_t)C * k * W;
   PC_REQUIRE(smem <= 200 * 1024, PC_EVALUE, "im2col: input rows do not fit shared memory");
   if (B == 0) return PC_OK;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(im2col_rows_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  im2col_rows_k<<<B * Ho, 256, smem, S(st)>>>(C, H, W, k, s, p, Ho, Wo, Kp, src,
-                                              static_cast<__nv_bfloat16*>(dst));
+  DISPATCH_PREC(src_prec, TS, {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(im2col_rows_k<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    im2col_rows_k<TS><<<B * Ho, 256, smem, S(st)>>>(C, H, W, k, s, p, Ho, Wo, Kp, static_cast<const TS*>(src),
+                                                    static_cast<__nv_bfloat16*>(dst));
+  });
   PC_CUDA_CHECK_LAUNCH("im2col");
   return PC_OK;
 }

@@ -330,12 +330,15 @@ class ColumnEngine:
         PROFILE.append((self.wid, st.cl.index, st.kind, name, a, b))
 
     def load_batch(self, x_nchw: torch.Tensor, labels_i32: torch.Tensor):
-        """x_nchw: device float32 (B, C, H, W) slice of the global batch."""
+        """x_nchw: device (B, C, H, W) slice of the global batch: float32, or bf16
+        for the explicit-im2col input layer (the bf16 rounding the device would
+        apply anyway, done by the caller's input pipeline)."""
         c, h, w = self.cs.base.input_shape
         if self.col_kp:
             lay = self.cs.col_layers[0].layer
             self.lib.call("pc_im2col", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
-                          x_nchw.data_ptr(), self.x.data_ptr(), self.stream)
+                          x_nchw.data_ptr(), L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32,
+                          self.x.data_ptr(), self.stream)
         else:
             self.lib.call("pc_nchw_to_nhwc", self.B, c, h, w, self.in_cp, x_nchw.data_ptr(),
                           self.x.data_ptr(), self.prec, self.stream)

@@ -115,21 +115,27 @@ class _Runner:
         numpy input is staged through pinned memory; a pinned float32 CPU
         tensor is copied directly; a CUDA tensor is used in place."""
         dev = self.fabric.torch_device
-        if isinstance(batch_x, torch.Tensor) and batch_x.is_cuda and batch_x.dtype == torch.float32:
+        # a bf16 host batch (an input pipeline that stores images in bf16) is copied as
+        # bf16 when every engine's input layer is the explicit-im2col GEMM, which rounds
+        # to bf16 first anyway (identical results, half the host->device bytes)
+        keep_bf16 = isinstance(batch_x, torch.Tensor) and batch_x.dtype == torch.bfloat16 and \
+            all(e.col_kp for e in self.engines.values())
+        xdt = torch.bfloat16 if keep_bf16 else torch.float32
+        if isinstance(batch_x, torch.Tensor) and batch_x.is_cuda and batch_x.dtype == xdt:
             xs = batch_x.contiguous()
         else:
             xs = None
             if isinstance(batch_x, torch.Tensor):
-                x = batch_x if batch_x.dtype == torch.float32 else batch_x.float()
+                x = batch_x if batch_x.dtype == xdt else batch_x.to(xdt)
             else:
                 x = torch.as_tensor(np.ascontiguousarray(batch_x, dtype=np.float32))
         y = torch.as_tensor(np.asarray(batch_y, dtype=np.int32)) if not isinstance(batch_y, torch.Tensor) \
             else batch_y.to(torch.int32)
         shape = tuple(xs.shape if xs is not None else x.shape)
-        if self.x_dev is None or tuple(self.x_dev.shape) != shape:
-            self.x_host = torch.empty(shape, dtype=torch.float32).pin_memory()
+        if self.x_dev is None or tuple(self.x_dev.shape) != shape or self.x_dev.dtype != xdt:
+            self.x_host = torch.empty(shape, dtype=xdt).pin_memory()
             self.y_host = torch.empty(tuple(y.shape), dtype=torch.int32).pin_memory()
-            self.x_dev = torch.empty(shape, dtype=torch.float32, device=dev)
+            self.x_dev = torch.empty(shape, dtype=xdt, device=dev)
             self.y_dev = torch.empty(tuple(y.shape), dtype=torch.int32, device=dev)
         if xs is not None:
             self.x_dev.copy_(xs)
