@@ -235,7 +235,7 @@ def test_fc_bf16_on_tensor_cores(shape):
     assert simt1 == simt0 and tc1 - tc0 == 3
 
 
-@pytest.mark.parametrize("shape", [(2, 16, 13, 13), (1, 32, 27, 27), (2, 8, 12, 14), (1, 24, 7, 9)])
+@pytest.mark.parametrize("shape", [(2, 16, 13, 13), (1, 32, 27, 27), (2, 8, 11, 15), (1, 24, 7, 9)])
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
 def test_maxpool_k3s2_vectorised_backward(shape, prec):
     """The 2x2-block k=3/s=2 backward (C % 8 == 0) against the oracle's scatter."""
