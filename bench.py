@@ -250,14 +250,15 @@ def main():
     barrier()
     clocks = ClockSampler(dev.index)
     clocks.start()
-    l0 = lib().dll.pc_launch_count()
+    l0, r0 = lib().dll.pc_launch_count(), run.replays
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         run.program(scale)
     e1.record(stream)
     barrier()
-    launches = lib().dll.pc_launch_count() - l0
+    # graph replays launch the captured sequence without passing the C ABI's counter
+    launches = lib().dll.pc_launch_count() - l0 + run.graph_launches * (run.replays - r0)
     ms = e0.elapsed_time(e1) / args.steps
     # ---- end to end through the public API (pinned host batch, loss read-back)
     for _ in range(2):
@@ -274,7 +275,7 @@ def main():
     ms_e2e = e2.elapsed_time(e3) / args.steps
     # ---- per-kernel timing of one step (roofline of the dominant contraction)
     E.PROFILE = []
-    run.program(scale)
+    run.program(scale, eager=True)
     torch.cuda.synchronize()
     prof, E.PROFILE = E.PROFILE, None
     t_by = {}

@@ -149,6 +149,18 @@ PC_API int pc_sgd_step(int n_tensors, const pc_sgd_tensor* table, long long max_
  * pc_fc_forward / pc_fc_backward over pixels with weights [N][Kp]. */
 PC_API int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const void* src, int src_prec,
                      void* dst, pc_stream_t stream);
+/* Space-to-depth of the NCHW network input (float32 or bf16 in, bf16 out) for a
+ * strided input conv: dst[b][Y][X][(dy*s + dx)*C + c] = x[b][c][Y*s+dy-p][X*s+dx-p]
+ * (0 outside the image and for channels >= s*s*C), Y < ceil((H+2p)/s), channels
+ * padded to Cs (multiple of 8; 64 for the TMA im2col path). A k x k / stride-s
+ * conv of x equals a ceil(k/s)^2 / stride-1 / pad-0 conv of dst with the weights
+ * regrouped the same way (taps beyond k zero), so the input layer runs on the
+ * tensor-core implicit GEMM with 128-byte channel rows. */
+PC_API int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
+                             void* dst, pc_stream_t stream);
+/* buf[i] = 0 where keep[i] == 0 (fp32): pins the regrouped conv's structural-zero
+ * weights by zeroing their gradients before the SGD update. */
+PC_API int pc_mask_f32(long long n, const uint8_t* keep, float* buf, pc_stream_t stream);
 /* NCHW float (reference layout) -> NHWC prec with C padded to Cp (zeros). */
 PC_API int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* src, void* dst, int prec,
                     pc_stream_t stream);

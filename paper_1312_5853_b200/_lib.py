@@ -55,6 +55,8 @@ SIGNATURES = {
     "pc_softmax_xent": (_i, [_i, _i, _vp, _vp, _d, _vp, _vp, _vp, _i, _vp]),
     "pc_sum_f64": (_i, [_i, _vp, _vp, _vp]),
     "pc_sgd_step": (_i, [_i, _vp, _ll, _f, _f, _f, _vp]),
+    "pc_space_to_depth": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
+    "pc_mask_f32": (_i, [_ll, _vp, _vp, _vp]),
     "pc_nchw_to_nhwc": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i, _vp]),
     "pc_im2col": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "pc_sum_buffers": (_i, [_i, _ll, _vp, _vp, _i, _vp]),

@@ -381,6 +381,50 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
   }
 }
 
+// Space-to-depth of the network input for a strided input conv: one CTA per
+// output block row (b, Y). The s input rows y = Y*s + dy - p (dy < s) of all C
+// planes are read coalesced into shared memory; the block row is written
+// channels-last, ch = (dy*s + dx)*C + c, zero for padding and ch >= s*s*C,
+// 8 channels (16 B) per store.
+template <typename TS>
+__global__ void s2d_rows_k(int C, int H, int W, int s, int p, int Hs, int Ws, int Cs,
+                           const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst) {
+  extern __shared__ float rows[];  // [C][s][W]
+  const int by = blockIdx.x;
+  const int b = by / Hs, Y = by - b * Hs;
+  for (int t = threadIdx.x; t < C * s * W; t += blockDim.x) {
+    const int xw = t % W, r = t / W;
+    const int dy = r % s, c = r / s;
+    const int iy = Y * s + dy - p;
+    rows[t] = (iy >= 0 && iy < H) ? ld(x + (((long long)b * C + c) * H + iy) * W + xw) : 0.f;
+  }
+  __syncthreads();
+  const int chunks = Cs / 8, real = s * s * C;
+  __nv_bfloat16* out = dst + (long long)by * Ws * Cs;
+  for (int t = threadIdx.x; t < Ws * chunks; t += blockDim.x) {
+    const int X = t / chunks, q = t - X * chunks;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int ch = q * 8 + e;
+      float val = 0.f;
+      if (ch < real) {
+        const int c = ch % C, dd = ch / C;
+        const int dy = dd / s, dx = dd - dy * s;
+        const int ix = X * s + dx - p;
+        if (ix >= 0 && ix < W) val = rows[(c * s + dy) * W + ix];
+      }
+      v[e] = val;
+    }
+    Vec8<__nv_bfloat16>::store(out + (long long)X * Cs + q * 8, v);
+  }
+}
+
+__global__ void mask_f32_k(long long n, const uint8_t* __restrict__ keep, float* __restrict__ buf) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!keep[i]) buf[i] = 0.f;
+}
+
 // One CTA per image row (b, y): coalesced read of the C planes of that row into
 // shared memory, coalesced write of the W x Cp channels-last row.
 template <typename T>
@@ -577,6 +621,33 @@ extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp
                                                     static_cast<__nv_bfloat16*>(dst));
   });
   PC_CUDA_CHECK_LAUNCH("im2col");
+  return PC_OK;
+}
+
+extern "C" int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
+                                 void* dst, pc_stream_t st) {
+  PC_REQUIRE(B >= 0 && C > 0 && H > 0 && W > 0 && s > 0 && p >= 0 && Cs % 8 == 0 && Cs >= s * s * C, PC_EVALUE,
+             "space_to_depth: bad arguments (Cs must be a multiple of 8 and >= s*s*C)");
+  const int Hs = (H + 2 * p + s - 1) / s, Ws = (W + 2 * p + s - 1) / s;
+  size_t smem = sizeof(float) * (size_t)C * s * W;
+  PC_REQUIRE(smem <= 200 * 1024, PC_EVALUE, "space_to_depth: input rows do not fit shared memory");
+  if (B == 0) return PC_OK;
+  DISPATCH_PREC(src_prec, TS, {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(s2d_rows_k<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    s2d_rows_k<TS><<<B * Hs, 256, smem, S(st)>>>(C, H, W, s, p, Hs, Ws, Cs, static_cast<const TS*>(src),
+                                                 static_cast<__nv_bfloat16*>(dst));
+  });
+  PC_CUDA_CHECK_LAUNCH("space_to_depth");
+  return PC_OK;
+}
+
+extern "C" int pc_mask_f32(long long n, const uint8_t* keep, float* buf, pc_stream_t st) {
+  if (n == 0) return PC_OK;
+  int g = grid_for(n, 256);
+  if (g > 148 * 8) g = 148 * 8;
+  mask_f32_k<<<g, 256, 0, S(st)>>>(n, keep, buf);
+  PC_CUDA_CHECK_LAUNCH("mask_f32");
   return PC_OK;
 }
 

@@ -66,6 +66,8 @@ class LayerState:
     geom: object = None
     row_loss: torch.Tensor | None = None
     col: int = 0                         # explicit-im2col input conv: padded K (0 = implicit GEMM)
+    s2d: int = 0                         # space-to-depth input conv: block size (= reference stride)
+    keep: torch.Tensor | None = None     # s2d: uint8 mask of real filter taps in the device weights
 
 
 class ColumnEngine:
@@ -98,17 +100,29 @@ class ColumnEngine:
         self.in_c = c
         self.in_cp = c
         # bf16 input conv with channels too narrow for 128-byte im2col rows (AlexNet:
-        # 3): materialise its columns once per step (pc_im2col) and run it as a
-        # dense GEMM over pixels; col_kp = padded K (reference (c, i, j) order).
+        # 3). Strided (AlexNet 11x11/s4): space-to-depth the image into s x s blocks
+        # (s*s*C <= 64 channels, padded to 64) and run the layer as a stride-1
+        # ceil(k/s)^2 implicit-GEMM conv on the tensor cores. Stride 1: materialise
+        # its columns once per step (pc_im2col) and run it as a dense GEMM over
+        # pixels; col_kp = padded K (reference (c, i, j) order).
         self.col_kp = 0
-        if self.prec == L.PC_BF16 and isinstance(first.layer, Conv) and c % 64:
-            k0 = first.layer.kernel
+        self.s2d = 0
+        lay0 = first.layer if isinstance(first.layer, Conv) else None
+        if self.prec == L.PC_BF16 and lay0 is not None and c % 64 and lay0.stride > 1 and \
+                c * lay0.stride ** 2 <= 64:
+            self.s2d = lay0.stride
+            self.s2d_hw = (layout.s2d_extent(h, lay0.kernel, lay0.stride, lay0.pad)[0],
+                           layout.s2d_extent(w, lay0.kernel, lay0.stride, lay0.pad)[0])
+            self.in_cp = 64
+            self.x = self._new(B * self.s2d_hw[0] * self.s2d_hw[1] * 64)
+        elif self.prec == L.PC_BF16 and lay0 is not None and c % 64:
+            k0 = lay0.kernel
             self.col_kp = (c * k0 * k0 + 7) // 8 * 8
             ho0, wo0 = first.out_shape[1], first.out_shape[2]
             self.x = self._new(B * ho0 * wo0 * self.col_kp)
         else:
             self.x = self._new(B * h * w * self.in_cp)
-        prev_out, prev_shape = self.x, (h, w, self.in_cp)
+        prev_out, prev_shape = self.x, (self.s2d_hw + (64,)) if self.s2d else (h, w, self.in_cp)
         n = len(cs.col_layers)
         for i, cl in enumerate(cs.col_layers):
             layer = cl.layer
@@ -125,17 +139,21 @@ class ColumnEngine:
                 st.inp, st.in_nhwc = prev_out, prev_shape
             if kind == "conv":
                 hh, ww, cc = st.in_nhwc
-                ho = (hh + 2 * layer.pad - layer.kernel) // layer.stride + 1
-                wo = (ww + 2 * layer.pad - layer.kernel) // layer.stride + 1
+                kk, ss, pp = layer.kernel, layer.stride, layer.pad
+                if i == 0 and self.s2d:
+                    st.s2d = self.s2d
+                    kk, ss, pp = -(-layer.kernel // self.s2d), 1, 0
+                ho = (hh + 2 * pp - kk) // ss + 1
+                wo = (ww + 2 * pp - kk) // ss + 1
                 nout = cl.out_shape[0]
+                assert (ho, wo) == tuple(cl.out_shape[1:]), (ho, wo, cl.out_shape)
                 if i == 0 and self.col_kp:
                     st.col = self.col_kp
                 elif cc % 8 and self.prec == L.PC_BF16:
                     raise ValidationError(f"layer {cl.index}: bf16 conv needs C % 8 == 0 (C={cc})")
                 st.cp = cc
                 cs_blk = cc // st.in_blocks
-                st.geom = L.ConvGeom(B, hh, ww, cc, nout, layer.kernel, layer.stride, layer.pad, ho, wo,
-                                     cs_blk, B * hh * ww * cs_blk)
+                st.geom = L.ConvGeom(B, hh, ww, cc, nout, kk, ss, pp, ho, wo, cs_blk, B * hh * ww * cs_blk)
                 st.out_nhwc = (ho, wo, nout)
                 st.out = self._new(B * ho * wo * nout)
             elif kind == "fc":
@@ -189,7 +207,15 @@ class ColumnEngine:
         for st in self.layers:
             if st.kind not in ("conv", "fc"):
                 continue
-            st.w_shape = (st.cl.weight_shape[0], st.col) if st.col else layout.device_weight_shape(st.cl, st.cp)
+            if st.col:
+                st.w_shape = (st.cl.weight_shape[0], st.col)
+            elif st.s2d:
+                n_, c_, k_, _ = st.cl.weight_shape
+                keep = layout.s2d_keep_mask(n_, c_, k_, st.s2d, st.cp)
+                st.w_shape = keep.shape
+                st.keep = torch.from_numpy(keep.reshape(-1)).to(self.device)
+            else:
+                st.w_shape = layout.device_weight_shape(st.cl, st.cp)
             st.w_off = off
             off += -(-layout.numel(st.w_shape) // ALIGN) * ALIGN
             st.b_off = off
@@ -245,6 +271,8 @@ class ColumnEngine:
                 if st.col:
                     dw = np.zeros(st.w_shape, dtype=np.float32)
                     dw[:, : w[0].size] = w.reshape(w.shape[0], -1)
+                elif st.s2d:
+                    dw = layout.conv_to_device_s2d(w, st.s2d, st.cp)
                 elif st.kind == "conv":
                     dw = layout.conv_to_device(w, st.cp)
                 else:
@@ -266,6 +294,8 @@ class ColumnEngine:
             wd = flat[st.w_off:st.w_off + n].reshape(st.w_shape)
             if st.col:
                 w = wd[:, : math.prod(st.cl.weight_shape[1:])].reshape(st.cl.weight_shape).astype(np.float64)
+            elif st.s2d:
+                w = layout.conv_from_device_s2d(wd, st.cl.weight_shape[1], st.cl.weight_shape[2], st.s2d)
             elif st.kind == "conv":
                 w = layout.conv_from_device(wd, st.cl.weight_shape[1])
             else:
@@ -334,7 +364,12 @@ class ColumnEngine:
         for the explicit-im2col input layer (the bf16 rounding the device would
         apply anyway, done by the caller's input pipeline)."""
         c, h, w = self.cs.base.input_shape
-        if self.col_kp:
+        src_prec = L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32
+        if self.s2d:
+            lay = self.cs.col_layers[0].layer
+            self.lib.call("pc_space_to_depth", self.B, c, h, w, lay.stride, lay.pad, 64, x_nchw.data_ptr(),
+                          src_prec, self.x.data_ptr(), self.stream)
+        elif self.col_kp:
             lay = self.cs.col_layers[0].layer
             self.lib.call("pc_im2col", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
                           x_nchw.data_ptr(), L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32,
@@ -419,6 +454,9 @@ class ColumnEngine:
                 self._call(st, "pc_maxpool_backward", self.B, hh, ww, cc, st.cl.layer.kernel, st.cl.layer.stride,
                          st.gout.data_ptr(), st.argmax.data_ptr(),
                          st.inp.data_ptr() if st.mask_dx else None, st.gin.data_ptr(), self.prec, s)
+        if st.keep is not None:
+            self.lib.call("pc_mask_f32", st.keep.numel(), st.keep.data_ptr(), self.g32[st.w_off:].data_ptr(),
+                          s)
         if st.cl.cross and st.cl.shared and want_dx and self.m > 1:
             n = st.gin.numel()
             self._call(st, "pc_scale", n, st.gin.data_ptr(), st.gin.data_ptr(), 1.0 / self.m, self.prec, s)

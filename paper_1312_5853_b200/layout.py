@@ -70,3 +70,34 @@ def device_weight_shape(cl, cp: int) -> tuple:
 
 def numel(shape) -> int:
     return int(math.prod(shape))
+
+
+def s2d_extent(n: int, k: int, s: int, p: int) -> tuple:
+    """(blocked extent, blocked kernel) of a k x k / stride-s / pad-p input conv
+    rewritten as a stride-1 conv over s x s space-to-depth blocks."""
+    return -(-(n + 2 * p) // s), -(-k // s)
+
+
+def conv_to_device_s2d(w: np.ndarray, s: int, cs: int) -> np.ndarray:
+    """[N][C][k][k] -> [N][k'][k'][cs] with channel (dy*s + dx)*C + c of block tap
+    (I, J) = w[n][c][I*s+dy][J*s+dx] (zero where the tap falls beyond k, and for
+    channels >= s*s*C)."""
+    n, c, k, _ = w.shape
+    kb = -(-k // s)
+    wp = np.zeros((n, c, kb * s, kb * s), dtype=np.float64)
+    wp[:, :, :k, :k] = w
+    r = wp.reshape(n, c, kb, s, kb, s).transpose(0, 2, 4, 3, 5, 1).reshape(n, kb, kb, s * s * c)
+    out = np.zeros((n, kb, kb, cs), dtype=np.float32)
+    out[..., : s * s * c] = r
+    return out
+
+
+def conv_from_device_s2d(wd: np.ndarray, c: int, k: int, s: int) -> np.ndarray:
+    n, kb = wd.shape[0], wd.shape[1]
+    r = wd[..., : s * s * c].reshape(n, kb, kb, s, s, c).transpose(0, 5, 1, 3, 2, 4)
+    return np.ascontiguousarray(r.reshape(n, c, kb * s, kb * s)[:, :, :k, :k], dtype=np.float64)
+
+
+def s2d_keep_mask(n: int, c: int, k: int, s: int, cs: int) -> np.ndarray:
+    """uint8 [N][k'][k'][cs]: 1 where the regrouped weight is a real filter tap."""
+    return (conv_to_device_s2d(np.ones((n, c, k, k)), s, cs) != 0).astype(np.uint8)

@@ -14,6 +14,7 @@ replaced by bit-identical local updates; the ledger still books it).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -109,6 +110,8 @@ class _Runner:
             self.columns.setdefault(eng.column, []).append(eng)
         self.x_dev = None
         self.y_dev = None
+        self._graphs, self._seen = {}, set()
+        self.graph_launches, self.replays = 0, 0
 
     def upload(self, batch_x, batch_y):
         """Host -> device copy of the global batch (float32 NCHW, int32 labels).
@@ -119,7 +122,7 @@ class _Runner:
         # bf16 when every engine's input layer is the explicit-im2col GEMM, which rounds
         # to bf16 first anyway (identical results, half the host->device bytes)
         keep_bf16 = isinstance(batch_x, torch.Tensor) and batch_x.dtype == torch.bfloat16 and \
-            all(e.col_kp for e in self.engines.values())
+            all(e.col_kp or e.s2d for e in self.engines.values())
         xdt = torch.bfloat16 if keep_bf16 else torch.float32
         if isinstance(batch_x, torch.Tensor) and batch_x.is_cuda and batch_x.dtype == xdt:
             xs = batch_x.contiguous()
@@ -150,8 +153,39 @@ class _Runner:
             self.y_host.copy_(y)
             self.y_dev.copy_(self.y_host, non_blocking=True)
 
-    def program(self, loss_scale: float):
-        """The device step (no host synchronisation inside)."""
+    def program(self, loss_scale: float, eager: bool = False):
+        """The device step (no host synchronisation inside).
+
+        The first call for a given (loss scale, batch buffer) runs eagerly (it
+        is a real update, and it warms every kernel's launch attributes); the
+        second captures the same launch sequence into a CUDA graph, and every
+        call from then on replays it, so the ~60 launches of a step cost one
+        host call. Under torchrun the NCCL collectives stay eager unless
+        ``PC_GRAPH_DIST=1``."""
+        if eager or not self._graph_enabled():
+            return self._launch(loss_scale)
+        key = (float(loss_scale), self.x_dev.data_ptr(), self.x_dev.dtype)
+        g = self._graphs.get(key)
+        if g is None:
+            if key not in self._seen:
+                self._seen.add(key)
+                return self._launch(loss_scale)
+            torch.cuda.synchronize(self.fabric.torch_device)
+            g = torch.cuda.CUDAGraph()
+            l0 = L.lib().dll.pc_launch_count()
+            with torch.cuda.graph(g):
+                self._launch(loss_scale)
+            self.graph_launches = int(L.lib().dll.pc_launch_count() - l0)
+            self._graphs[key] = g
+        g.replay()
+        self.replays += 1
+
+    def _graph_enabled(self) -> bool:
+        if os.environ.get("PC_GRAPH", "1") == "0":
+            return False
+        return not self.fabric.dist or os.environ.get("PC_GRAPH_DIST", "0") == "1"
+
+    def _launch(self, loss_scale: float):
         shard = self.shard
         for eng in self.engines.values():
             lo = eng.replica * shard

@@ -225,3 +225,44 @@ def test_equivalence_fp32_all_small_grids():
              P.ParallelPlan(2, 2, (3,)), P.ParallelPlan(1, 4, (3,))]
     for dv in P.run_equivalence(net, plans, steps=4, batch=8, precision="fp32"):
         assert dv.worst < 1e-5, dv
+
+
+def test_alexnet_input_layer_space_to_depth_bf16():
+    """The bf16 input layer (11x11/s4 over 3 channels) runs as a 3x3/s1 conv over
+    4x4 space-to-depth blocks. Against the float64 oracle on the same
+    bf16-rounded operands: forward (bias+ReLU fused, bf16 store) within 2^-7,
+    weight and bias gradients (fed the device's own upstream gradient) within
+    1e-3; the regrouped weights' structural zeros stay exactly zero after SGD."""
+    import torch
+    import paper_1312_5853_b200 as P
+    from oracle import ref_kernels as O
+    net = P.load_network(CONFIGS / "alexnet.net")
+    plan = P.ParallelPlan(1, 1)
+    cs = P.columnize(net, 1)
+    dense = f32_params(P.init_dense_params(net, 0, std=0.01))
+    tr, _ = P.gen_synthetic(4, 1, net.input_shape, seed=2)
+    x, y = tr.images, np.array([3, 1, 2, 0])
+    fab = P.spawn(1, precision="bf16")
+    P.setup_workers(fab, plan, cs, dense, P.SgdState())
+    P.hybrid_step(fab, plan, cs, x, y)
+    eng = fab._engines[0]
+    st0 = eng.layers[0]
+    assert st0.s2d == 4 and st0.geom.k == 3 and st0.geom.stride == 1 and st0.geom.C == 64
+
+    def bf(a):
+        return torch.as_tensor(np.asarray(a, np.float32)).bfloat16().double().numpy()
+
+    xb, wb = bf(x), bf(dense[0]["w"])
+    want = O.relu_forward(O.conv2d_forward(xb, wb, dense[0]["b"], 4, 0))
+    got = eng.activation_host(0, "out")
+    assert rel(got, want) < 2.0 ** -7
+    ho = st0.out_nhwc
+    gy = st0.gout[: 4 * ho[0] * ho[1] * ho[2]].float().cpu().numpy().astype(np.float64)
+    gy = gy.reshape(4, *ho).transpose(0, 3, 1, 2)
+    _, gw, gb = O.conv2d_backward(xb, wb, gy, 4, 0)
+    grads = eng.grads_host()
+    assert rel(grads[0]["w"], gw) < 1e-3
+    assert rel(grads[0]["b"], gb) < 1e-3
+    keep = st0.keep.cpu().numpy().astype(bool)
+    wdev = eng.p32[st0.w_off: st0.w_off + keep.size].cpu().numpy()
+    assert np.all(wdev[~keep] == 0.0) and np.any(wdev[keep] != 0.0)
