@@ -49,18 +49,71 @@ int reduce_partials(const float* ws, int splits, long long n, float* out, cudaSt
 
 // Bias gradients: pass 1 sums rows [r*RB, (r+1)*RB) per column block; pass 2
 // sums the row-block partials in ascending order. Fixed order => deterministic.
-constexpr int CS_RB = 512;
-long long colsum_ws(long long P, int N) { return ((P + CS_RB - 1) / CS_RB) * (long long)N; }
+// Long reductions (conv: P = pixels) use 512-row blocks, short ones (FC: P =
+// batch) 64-row blocks so that pass 1 still fills the machine.
+static long long cs_rb(long long P) { return P >= 65536 ? 512 : 64; }
+long long colsum_ws(long long P, int N) { return ((P + cs_rb(P) - 1) / cs_rb(P)) * (long long)N; }
 
 template <typename T>
-__global__ void colsum1_k(const T* __restrict__ g, long long P, int N, float* __restrict__ part) {
+__global__ void colsum1_k(const T* __restrict__ g, long long P, int N, int RB, float* __restrict__ part) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= N) return;
-  long long r0 = (long long)blockIdx.y * CS_RB, r1 = min(P, r0 + CS_RB);
+  long long r0 = (long long)blockIdx.y * RB, r1 = min(P, r0 + RB);
   float acc = 0.f;
   for (long long r = r0; r < r1; ++r) acc += ld(g + r * N + c);
   part[(long long)blockIdx.y * N + c] = acc;
 }
+
+template <typename T> struct V8;
+template <> struct V8<__nv_bfloat16> {
+  static __device__ __forceinline__ void add(const __nv_bfloat16* p, float* a) {
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      a[2 * i] += f.x;
+      a[2 * i + 1] += f.y;
+    }
+  }
+};
+template <> struct V8<float> {
+  static __device__ __forceinline__ void add(const float* p, float* a) {
+    float4 x = __ldg(reinterpret_cast<const float4*>(p)), y = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w; a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+  }
+};
+
+// Vectorised pass 1 (N % 8 == 0, 16-byte rows): a CTA owns CB 8-column groups of
+// one row block; its 256 threads are CB column groups x (256 / CB) row lanes, each
+// lane accumulating 8 columns with 16-byte loads; lanes combine in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum1_v8_k(const T* __restrict__ g, long long P, int N, int RB,
+                                                    float* __restrict__ part) {
+  __shared__ float sh[256 * 8];
+  const int groups = N / 8;
+  const int CB = min(groups, 256), lanes = 256 / CB;
+  const int q = threadIdx.x % CB, lane = threadIdx.x / CB;
+  const int grp = blockIdx.x * CB + q;
+  const long long r0 = (long long)blockIdx.y * RB, r1 = min(P, r0 + RB);
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (lane < lanes && grp < groups) {
+    const T* col = g + (long long)grp * 8;
+#pragma unroll 4
+    for (long long r = r0 + lane; r < r1; r += lanes) V8<T>::add(col + r * N, a);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sh[threadIdx.x * 8 + i] = a[i];
+  __syncthreads();
+  for (int t = threadIdx.x; t < CB * 8; t += 256) {
+    const int qq = t / 8, i = t % 8;
+    if (blockIdx.x * CB + qq >= groups) continue;
+    float s = 0.f;
+    for (int l = 0; l < lanes; ++l) s += sh[(l * CB + qq) * 8 + i];
+    part[(long long)blockIdx.y * N + (long long)(blockIdx.x * CB + qq) * 8 + i] = s;
+  }
+}
+
 // 32 columns x 8 row lanes per CTA; lanes combine in a fixed order (deterministic).
 __global__ void colsum2_k(const float* __restrict__ part, int R, int N, float* __restrict__ out) {
   __shared__ float sh[8][33];
@@ -80,16 +133,27 @@ __global__ void colsum2_k(const float* __restrict__ part, int R, int N, float* _
 
 int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, cudaStream_t st) {
   if (N == 0) return PC_OK;
-  int R = (int)((P + CS_RB - 1) / CS_RB);
+  const int RB = (int)cs_rb(P);
+  int R = (int)((P + RB - 1) / RB);
   if (R == 0) {
     cudaMemsetAsync(out, 0, sizeof(float) * N, st);
     return PC_OK;
   }
-  dim3 g1((N + 127) / 128, R);
-  if (prec == PC_FP32)
-    colsum1_k<float><<<g1, 128, 0, st>>>(static_cast<const float*>(g), P, N, ws);
-  else
-    colsum1_k<__nv_bfloat16><<<g1, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(g), P, N, ws);
+  const bool vec = N % 8 == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+  if (vec) {
+    const int groups = N / 8, CB = groups < 256 ? groups : 256;
+    dim3 g1((groups + CB - 1) / CB, R);
+    if (prec == PC_FP32)
+      colsum1_v8_k<float><<<g1, 256, 0, st>>>(static_cast<const float*>(g), P, N, RB, ws);
+    else
+      colsum1_v8_k<__nv_bfloat16><<<g1, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(g), P, N, RB, ws);
+  } else {
+    dim3 g1((N + 127) / 128, R);
+    if (prec == PC_FP32)
+      colsum1_k<float><<<g1, 128, 0, st>>>(static_cast<const float*>(g), P, N, RB, ws);
+    else
+      colsum1_k<__nv_bfloat16><<<g1, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(g), P, N, RB, ws);
+  }
   colsum2_k<<<(N + 31) / 32, 256, 0, st>>>(ws, R, N, out);
   count_launches(1);
   PC_CUDA_CHECK_LAUNCH("colsum");

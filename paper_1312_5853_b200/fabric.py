@@ -205,18 +205,34 @@ class Fabric:
         """(column_group, replica_group) of this rank, created collectively once."""
         key = (d, m)
         if key not in self._groups:
-            dist = torch.distributed
-            col = rep = None
-            for i in range(d):
-                g = dist.new_group([i * m + j for j in range(m)]) if m > 1 else None
-                if self.rank // m == i:
-                    col = g
-            for j in range(m):
-                g = dist.new_group([r * m + j for r in range(d)]) if d > 1 else None
-                if self.rank % m == j:
-                    rep = g
-            self._groups[key] = (col, rep)
+            self._groups[key] = make_groups(d, m, self.rank)
         return self._groups[key]
+
+
+def group_members(d: int, m: int) -> tuple:
+    """Rank lists of the column groups (replica i: {i*m .. i*m+m-1}) and the
+    replica groups (column j: {j, m+j, ...}), `schemes.py:84-85, 541-542`."""
+    cols = [[i * m + j for j in range(m)] for i in range(d)]
+    reps = [[r * m + j for r in range(d)] for j in range(m)]
+    return cols, reps
+
+
+def make_groups(d: int, m: int, rank: int):
+    """Create every column and replica group (a collective call: all ranks
+    create all groups in the same order) and return this rank's pair; None
+    where the group would have one member."""
+    dist = torch.distributed
+    cols, reps = group_members(d, m)
+    col = rep = None
+    for i, ranks in enumerate(cols):
+        g = dist.new_group(ranks) if m > 1 else None
+        if rank // m == i:
+            col = g
+    for j, ranks in enumerate(reps):
+        g = dist.new_group(ranks) if d > 1 else None
+        if rank % m == j:
+            rep = g
+    return col, rep
 
 
 def spawn(n: int, device: DeviceSpec | None = None, scheduling: str = "lockstep",

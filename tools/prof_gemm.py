@@ -33,3 +33,12 @@ for name, fn in (("fwd K/K", fwd), ("dgrad K/MN", dgrad), ("wgrad MN/MN", wgrad)
     b.record(); torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
     print(f"n={n} {name:12s} {ms*1e3:8.1f} us {fl/ms/1e9:7.1f} TFLOP/s")
+# cuBLAS reference on the same shape (library GEMM, for calibration only)
+xa, wa = x.view(B, D), w.view(U, D)
+torch.matmul(xa, wa.t()); torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(reps): torch.matmul(xa, wa.t())
+b.record(); torch.cuda.synchronize()
+ms = a.elapsed_time(b) / reps
+print(f"n={n} {'cuBLAS':12s} {ms*1e3:8.1f} us {fl/ms/1e9:7.1f} TFLOP/s")
