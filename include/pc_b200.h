@@ -69,6 +69,9 @@ PC_API unsigned long long pc_launch_count(void);
  * CUDA-core kernel used only for extents the tensor-core path cannot tile
  * (e.g. a 10-class head: rows not 16-byte aligned). */
 PC_API void pc_contraction_counts(unsigned long long* tensor_core, unsigned long long* simt);
+/* Debug (tools/trace_gemm.py): per-tile clock64 timeline of the following tensor-core
+ * GEMM launches into a device buffer of >= grid x 64 tiles x 8 u64; NULL turns it off. */
+PC_API void pc_debug_trace_gemm(void* buf);
 /* 1 when the tcgen05/TMA tensor-core path is compiled in and the device is sm_100. */
 PC_API int pc_has_tcgen05(void);
 

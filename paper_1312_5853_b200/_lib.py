@@ -42,6 +42,7 @@ SIGNATURES = {
     "pc_launch_count": (C.c_ulonglong, []),
     "pc_contraction_counts": (None, [_vp, _vp]),
     "pc_has_tcgen05": (_i, []),
+    "pc_debug_trace_gemm": (None, [_vp]),
     "pc_conv2d_forward": (_i, [_P(ConvGeom), _vp, _vp, _vp, _vp, _i, _i, _vp]),
     "pc_conv2d_backward_workspace": (_sz, [_P(ConvGeom), _i]),
     "pc_conv2d_backward": (_i, [_P(ConvGeom), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _sz, _vp]),

@@ -65,11 +65,27 @@ struct alignas(64) Params {
   const __nv_bfloat16* mask;
   int relu;
   int b_chunked;  // MN-major B encoded as a chunked 4-D view: one TMA op per stage
-  int bn_hint;    // tile N fixed by the B view (0: launch picks)
   // im2col-mode A: K index = (i, j, c) over i2c_C channels in blocks of i2c_cs,
   // output-pixel walk over (i2c_Ho, i2c_Wo) with stride i2c_s from corner (lw, lh)
   int i2c_C, i2c_cs, i2c_k, i2c_s, i2c_lw, i2c_lh, i2c_Wo, i2c_Ho;
+  unsigned long long* trace;  // debug: per-CTA per-tile clock64 stamps (tools/trace_gemm.py), normally null
 };
+
+// Debug timeline: slot s of tile lt of CTA b (first TRACE_TILES tiles).
+constexpr int TRACE_TILES = 64;
+constexpr int TRACE_SLOTS = 16;
+__device__ __forceinline__ long long clk() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+__device__ __forceinline__ void trace_put(const Params& p, int lt, int slot, long long v) {
+  if (p.trace != nullptr && lt < TRACE_TILES)
+    p.trace[((size_t)blockIdx.x * TRACE_TILES + lt) * TRACE_SLOTS + slot] = (unsigned long long)v;
+}
+__device__ __forceinline__ void trace_stamp(const Params& p, int lt, int slot) {
+  if (p.trace != nullptr) trace_put(p, lt, slot, clk());
+}
 
 // ----------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -108,50 +124,132 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
                : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, uint32_t dst, int c0, int c1,
-                                            int c2) {
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      "{\n\t.reg .pred P;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// Cluster (CTA pair) helpers -------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Arrive on the barrier at the same smem offset in CTA `rank` of the cluster.
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
       : "memory");
 }
+
+// TMA loads. CG == 2: the 2-SM form — both CTAs of the pair load their own half
+// into their own shared memory, and the transaction bytes complete on the
+// LEADER's (rank 0) barrier at the same offset (peer bit cleared).
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;
+template <int CG>
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, uint32_t dst, int c0, int c1,
+                                            int c2) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  }
+}
+template <int CG>
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, uint32_t dst, int c0, int c1,
                                             int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+  }
 }
 // im2col mode: {c, w, h, d, n} = (channel offset, pixel-walk start, batch, block),
 // im2col offsets {w, h, d} = filter tap (j, i, 0).
+template <int CG>
 __device__ __forceinline__ void tma_im2col_5d(const CUtensorMap* map, uint64_t* bar, uint32_t dst, int c, int w,
                                               int h, int d, int n, uint16_t ow, uint16_t oh) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], {%8, %9, %10};" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(d), "r"(n),
-      "h"(ow), "h"(oh), "h"((uint16_t)0)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], {%8, %9, %10};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(d), "r"(n),
+        "h"(ow), "h"(oh), "h"((uint16_t)0)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], {%8, %9, %10};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c), "r"(w), "r"(h), "r"(d),
+        "r"(n), "h"(ow), "h"(oh), "h"((uint16_t)0)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// MMA completion -> mbarrier; CG == 2 signals the barrier in BOTH CTAs of the pair.
+template <int CG>
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  }
 }
+template <int CG>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
@@ -174,12 +272,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint3
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// Instruction descriptor: D f32, A/B bf16, majorness, N (pair tile width), M = 128 * CG.
+template <int BN, bool A_MN, bool B_MN, int CG>
 __host__ __device__ constexpr uint32_t make_idesc() {
   return (1u << 4)                  // D = f32
          | (1u << 7) | (1u << 10)   // A, B = bf16
          | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16)
-         | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
 }
 
 template <int BN>
@@ -190,16 +289,23 @@ constexpr int tmem_cols() {
 template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM <= A_GATHER_WGRAD; }
 template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN; }
 
-template <int BN, int STAGES>
+// Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
+template <int BN, int STAGES, int CG>
 constexpr int smem_bytes() {
-  return 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
+  return 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + (BN / CG) * BK * 2) + (2 * STAGES + 4) * 8 + 16;
 }
 
 // ------------------------------------------------------------------- kernel
-// Persistent: each CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
+// Persistent: each CTA (CG == 1) or CTA pair (CG == 2, a 2-SM cluster issuing
+// tcgen05.mma.cta_group::2 with M = 256) walks tiles t = unit, unit + units, ...
 // (tile order: split-K slice, then M, then N fastest). The smem stage ring runs
 // continuously across tiles, and with two TMEM accumulators the epilogue of
 // tile t overlaps the mainloop of tile t+1.
+// CTA pair: each CTA loads its own 128 A rows and half of the B tile (BN/2
+// rows) into its own smem; the leader (rank 0) waits on its full barrier for
+// both halves' bytes, issues the MMAs, and its commits arrive on both CTAs'
+// empty / accumulator-full barriers. Each CTA's epilogue drains its own TMEM
+// (its 128 rows x BN) and arrives on the leader's accumulator-empty barrier.
 template <int BN>
 constexpr int acc_count() { return 2 * tmem_cols<BN>() <= 512 ? 2 : 1; }
 
@@ -207,12 +313,14 @@ struct TileCoord {
   int m0, n0, z, kb_begin, nkb;
 };
 
+template <int CG>
 __device__ __forceinline__ TileCoord tile_coord(const Params& p, int t, int bn) {
-  const int tn = (p.N + bn - 1) / bn, tm = (p.M + BM - 1) / BM;
+  const int bmt = BM * CG;
+  const int tn = (p.N + bn - 1) / bn, tm = (p.M + bmt - 1) / bmt;
   TileCoord c;
   c.z = t / (tm * tn);
   const int r = t - c.z * (tm * tn);
-  c.m0 = (r / tn) * BM;
+  c.m0 = (r / tn) * bmt;
   c.n0 = (r - (r / tn) * tn) * bn;
   c.kb_begin = c.z * p.kb_per_split;
   c.nkb = max(min(p.num_kb, c.kb_begin + p.kb_per_split) - c.kb_begin, 0);
@@ -223,14 +331,119 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int AM, int BMODE, int EPI, int BN, int STAGES>
-__global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
-    umma_gemm_k(const __grid_constant__ Params p) {
+// Epilogue: drain one accumulator (this CTA's 128 rows x BN fp32 in TMEM) per
+// tile. EPW warps per TMEM lane quadrant split the 16-column chunks. Output
+// addressing keeps (channel block, offset) incrementally — no divisions.
+template <int EPI, int BN, int CG, int EPW>
+__device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty, int unit,
+                                         int units, uint32_t rank, int quad, int grp, int lane) {
+  constexpr int TCOLS = tmem_cols<BN>();
+  constexpr int ACC = acc_count<BN>();
+  const int row = quad * 32 + lane;
+  int lt = 0;
+  for (int t = unit; t < p.tiles; t += units, ++lt) {
+    const TileCoord tc = tile_coord<CG>(p, t, BN);
+    const int acc = lt % ACC;
+    mbar_wait(&tfull[acc], (lt / ACC) & 1);
+    tc_fence_after();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
+    const long long m = (long long)tc.m0 + (long long)rank * BM + row;
+    const bool mrow = m < p.M;
+    const uint32_t tbase = tmem + acc * TCOLS + ((uint32_t)(quad * 32) << 16);
+    const long long rowoff = m * p.o_ld;
+    // (blk, rem) of output column n = n0 + c0 in a channel-blocked view (o_cb % 8 == 0)
+    long long n = (long long)tc.n0 + grp * 16;
+    long long blk = 0, rem = n;
+    if constexpr (EPI == EPI_BF16) {
+      blk = n / p.o_cb;
+      rem = n - blk * p.o_cb;
+    }
+#pragma unroll 1
+    for (int c0 = grp * 16; c0 < BN; c0 += 16 * EPW) {
+      float v[16];
+      if (tc.nkb > 0) {
+        tmem_ld16(tbase + c0, v);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = 0.f;
+      }
+      if (mrow && n < p.N) {
+        if constexpr (EPI == EPI_BF16) {
+          long long b = blk, r = rem;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const long long nn = n + 8 * h;
+            if (nn >= p.N) break;
+            float o[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float val = v[8 * h + q];
+              if (p.bias) val += __ldg(p.bias + nn + q);
+              if (p.relu) val = val > 0.f ? val : 0.f;
+              o[q] = val;
+            }
+            const long long idx = b * p.o_bstride + rowoff + r;
+            if (p.mask) {
+              uint4 mk = *reinterpret_cast<const uint4*>(p.mask + idx);
+              const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] = __bfloat162float(mb[q]) > 0.f ? o[q] : 0.f;
+            }
+            uint4 u;
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) hh[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
+            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + idx) = u;
+            r += 8;
+            if (r >= p.o_cb) { r -= p.o_cb; ++b; }
+          }
+        } else if constexpr (EPI == EPI_F32) {
+          float* o = static_cast<float*>(p.out) + tc.z * p.split_stride + rowoff + n;
+          if (n + 16 <= p.N) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+            for (int q = 0; q < 16 && n + q < p.N; ++q) o[q] = v[q];
+          }
+        } else {
+          float* o = static_cast<float*>(p.out) + tc.z * p.split_stride + m;
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (n + q < p.N) o[(n + q) * p.o_ld] = v[q];
+        }
+      }
+      n += 16 * EPW;
+      if constexpr (EPI == EPI_BF16) {
+        rem += 16 * EPW;
+        while (rem >= p.o_cb) { rem -= p.o_cb; ++blk; }
+      }
+    }
+    // accumulator drained: let the (leader's) MMA warp reuse it
+    tc_fence_before();
+    __syncwarp();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
+    if (lane == 0) {
+      if constexpr (CG == 1) {
+        mbar_arrive(&tempty[acc]);
+      } else {
+        mbar_arrive_cluster(&tempty[acc], 0);
+      }
+    }
+  }
+}
+
+template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
+__global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Params p) {
   constexpr bool GATHER = a_is_gather<AM>();
+  constexpr int EPW = GATHER ? 1 : 2;  // epilogue warps per TMEM lane quadrant (warps 0-3, and 6-9 unless gathering)
+  static_assert(!(GATHER && CG == 2), "the cp.async gather producers are single-CTA");
   constexpr bool A_MN = a_is_mn<AM>();
   constexpr bool B_MN = BMODE == B_TMA_MN;
-  constexpr int B_STAGE_BYTES = BN * BK * 2;
-  constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN>();
+  constexpr int BNC = BN / CG;  // B rows (N) this CTA loads
+  static_assert(!B_MN || BNC % 64 == 0, "MN-major B is loaded in 64-column chunks");
+  constexpr int B_STAGE_BYTES = BNC * BK * 2;
+  constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN, CG>();
   constexpr int TCOLS = tmem_cols<BN>();
   constexpr int ACC = acc_count<BN>();
 
@@ -246,6 +459,10 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.tiles;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 4) {
     if (lane == 0) {
@@ -255,110 +472,169 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
       }
       for (int a = 0; a < ACC; ++a) {
         mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 4);
+        mbar_init(&tempty[a], 4 * EPW * CG);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TCOLS * ACC));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TCOLS * ACC));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TCOLS * ACC));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   if (warp == 5 && lane == 0) {
     prefetch_tmap(&p.tma_b);
     if constexpr (!GATHER) prefetch_tmap(&p.tma_a);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) {
+    __syncthreads();
+  } else {
+    cluster_sync();  // barrier inits and TMEM allocation visible to the peer before any remote arrive
+  }
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 5) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int git = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = tile_coord(p, t, BN);
-        const int m0 = tc.m0, n0 = tc.n0;
-        int t_b = 0, t_oy = 0, t_ox = 0;  // first output pixel of this M tile (im2col K-major)
-        if constexpr (AM == A_IM2COL_K) {
-          t_ox = m0 % p.i2c_Wo;
-          const int q = m0 / p.i2c_Wo;
-          t_oy = q % p.i2c_Ho;
-          t_b = q / p.i2c_Ho;
+    // Warp-uniform loop (coordinates live in uniform registers); one elected
+    // lane issues. im2col coordinates advance incrementally: the divisions run
+    // once per tile, not once per k-block.
+    int git = 0, plt = 0;
+    for (int t = unit; t < total; t += units, ++plt) {
+      if (lane == 0) trace_stamp(p, plt, 0);
+      long long tr_wait = 0, tr_issue = 0;
+      const TileCoord tc = tile_coord<CG>(p, t, BN);
+      const int m0 = tc.m0 + (int)rank * BM;     // this CTA's A rows
+      const int n0 = tc.n0 + (int)rank * BNC;    // this CTA's B rows
+      // A_IM2COL_K: tile's first output pixel (fixed) and the K position (c, i, j) of kb
+      int t_b = 0, t_oy = 0, t_ox = 0, kc = 0, ki = 0, kj = 0, kblk = 0, kcoff = 0;
+      // A_IM2COL_MN: per-chunk (i, j, blk, coff) of the tile's M rows (fixed) and kb's pixel (b, oy, ox)
+      int ci[BM / 64], cj[BM / 64], cblk[BM / 64], ccoff[BM / 64];
+      int pb = 0, poy = 0, pox = 0;
+      if constexpr (AM == A_IM2COL_K) {
+        t_ox = m0 % p.i2c_Wo;
+        const int q = m0 / p.i2c_Wo;
+        t_oy = q % p.i2c_Ho;
+        t_b = q / p.i2c_Ho;
+        const int k = tc.kb_begin * BK;
+        kc = k % p.i2c_C;
+        const int ij = k / p.i2c_C;
+        ki = ij / p.i2c_k;
+        kj = ij - ki * p.i2c_k;
+        kblk = kc / p.i2c_cs;
+        kcoff = kc - kblk * p.i2c_cs;
+      } else if constexpr (AM == A_IM2COL_MN) {
+#pragma unroll
+        for (int cch = 0; cch < BM / 64; ++cch) {
+          int kk = m0 + 64 * cch;
+          if (kk >= p.M) kk = 0;  // rows past M are discarded by the epilogue
+          const int c = kk % p.i2c_C, ij = kk / p.i2c_C;
+          ci[cch] = ij / p.i2c_k;
+          cj[cch] = ij - ci[cch] * p.i2c_k;
+          cblk[cch] = c / p.i2c_cs;
+          ccoff[cch] = c - cblk[cch] * p.i2c_cs;
         }
-        for (int it = 0; it < tc.nkb; ++it, ++git) {
-          const int s = git % STAGES;
-          const uint32_t ph = (git / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          const int kb = tc.kb_begin + it;
-          mbar_arrive_expect_tx(&full[s], B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES));
+        const int pix0 = tc.kb_begin * BK, hw = p.i2c_Ho * p.i2c_Wo;
+        pb = pix0 / hw;
+        const int rem = pix0 - pb * hw;
+        poy = rem / p.i2c_Wo;
+        pox = rem - poy * p.i2c_Wo;
+      }
+      for (int it = 0; it < tc.nkb; ++it, ++git) {
+        const int s = git % STAGES;
+        const uint32_t ph = (git / STAGES) & 1;
+        const long long c0 = p.trace ? clk() : 0;
+        mbar_wait(&empty[s], ph ^ 1);
+        const long long c1 = p.trace ? clk() : 0;
+        const int kb = tc.kb_begin + it;
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES)));
           const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
           if constexpr (B_MN) {
-            if (p.b_chunked) {  // one op: {64 cols, BK rows, BN/64 chunks} of the chunked view
-              tma_load_4d(&p.tma_b, &full[s], dB, 0, kb * BK, blk_off(n0, p.b_cb) >> 6, blk_idx(n0, p.b_cb));
+            if (p.b_chunked) {  // one op: {64 cols, BK rows, BNC/64 chunks} of the chunked view
+              tma_load_4d<CG>(&p.tma_b, &full[s], dB, 0, kb * BK, blk_off(n0, p.b_cb) >> 6, blk_idx(n0, p.b_cb));
             } else {
 #pragma unroll
-              for (int c = 0; c < BN / 64; ++c) {
+              for (int c = 0; c < BNC / 64; ++c) {
                 int n = n0 + 64 * c;
-                tma_load_3d(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK,
-                            blk_idx(n, p.b_cb));
+                tma_load_3d<CG>(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK,
+                                blk_idx(n, p.b_cb));
               }
             }
           } else {
             int k = kb * BK;
-            tma_load_3d(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
+            tma_load_3d<CG>(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
           }
           if constexpr (AM == A_IM2COL_K) {
             // 128 output pixels from the tile's first pixel; K block = 64 channels of tap (i, j)
-            const int k = kb * BK;
-            const int c = (int)((unsigned)k % (unsigned)p.i2c_C), ij = (int)((unsigned)k / (unsigned)p.i2c_C);
-            const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
-            const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
-            tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), coff,
-                          t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, blk, (uint16_t)j,
-                          (uint16_t)i);
+            tma_im2col_5d<CG>(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
+                              t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
+                              (uint16_t)ki);
           } else if constexpr (AM == A_IM2COL_MN) {
             // K block = 64 consecutive pixels; M = (i, j, c): two 64-channel chunks
-            const unsigned pix0 = (unsigned)(kb * BK), hw = (unsigned)(p.i2c_Ho * p.i2c_Wo);
-            const int b = (int)(pix0 / hw), rem = (int)(pix0 - (unsigned)b * hw);
-            const int oy = rem / p.i2c_Wo, ox = rem - (rem / p.i2c_Wo) * p.i2c_Wo;
 #pragma unroll
-            for (int cch = 0; cch < BM / 64; ++cch) {
-              int kc = m0 + 64 * cch;
-              if (kc >= p.M) kc = m0;  // rows past M are discarded by the epilogue
-              const int c = (int)((unsigned)kc % (unsigned)p.i2c_C),
-                        ij = (int)((unsigned)kc / (unsigned)p.i2c_C);
-              const int i = ij / p.i2c_k, j = ij - i * p.i2c_k;
-              const int blk = c / p.i2c_cs, coff = c - blk * p.i2c_cs;
-              tma_im2col_5d(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES) + cch * (64 * BK * 2), coff,
-                            ox * p.i2c_s + p.i2c_lw, oy * p.i2c_s + p.i2c_lh, b, blk, (uint16_t)j, (uint16_t)i);
-            }
+            for (int cch = 0; cch < BM / 64; ++cch)
+              tma_im2col_5d<CG>(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES) + cch * (64 * BK * 2),
+                                ccoff[cch], pox * p.i2c_s + p.i2c_lw, poy * p.i2c_s + p.i2c_lh, pb, cblk[cch],
+                                (uint16_t)cj[cch], (uint16_t)ci[cch]);
           } else if constexpr (!GATHER) {
             const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES);
             if constexpr (A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / 64; ++c) {
                 int m = m0 + 64 * c;
-                tma_load_3d(&p.tma_a, &full[s], dA + c * (64 * BK * 2), blk_off(m, p.a_cb), kb * BK,
-                            blk_idx(m, p.a_cb));
+                tma_load_3d<CG>(&p.tma_a, &full[s], dA + c * (64 * BK * 2), blk_off(m, p.a_cb), kb * BK,
+                                blk_idx(m, p.a_cb));
               }
             } else {
               int k = kb * BK;
-              tma_load_3d(&p.tma_a, &full[s], dA, blk_off(k, p.a_cb), m0, blk_idx(k, p.a_cb));
+              tma_load_3d<CG>(&p.tma_a, &full[s], dA, blk_off(k, p.a_cb), m0, blk_idx(k, p.a_cb));
             }
           }
         }
+        __syncwarp();
+        // advance the im2col K position / pixel walk to the next k-block
+        if constexpr (AM == A_IM2COL_K) {
+          kc += BK;
+          kcoff += BK;
+          if (kcoff == p.i2c_cs) { kcoff = 0; ++kblk; }
+          if (kc == p.i2c_C) {
+            kc = kcoff = kblk = 0;
+            if (++kj == p.i2c_k) { kj = 0; ++ki; }
+          }
+        } else if constexpr (AM == A_IM2COL_MN) {
+          pox += BK;
+          while (pox >= p.i2c_Wo) {
+            pox -= p.i2c_Wo;
+            if (++poy == p.i2c_Ho) { poy = 0; ++pb; }
+          }
+        }
+        if (p.trace) {
+          const long long c2 = clk();
+          tr_wait += c1 - c0;
+          tr_issue += c2 - c1;
+        }
+      }
+      if (lane == 0) {
+        trace_stamp(p, plt, 1);
+        trace_put(p, plt, 8, tr_wait);
+        trace_put(p, plt, 9, tr_issue);
       }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 6 && GATHER) {
     // ----------------------------------------------------- im2col gather producer
     if constexpr (GATHER) {
       const int gt = threadIdx.x - 192;
       const pc_conv_geom& g = p.g;
       int git = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = tile_coord(p, t, BN);
+      for (int t = unit; t < total; t += units) {
+        const TileCoord tc = tile_coord<CG>(p, t, BN);
         const int m0 = tc.m0;
         if constexpr (AM == A_GATHER_FWD || AM == A_GATHER_DGRAD) {
           // K-major rows = pixels; thread owns 16B chunk q of rows rb + 16*r8
@@ -477,111 +753,73 @@ __global__ void __launch_bounds__(a_is_gather<AM>() ? 320 : 192, 1)
     }
   } else if (warp == 4) {
     // --------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // Warp-uniform loop; one elected lane issues the tcgen05.mma / commit.
+    // Descriptors: the stage-0 descriptor plus (byte offset >> 4) of stage / k step.
+    if (leader) {
+      const uint64_t a0 = A_MN ? make_desc(smem_u32(sA), 64 * BK * 2, 1024) : make_desc(smem_u32(sA), 16, 1024);
+      const uint64_t b0 = B_MN ? make_desc(smem_u32(sB), 64 * BK * 2, 1024) : make_desc(smem_u32(sB), 16, 1024);
+      constexpr uint32_t A_KSTEP = (A_MN ? 2048 : 32) >> 4, B_KSTEP = (B_MN ? 2048 : 32) >> 4;
       int git = 0, lt = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-        const TileCoord tc = tile_coord(p, t, BN);
+      for (int t = unit; t < total; t += units, ++lt) {
+        const TileCoord tc = tile_coord<CG>(p, t, BN);
         const int acc = lt % ACC;
         const uint32_t aph = (lt / ACC) & 1;
+        if (lane == 0) trace_stamp(p, lt, 2);
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
+        if (lane == 0) trace_stamp(p, lt, 3);
         const uint32_t tacc = tmem + acc * TCOLS;
+        long long tr_wait = 0, tr_issue = 0;
         for (int it = 0; it < tc.nkb; ++it, ++git) {
           const int s = git % STAGES;
           const uint32_t ph = (git / STAGES) & 1;
+          const long long c0 = p.trace ? clk() : 0;
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          const long long c1 = p.trace ? clk() : 0;
+          if (it == 0 && lane == 0) trace_stamp(p, lt, 7);
           if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          const uint32_t aBase = smem_u32(sA + s * A_STAGE_BYTES);
-          const uint32_t bBase = smem_u32(sB + s * B_STAGE_BYTES);
+          if (elect_one()) {
+            const uint64_t ad = a0 + (uint64_t)((s * A_STAGE_BYTES) >> 4);
+            const uint64_t bd = b0 + (uint64_t)((s * B_STAGE_BYTES) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            uint64_t ad = A_MN ? make_desc(aBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(aBase + kk * 32, 16, 1024);
-            uint64_t bd = B_MN ? make_desc(bBase + kk * 2048, 64 * BK * 2, 1024) : make_desc(bBase + kk * 32, 16, 1024);
-            tc_mma(tacc, ad, bd, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk)
+              tc_mma<CG>(tacc, ad + kk * A_KSTEP, bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+            tc_commit<CG>(&empty[s]);
           }
-          tc_commit(&empty[s]);
+          __syncwarp();
+          if (p.trace) {
+            const long long c2 = clk();
+            tr_wait += c1 - c0;
+            tr_issue += c2 - c1;
+          }
         }
-        tc_commit(&tfull[acc]);
+        if (elect_one()) tc_commit<CG>(&tfull[acc]);
+        __syncwarp();
+        if (lane == 0) {
+          trace_stamp(p, lt, 4);
+          trace_put(p, lt, 10, tr_wait);
+          trace_put(p, lt, 11, tr_issue);
+        }
       }
     }
   } else {
-    // ------------------------------------------------------------------ epilogue
-    const int row = warp * 32 + lane;
-    int lt = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-      const TileCoord tc = tile_coord(p, t, BN);
-      const int acc = lt % ACC;
-      mbar_wait(&tfull[acc], (lt / ACC) & 1);
-      tc_fence_after();
-      const long long m = (long long)tc.m0 + row;
-      const uint32_t tbase = tmem + acc * TCOLS + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        if (tc.nkb > 0) {
-          tmem_ld16(tbase + c0, v);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] = 0.f;
-        }
-        const long long n = (long long)tc.n0 + c0;
-        if (m >= p.M || n >= p.N) continue;
-        if constexpr (EPI == EPI_BF16) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            long long nn = n + 8 * h;
-            if (nn >= p.N) break;
-            float o[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float val = v[8 * h + q];
-              if (p.bias) val += __ldg(p.bias + nn + q);
-              if (p.relu) val = val > 0.f ? val : 0.f;
-              o[q] = val;
-            }
-            long long blk = nn / p.o_cb;
-            long long idx = blk * p.o_bstride + m * p.o_ld + (nn - blk * p.o_cb);
-            if (p.mask) {
-              uint4 mk = *reinterpret_cast<const uint4*>(p.mask + idx);
-              const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) o[q] = __bfloat162float(mb[q]) > 0.f ? o[q] : 0.f;
-            }
-            uint4 u;
-            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) hh[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
-            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + idx) = u;
-          }
-        } else if constexpr (EPI == EPI_F32) {
-          float* o = static_cast<float*>(p.out) + tc.z * p.split_stride + m * p.o_ld + n;
-          if (n + 16 <= p.N) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          } else {
-            for (int q = 0; q < 16 && n + q < p.N; ++q) o[q] = v[q];
-          }
-        } else {
-          float* o = static_cast<float*>(p.out) + tc.z * p.split_stride + m;
-#pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (n + q < p.N) o[(n + q) * p.o_ld] = v[q];
-        }
-      }
-      // accumulator drained: let the MMA warp reuse it
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-    }
+    epilogue<EPI, BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, warp & 3, warp >= 6 ? 1 : 0, lane);
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) {
+    __syncthreads();
+  } else {
+    cluster_sync();  // the leader's MMAs read this CTA's smem until the last tile drains
+  }
   if (warp == 4) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS * ACC));
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS * ACC));
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS * ACC));
+    }
   }
 }
 
@@ -665,37 +903,79 @@ static int make_im2col_map(CUtensorMap* map, const void* ptr, int cs, int W, int
 }
 
 static std::atomic<unsigned long long> g_tc_launches{0}, g_simt_launches{0};
+static unsigned long long* g_trace = nullptr;  // pc_debug_trace_gemm
 
-template <int AM, int BMODE, int EPI, int BN, int STAGES>
+template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
 static int launch(const Params& p, int splits, cudaStream_t st) {
-  auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES>;
-  constexpr int smem = smem_bytes<BN, STAGES>();
-  constexpr int threads = a_is_gather<AM>() ? 320 : 192;
+  auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES, CG>;
+  constexpr int smem = smem_bytes<BN, STAGES, CG>();
+  static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
+  constexpr int threads = 320;
   static int resident = 0;  // persistent CTAs the device holds at once
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-    const int tmem_cap = 512 / (tmem_cols<BN>() * acc_count<BN>());
-    per_sm = std::max(1, std::min(per_sm, tmem_cap));
-    resident = sms * per_sm;
+    if (CG == 1) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+      const int tmem_cap = 512 / (tmem_cols<BN>() * acc_count<BN>());
+      per_sm = std::max(1, std::min(per_sm, tmem_cap));
+      resident = sms * per_sm;
+    } else {
+      int clusters = 0;
+      cfg.gridDim = dim3(sms & ~1);
+      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters < 1) {
+        cudaGetLastError();
+        clusters = sms / 2;
+      }
+      resident = 2 * clusters;
+    }
   }
   Params q = p;
-  q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, BM) * splits;
-  dim3 grid(std::min(q.tiles, resident));
-  kern<<<grid, threads, smem, st>>>(q);
+  q.trace = g_trace;
+  q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, BM * CG) * splits;
+  const int units = std::min(q.tiles, resident / CG);
+  cfg.gridDim = dim3(units * CG);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, q);
+  PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "umma_gemm launch: %s", cudaGetErrorString(e));
   g_tc_launches.fetch_add(1, std::memory_order_relaxed);
   PC_CUDA_CHECK_LAUNCH("umma_gemm");
   return PC_OK;
 }
 
-// Tile N. Wide tiles halve the A-operand traffic per MMA; when the grid would
-// leave SMs idle (small-M FC layers: M = batch), narrower tiles buy parallelism.
-// For a K-major B the TMA box height equals the tile (bn_for is also used to
-// encode that box); an MN-major B is loaded in 64-column chunks.
+// Tile shape: BN (the MMA's N) and CG (1 = one SM, M = 128; 2 = CTA pair,
+// M = 256, each SM holding half of B). Wide tiles cut the operand bytes each
+// SM pulls from L2 per FLOP — the limit of these kernels — so the pair is used
+// whenever the A operand comes by TMA and there are enough M tiles to occupy
+// the 74 pairs; small-M FC layers (M = batch) stay single-SM and narrow N until
+// the grid fills the machine. For a K-major B the TMA box height is BN / CG;
+// an MN-major B is loaded in 64-column chunks, so BN / CG must be 64 or 128.
+struct Tile {
+  int bn, cg;
+};
+
+static bool cg2_enabled() {
+  static const int on = [] {
+    const char* e = getenv("PC_CG2");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+
 static int bn_for(int N, int M = 1 << 30) {
   int bn = N <= 64 ? 64 : N <= 96 ? 96 : N <= 128 ? 128 : N % 192 == 0 ? 192 : 256;
   const long long tm = (M + BM - 1) / BM;
@@ -709,34 +989,67 @@ static int bn_for_mn(int N, int M = 1 << 30) {
   return bn;
 }
 
+static Tile pick_k(int M, int N, bool pair_ok, int splits = 1) {
+  if (pair_ok && cg2_enabled()) {
+    const int bn = N <= 64 ? 64 : N <= 96 ? 96 : N <= 128 ? 128 : N % 192 == 0 ? 192 : 256;
+    const long long units = (long long)((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn) * splits;
+    if (units >= 74) return {bn, 2};
+  }
+  return {bn_for(N, splits > 1 ? 1 << 30 : M), 1};
+}
+static Tile pick_mn(int M, int N, bool pair_ok, int splits = 1) {
+  if (pair_ok && cg2_enabled()) {
+    const int bn = N <= 128 ? 128 : 256;
+    const long long units = (long long)((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn) * splits;
+    if (units >= 74) return {bn, 2};
+  }
+  return {bn_for_mn(N, splits > 1 ? 1 << 30 : M), 1};
+}
+
 template <int AM, int EPI>
-static int launch_kb(const Params& p, int splits, cudaStream_t st) {
-  switch (bn_for(p.N, p.M)) {
-    case 64: return launch<AM, B_TMA_K, EPI, 64, 6>(p, splits, st);
-    case 96: return launch<AM, B_TMA_K, EPI, 96, 6>(p, splits, st);
-    case 128: return launch<AM, B_TMA_K, EPI, 128, 5>(p, splits, st);
-    case 192: return launch<AM, B_TMA_K, EPI, 192, 4>(p, splits, st);
-    default: return launch<AM, B_TMA_K, EPI, 256, 4>(p, splits, st);
+static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
+  if constexpr (!a_is_gather<AM>()) {
+    if (t.cg == 2) {
+      switch (t.bn) {
+        case 64: return launch<AM, B_TMA_K, EPI, 64, 8, 2>(p, splits, st);
+        case 96: return launch<AM, B_TMA_K, EPI, 96, 8, 2>(p, splits, st);
+        case 128: return launch<AM, B_TMA_K, EPI, 128, 8, 2>(p, splits, st);
+        case 192: return launch<AM, B_TMA_K, EPI, 192, 7, 2>(p, splits, st);
+        default: return launch<AM, B_TMA_K, EPI, 256, 6, 2>(p, splits, st);
+      }
+    }
+  }
+  switch (t.bn) {
+    case 64: return launch<AM, B_TMA_K, EPI, 64, 8, 1>(p, splits, st);
+    case 96: return launch<AM, B_TMA_K, EPI, 96, 7, 1>(p, splits, st);
+    case 128: return launch<AM, B_TMA_K, EPI, 128, 6, 1>(p, splits, st);
+    case 192: return launch<AM, B_TMA_K, EPI, 192, 5, 1>(p, splits, st);
+    default: return launch<AM, B_TMA_K, EPI, 256, 4, 1>(p, splits, st);
   }
 }
 template <int AM, int EPI>
-static int launch_mn(const Params& p, int splits, cudaStream_t st) {
-  switch (p.bn_hint ? p.bn_hint : bn_for_mn(p.N, splits > 1 ? 1 << 30 : p.M)) {
-    case 64: return launch<AM, B_TMA_MN, EPI, 64, 6>(p, splits, st);
-    case 128: return launch<AM, B_TMA_MN, EPI, 128, 5>(p, splits, st);
-    case 192: return launch<AM, B_TMA_MN, EPI, 192, 4>(p, splits, st);
-    default: return launch<AM, B_TMA_MN, EPI, 256, 4>(p, splits, st);
+static int launch_mn(const Params& p, Tile t, int splits, cudaStream_t st) {
+  if constexpr (!a_is_gather<AM>()) {
+    if (t.cg == 2) {
+      if (t.bn == 128) return launch<AM, B_TMA_MN, EPI, 128, 8, 2>(p, splits, st);
+      return launch<AM, B_TMA_MN, EPI, 256, 6, 2>(p, splits, st);
+    }
+  }
+  switch (t.bn) {
+    case 64: return launch<AM, B_TMA_MN, EPI, 64, 8, 1>(p, splits, st);
+    case 128: return launch<AM, B_TMA_MN, EPI, 128, 6, 1>(p, splits, st);
+    case 192: return launch<AM, B_TMA_MN, EPI, 192, 5, 1>(p, splits, st);
+    default: return launch<AM, B_TMA_MN, EPI, 256, 4, 1>(p, splits, st);
   }
 }
 
-// MN-major B: prefer the chunked single-op view for the tile width launch_mn will
-// pick (p.M / p.N must be set); fall back to one 3-D load per 64-column chunk.
+// MN-major B for tile t: prefer the chunked single-op view ({64 cols, BK rows,
+// BN/CG/64 chunks} per CTA); fall back to one 3-D load per 64-column chunk.
 static int setup_mn_b(Params& p, const void* ptr, long long cb, long long rows, long long blocks, long long ld,
-                      long long bstride, int splits) {
-  const int bn = bn_for_mn(p.N, splits > 1 ? 1 << 30 : p.M);
-  p.bn_hint = bn;
-  p.b_chunked = (blocks == 1 || cb % bn == 0) &&
-                make_mn_chunked_map(&p.tma_b, ptr, cb, rows, blocks, ld, bstride, bn / 64);
+                      long long bstride, Tile t) {
+  const int bnc = t.bn / t.cg;
+  p.b_chunked = (blocks == 1 || cb % bnc == 0) &&
+                make_mn_chunked_map(&p.tma_b, ptr, cb, rows, blocks, ld, bstride, bnc / 64);
   if (p.b_chunked) return PC_OK;
   return make_map(&p.tma_b, ptr, cb, rows, blocks, ld, bstride, 64);
 }
@@ -797,7 +1110,9 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   }
   int M = g.B * g.Ho * g.Wo, K = g.k * g.k * g.C;
   Params p = base_params(M, g.N, K);
-  int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, bn_for(g.N, M));
+  const bool i2c = im2col_ok(g.cs, g.C, g.cstride);
+  const Tile t = pick_k(M, g.N, i2c);
+  int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, t.bn / t.cg);
   if (rc) return rc;
   p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
@@ -806,14 +1121,14 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   p.o_ld = g.N;
   p.bias = bias;
   p.relu = (flags & PC_RELU) != 0;
-  if (im2col_ok(g.cs, g.C, g.cstride)) {
+  if (i2c) {
     rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, BM, -g.pad, -g.pad,
                          g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
     if (rc) return rc;
     set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
-    return launch_kb<A_IM2COL_K, EPI_BF16>(p, 1, st);
+    return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
-  return launch_kb<A_GATHER_FWD, EPI_BF16>(p, 1, st);
+  return launch_kb<A_GATHER_FWD, EPI_BF16>(p, t, 1, st);
 }
 
 __global__ void transpose_w_k(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt, int N, int KK,
@@ -853,7 +1168,8 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
   PC_CUDA_CHECK_LAUNCH("transpose_w");
   int M = g.B * g.H * g.W, K = KK * g.N;
   Params p = base_params(M, g.C, K);
-  int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, bn_for(g.C, M));
+  const Tile t = pick_k(M, g.C, i2c);
+  int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, t.bn / t.cg);
   if (rc) return rc;
   p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(gy);
@@ -870,9 +1186,9 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
                          lo + g.H - g.Ho, 1);
     if (rc) return rc;
     set_i2c(p, g.N, g.N, g.k, 1, lo, g.W, g.H);
-    return launch_kb<A_IM2COL_K, EPI_BF16>(p, 1, st);
+    return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
-  return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, 1, st);
+  return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, t, 1, st);
 }
 
 // Split-K count for a long reduction: the persistent grid runs ceil(units/148)
@@ -880,29 +1196,41 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
 // and every extra slice costs a partial tile write + read in the reduction.
 // Pick the s with the smallest modelled time (wave quantisation matters:
 // 297 units on 148 SMs is three waves, 296 is two).
-static long long choose_splits(long long tiles, long long kbs, int bn) {
+static long long choose_splits(long long tiles, long long kbs, int bn, int cg = 1) {
   long long best = 1;
   double best_cost = 1e30;
-  const double tile_bytes = (double)BM * bn * 4 * 2;  // partial write + reduce read
-  const double kb_bytes = (double)(BM + bn) * BK * 2;  // operand bytes per k-block
+  const int cap = 148 / cg;                                  // concurrent units (SMs or SM pairs)
+  const double tile_bytes = (double)BM * cg * bn * 4 * 2;    // partial write + reduce read
+  const double kb_bytes = (double)(BM * cg + bn) * BK * 2;   // operand bytes per k-block
   for (long long sp = 1; sp <= 64; ++sp) {
     if (sp > 1 && kbs / sp < 8) break;
     const long long units = tiles * sp, kb_per = (kbs + sp - 1) / sp;
-    const long long waves = (units + 147) / 148;
+    const long long waves = (units + cap - 1) / cap;
     double cost = (double)waves * (kb_per + 4);
-    if (sp > 1) cost += (double)units * tile_bytes / (148.0 * kb_bytes);
+    if (sp > 1) cost += (double)units * tile_bytes / (cap * kb_bytes);
     if (cost < best_cost * 0.999) best_cost = cost, best = sp;
   }
   return best;
 }
 
-long long umma_wgrad_splits(const pc_conv_geom& g) {
-  long long Kc = (long long)g.k * g.k * g.C;
-  long long P = (long long)g.B * g.Ho * g.Wo;
-  int bn = bn_for_mn(g.N);
-  long long tiles = ((Kc + BM - 1) / BM) * ((g.N + bn - 1) / bn);
-  return choose_splits(tiles, (P + BK - 1) / BK, bn);
+// Weight gradient tiling: M = kh*kw*C, N = Cout, K = pixels (long) -> split-K.
+// The CTA pair applies when the A operand comes by TMA im2col.
+struct WgradPlan {
+  Tile t;
+  int splits;
+};
+static WgradPlan wgrad_plan(const pc_conv_geom& g) {
+  const long long Kc = (long long)g.k * g.k * g.C, P = (long long)g.B * g.Ho * g.Wo;
+  const bool i2c = im2col_ok(g.cs, g.C, g.cstride);
+  const Tile t = (i2c && cg2_enabled()) ? Tile{g.N <= 128 ? 128 : 256, 2} : Tile{bn_for_mn(g.N), 1};
+  const long long tiles = ((Kc + BM * t.cg - 1) / (BM * t.cg)) * ((g.N + t.bn - 1) / t.bn);
+  const long long kbs = (P + BK - 1) / BK;
+  long long sp = choose_splits(tiles, kbs, t.bn, t.cg);
+  const long long per = (kbs + sp - 1) / sp;
+  return {t, (int)((kbs + per - 1) / per)};
 }
+
+long long umma_wgrad_splits(const pc_conv_geom& g) { return wgrad_plan(g).splits; }
 
 int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float* gw, float* part,
                     cudaStream_t st) {
@@ -914,10 +1242,11 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   int Kc = g.k * g.k * g.C;
   long long P = (long long)g.B * g.Ho * g.Wo;
   Params p = base_params(Kc, g.N, (int)P);
-  int splits = (int)umma_wgrad_splits(g);
+  const WgradPlan wp = wgrad_plan(g);
+  int splits = wp.splits;
   p.kb_per_split = ceil_div(p.num_kb, splits);
   splits = ceil_div(p.num_kb, p.kb_per_split);
-  int rc = setup_mn_b(p, gy, g.N, P, 1, g.N, 0, splits);
+  int rc = setup_mn_b(p, gy, g.N, P, 1, g.N, 0, wp.t);
   if (rc) return rc;
   p.b_cb = 0;
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
@@ -932,7 +1261,8 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   }
   p.out = splits > 1 ? static_cast<void*>(part) : static_cast<void*>(gw);
   p.split_stride = splits > 1 ? (long long)g.N * Kc : 0;
-  rc = i2c ? launch_mn<A_IM2COL_MN, EPI_F32_T>(p, splits, st) : launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, splits, st);
+  rc = i2c ? launch_mn<A_IM2COL_MN, EPI_F32_T>(p, wp.t, splits, st)
+           : launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, wp.t, splits, st);
   if (rc || splits == 1) return rc;
   return reduce_partials(part, splits, (long long)g.N * Kc, gw, st);
 }
@@ -954,13 +1284,14 @@ int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const f
   int rc = make_map(&p.tma_a, x.ptr, cb, B, D / cb, x.ld, x.bstride, BM);
   if (rc) return rc;
   p.a_cb = cb < D ? (int)cb : 0;
-  if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, bn_for(U, B)))) return rc;
+  const Tile t = pick_k(B, U, true);
+  if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, t.bn / t.cg))) return rc;
   p.b_cb = 0;
   p.out = y;
   p.o_ld = U;
   p.bias = bias;
   p.relu = (flags & PC_RELU) != 0;
-  return launch_kb<A_TMA_K, EPI_BF16>(p, 1, st);
+  return launch_kb<A_TMA_K, EPI_BF16>(p, t, 1, st);
 }
 
 int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_mat& gx, const void* mask,
@@ -973,14 +1304,15 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
   int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, BM);
   if (rc) return rc;
   p.a_cb = 0;
-  if ((rc = setup_mn_b(p, w, D, U, 1, D, 0, 1))) return rc;
+  const Tile t = pick_mn(B, D, true);
+  if ((rc = setup_mn_b(p, w, D, U, 1, D, 0, t))) return rc;
   p.b_cb = 0;
   p.out = gx.ptr;
   p.o_ld = gx.ld;
   p.o_cb = gx.cb;
   p.o_bstride = gx.bstride;
   p.mask = static_cast<const __nv_bfloat16*>(mask);
-  return launch_mn<A_TMA_K, EPI_BF16>(p, 1, st);
+  return launch_mn<A_TMA_K, EPI_BF16>(p, t, 1, st);
 }
 
 // Split-K for the weight gradient when the reduction (the batch, or the pixel
@@ -1001,20 +1333,21 @@ int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* g
   if (rc) return rc;
   p.a_cb = 0;
   long long cb = x.cb < D ? x.cb : D;
-  if ((rc = setup_mn_b(p, x.ptr, cb, B, D / cb, x.ld, x.bstride, fc_wgrad_splits(B, D, U)))) return rc;
+  int splits = fc_wgrad_splits(B, D, U);
+  const Tile t{bn_for_mn(D, splits > 1 ? 1 << 30 : U), 1};
+  if ((rc = setup_mn_b(p, x.ptr, cb, B, D / cb, x.ld, x.bstride, t))) return rc;
   p.b_cb = cb < D ? (int)cb : 0;
   p.o_ld = D;
-  int splits = fc_wgrad_splits(B, D, U);
   p.kb_per_split = ceil_div(p.num_kb, splits);
   splits = ceil_div(p.num_kb, p.kb_per_split);
   if (splits == 1 || part == nullptr) {
     p.kb_per_split = p.num_kb;
     p.out = gw;
-    return launch_mn<A_TMA_MN, EPI_F32>(p, 1, st);
+    return launch_mn<A_TMA_MN, EPI_F32>(p, t, 1, st);
   }
   p.out = part;
   p.split_stride = (long long)U * D;
-  rc = launch_mn<A_TMA_MN, EPI_F32>(p, splits, st);
+  rc = launch_mn<A_TMA_MN, EPI_F32>(p, t, splits, st);
   if (rc) return rc;
   return reduce_partials(part, splits, (long long)U * D, gw, st);
 }
@@ -1026,6 +1359,12 @@ size_t umma_fc_extra_ws(int B, int D, int U, int prec) {
 }
 
 }  // namespace pc
+
+// Debug only (tools/trace_gemm.py): device buffer of >= grid * 64 * 8 u64 that
+// every following tensor-core GEMM launch stamps with clock64 per tile; NULL stops.
+extern "C" PC_API void pc_debug_trace_gemm(void* buf) {
+  pc::umma::g_trace = static_cast<unsigned long long*>(buf);
+}
 
 extern "C" PC_API void pc_contraction_counts(unsigned long long* tensor_core, unsigned long long* simt) {
   if (tensor_core) *tensor_core = pc::umma::g_tc_launches.load();

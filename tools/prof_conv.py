@@ -6,7 +6,7 @@ sys.path.insert(0, __file__.rsplit("/tools", 1)[0])
 from paper_1312_5853_b200 import _lib as L
 
 LAYERS = {  # name: (C, H, N, k, s, p)
-    "L0": (8, 227, 96, 11, 4, 0), "L3": (96, 27, 256, 5, 1, 2), "L6": (256, 13, 384, 3, 1, 1),
+    "L0": (64, 57, 96, 3, 1, 0), "L3": (96, 27, 256, 5, 1, 2), "L6": (256, 13, 384, 3, 1, 1),
     "L8": (384, 13, 384, 3, 1, 1), "L10": (384, 13, 256, 3, 1, 1)}
 name = sys.argv[1] if len(sys.argv) > 1 else "L3"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
