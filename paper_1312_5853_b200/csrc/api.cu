@@ -49,9 +49,13 @@ int reduce_partials(const float* ws, int splits, long long n, float* out, cudaSt
 
 // Bias gradients: pass 1 sums rows [r*RB, (r+1)*RB) per column block; pass 2
 // sums the row-block partials in ascending order. Fixed order => deterministic.
-// Long reductions (conv: P = pixels) use 512-row blocks, short ones (FC: P =
-// batch) 64-row blocks so that pass 1 still fills the machine.
-static long long cs_rb(long long P) { return P >= 65536 ? 512 : 64; }
+// Row blocks are sized so pass 1 runs ~2 CTA waves and pass 2 reads <= 296
+// partial rows per column.
+static long long cs_rb(long long P) {
+  // ~296 row blocks (two waves of pass-1 CTAs), at least 64 rows each
+  long long rb = (P + 295) / 296;
+  return rb < 64 ? 64 : rb;
+}
 long long colsum_ws(long long P, int N) { return ((P + cs_rb(P) - 1) / cs_rb(P)) * (long long)N; }
 
 template <typename T>

@@ -80,9 +80,12 @@ __global__ void relu_bwd_k(long long n, const T* __restrict__ x, const T* __rest
 
 // Max-pool ---------------------------------------------------------------------
 // One thread per (b, oy, ox, 8-channel group) when C % 8 == 0, else per channel.
-template <typename T, int V>
-__global__ void maxpool_fwd_k(int B, int H, int W, int C, int k, int s, int Ho, int Wo,
+template <typename T, int V, int KS = 0, int SS = 0>
+__global__ void maxpool_fwd_k(int B, int H, int W, int C, int k_, int s_, int Ho, int Wo,
                               const T* __restrict__ x, T* __restrict__ y, uint8_t* __restrict__ arg) {
+  // KS > 0: compile-time k x k / stride s (AlexNet 3/2): the window loop unrolls and
+  // all k*k loads are in flight at once
+  const int k = KS > 0 ? KS : k_, s = KS > 0 ? SS : s_;
   // 32-bit index math (the host guarantees < 2^31 work items): 64-bit division is emulated
   const unsigned cg = (unsigned)(C / V);
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -98,9 +101,13 @@ __global__ void maxpool_fwd_k(int B, int H, int W, int C, int k, int s, int Ho, 
   int bi[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) { best[v] = 0.f; bi[v] = -1; }
-  for (int i = 0; i < k; ++i) {
+#pragma unroll
+  for (int i = 0; i < (KS > 0 ? KS : 16); ++i) {
+    if (KS == 0 && i >= k) break;
     const T* xr = x + (((long long)b * H + oy * s + i) * W + ox * s) * C + c0;
-    for (int j = 0; j < k; ++j) {
+#pragma unroll
+    for (int j = 0; j < (KS > 0 ? KS : 16); ++j) {
+      if (KS == 0 && j >= k) break;
       float val[V];
       if constexpr (V == 8) {
         Vec8<T>::load(xr + (long long)j * C, val);
@@ -381,43 +388,55 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
   }
 }
 
-// Space-to-depth of the network input for a strided input conv: one CTA per
-// output block row (b, Y). The s input rows y = Y*s + dy - p (dy < s) of all C
-// planes are read coalesced into shared memory; the block row is written
-// channels-last, ch = (dy*s + dx)*C + c, zero for padding and ch >= s*s*C,
-// 8 channels (16 B) per store.
-template <typename TS>
-__global__ void s2d_rows_k(int C, int H, int W, int s, int p, int Hs, int Ws, int Cs,
-                           const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst) {
-  extern __shared__ float rows[];  // [C][s][W]
-  const int by = blockIdx.x;
-  const int b = by / Hs, Y = by - b * Hs;
-  for (int t = threadIdx.x; t < C * s * W; t += blockDim.x) {
-    const int xw = t % W, r = t / W;
-    const int dy = r % s, c = r / s;
-    const int iy = Y * s + dy - p;
-    rows[t] = (iy >= 0 && iy < H) ? ld(x + (((long long)b * C + c) * H + iy) * W + xw) : 0.f;
-  }
-  __syncthreads();
-  const int chunks = Cs / 8, real = s * s * C;
-  __nv_bfloat16* out = dst + (long long)by * Ws * Cs;
-  for (int t = threadIdx.x; t < Ws * chunks; t += blockDim.x) {
-    const int X = t / chunks, q = t - X * chunks;
-    float v[8];
+// Space-to-depth of the network input for a strided input conv: one thread per
+// output block (b, Y, X) reads its s x s x C input values (consecutive threads =
+// consecutive X, so each (c, row) read is coalesced across the warp) and writes
+// the Cs-channel row, ch = (dy*s + dx)*C + c, with 16-byte stores (zero for
+// padding and ch >= s*s*C). Each input element is read exactly once.
+template <typename TS, int CS, int SS, int CC>  // SS, CC > 0: compile-time stride / channels
+__global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_, int p, int Hs, int Ws,
+                                             const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst) {
+  const int s = SS > 0 ? SS : s_, C = CC > 0 ? CC : C_;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)B * Hs * Ws) return;
+  const int X = (int)(t % Ws);
+  const long long r = t / Ws;
+  const int Y = (int)(r % Hs), b = (int)(r / Hs);
+  float v[CS];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int ch = q * 8 + e;
-      float val = 0.f;
-      if (ch < real) {
-        const int c = ch % C, dd = ch / C;
-        const int dy = dd / s, dx = dd - dy * s;
-        const int ix = X * s + dx - p;
-        if (ix >= 0 && ix < W) val = rows[(c * s + dy) * W + ix];
+  for (int i = 0; i < CS; ++i) v[i] = 0.f;
+  if constexpr (SS > 0 && CC > 0) {
+#pragma unroll
+    for (int dy = 0; dy < SS; ++dy) {
+      const int iy = Y * SS + dy - p;
+#pragma unroll
+      for (int dx = 0; dx < SS; ++dx) {
+        const int ix = X * SS + dx - p;
+        const bool ok = iy >= 0 && iy < H && ix >= 0 && ix < W;
+#pragma unroll
+        for (int c = 0; c < CC; ++c)
+          v[(dy * SS + dx) * CC + c] = ok ? ld(x + (((long long)b * CC + c) * H + iy) * W + ix) : 0.f;
       }
-      v[e] = val;
     }
-    Vec8<__nv_bfloat16>::store(out + (long long)X * Cs + q * 8, v);
+  } else {
+    int ch = 0;
+    for (int dy = 0; dy < s; ++dy) {
+      const int iy = Y * s + dy - p;
+      for (int dx = 0; dx < s; ++dx) {
+        const int ix = X * s + dx - p;
+        const bool ok = iy >= 0 && iy < H && ix >= 0 && ix < W;
+        for (int c = 0; c < C; ++c, ++ch) {
+          const float val = ok ? ld(x + (((long long)b * C + c) * H + iy) * W + ix) : 0.f;
+#pragma unroll
+          for (int i = 0; i < CS; ++i)
+            if (i == ch) v[i] = val;
+        }
+      }
+    }
   }
+  __nv_bfloat16* out = dst + t * CS;
+#pragma unroll
+  for (int q = 0; q < CS / 8; ++q) Vec8<__nv_bfloat16>::store(out + q * 8, v + q * 8);
 }
 
 __global__ void mask_f32_k(long long n, const uint8_t* __restrict__ keep, float* __restrict__ buf) {
@@ -520,7 +539,10 @@ extern "C" int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, cons
   long long work = (long long)B * Ho * Wo * (vec ? C / 8 : C);
   PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
   DISPATCH_PREC(prec, T, {
-    if (vec)
+    if (vec && k == 3 && s == 2)
+      maxpool_fwd_k<T, 8, 3, 2><<<grid_for(work, 256), 256, 0, S(st)>>>(
+          B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(x), static_cast<T*>(y), argmax);
+    else if (vec)
       maxpool_fwd_k<T, 8><<<grid_for(work, 256), 256, 0, S(st)>>>(
           B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(x), static_cast<T*>(y), argmax);
     else
@@ -626,17 +648,23 @@ extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp
 
 extern "C" int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
                                  void* dst, pc_stream_t st) {
-  PC_REQUIRE(B >= 0 && C > 0 && H > 0 && W > 0 && s > 0 && p >= 0 && Cs % 8 == 0 && Cs >= s * s * C, PC_EVALUE,
-             "space_to_depth: bad arguments (Cs must be a multiple of 8 and >= s*s*C)");
+  PC_REQUIRE(B >= 0 && C > 0 && H > 0 && W > 0 && s > 0 && p >= 0 && Cs >= s * s * C && (Cs == 64 || Cs == 32),
+             PC_EVALUE, "space_to_depth: bad arguments (Cs must be 32 or 64 and >= s*s*C)");
   const int Hs = (H + 2 * p + s - 1) / s, Ws = (W + 2 * p + s - 1) / s;
-  size_t smem = sizeof(float) * (size_t)C * s * W;
-  PC_REQUIRE(smem <= 200 * 1024, PC_EVALUE, "space_to_depth: input rows do not fit shared memory");
-  if (B == 0) return PC_OK;
+  const long long n = (long long)B * Hs * Ws;
+  if (n == 0) return PC_OK;
+  const int g = grid_for(n, 256);
+  auto* d = static_cast<__nv_bfloat16*>(dst);
   DISPATCH_PREC(src_prec, TS, {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(s2d_rows_k<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    s2d_rows_k<TS><<<B * Hs, 256, smem, S(st)>>>(C, H, W, s, p, Hs, Ws, Cs, static_cast<const TS*>(src),
-                                                 static_cast<__nv_bfloat16*>(dst));
+    const TS* x = static_cast<const TS*>(src);
+    if (Cs == 64 && s == 4 && C == 3)        // AlexNet conv1 (11x11/s4)
+      s2d_k<TS, 64, 4, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
+    else if (Cs == 64 && s == 2 && C == 3)   // small64 conv1 (6x6/s2)
+      s2d_k<TS, 64, 2, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
+    else if (Cs == 64)
+      s2d_k<TS, 64, 0, 0><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
+    else
+      s2d_k<TS, 32, 0, 0><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
   });
   PC_CUDA_CHECK_LAUNCH("space_to_depth");
   return PC_OK;
