@@ -68,6 +68,11 @@ struct alignas(64) Params {
   // im2col-mode A: K index = (i, j, c) over i2c_C channels in blocks of i2c_cs,
   // output-pixel walk over (i2c_Ho, i2c_Wo) with stride i2c_s from corner (lw, lh)
   int i2c_C, i2c_cs, i2c_k, i2c_s, i2c_lw, i2c_lh, i2c_Wo, i2c_Ho;
+  // K-major im2col: K walks (tap, 64-channel chunk); i2c_cpt = chunks per tap = ceil(C / 64).
+  // A channel count that is not a multiple of 64 (AlexNet conv2: 96) loads its last
+  // chunk past the channel extent — TMA zero-fills it — and the MMA issues only the
+  // k16 steps that hold real channels.
+  int i2c_cpt;
   unsigned long long* trace;  // debug: per-CTA per-tile clock64 stamps (tools/trace_gemm.py), normally null
 };
 
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
       const int m0 = tc.m0 + (int)rank * BM;     // this CTA's A rows
       const int n0 = tc.n0 + (int)rank * BNC;    // this CTA's B rows
       // A_IM2COL_K: tile's first output pixel (fixed) and the K position (c, i, j) of kb
-      int t_b = 0, t_oy = 0, t_ox = 0, kc = 0, ki = 0, kj = 0, kblk = 0, kcoff = 0;
+      int t_b = 0, t_oy = 0, t_ox = 0, kc = 0, ki = 0, kj = 0, kblk = 0, kcoff = 0, ktap = 0;
       // A_IM2COL_MN: per-chunk (i, j, blk, coff) of the tile's M rows (fixed) and kb's pixel (b, oy, ox)
       int ci[BM / 64], cj[BM / 64], cblk[BM / 64], ccoff[BM / 64];
       int pb = 0, poy = 0, pox = 0;
@@ -522,11 +527,10 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
         const int q = m0 / p.i2c_Wo;
         t_oy = q % p.i2c_Ho;
         t_b = q / p.i2c_Ho;
-        const int k = tc.kb_begin * BK;
-        kc = k % p.i2c_C;
-        const int ij = k / p.i2c_C;
-        ki = ij / p.i2c_k;
-        kj = ij - ki * p.i2c_k;
+        ktap = tc.kb_begin / p.i2c_cpt;
+        kc = (tc.kb_begin - ktap * p.i2c_cpt) * BK;
+        ki = ktap / p.i2c_k;
+        kj = ktap - ki * p.i2c_k;
         kblk = kc / p.i2c_cs;
         kcoff = kc - kblk * p.i2c_cs;
       } else if constexpr (AM == A_IM2COL_MN) {
@@ -568,7 +572,7 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
               }
             }
           } else {
-            int k = kb * BK;
+            const int k = AM == A_IM2COL_K ? ktap * p.i2c_C + kc : kb * BK;
             tma_load_3d<CG>(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
           }
           if constexpr (AM == A_IM2COL_K) {
@@ -603,9 +607,10 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
         if constexpr (AM == A_IM2COL_K) {
           kc += BK;
           kcoff += BK;
-          if (kcoff == p.i2c_cs) { kcoff = 0; ++kblk; }
-          if (kc == p.i2c_C) {
+          if (kcoff >= p.i2c_cs) { kcoff = 0; ++kblk; }
+          if (kc >= p.i2c_C) {
             kc = kcoff = kblk = 0;
+            ++ktap;
             if (++kj == p.i2c_k) { kj = 0; ++ki; }
           }
         } else if constexpr (AM == A_IM2COL_MN) {
@@ -770,7 +775,16 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
         if (lane == 0) trace_stamp(p, lt, 3);
         const uint32_t tacc = tmem + acc * TCOLS;
         long long tr_wait = 0, tr_issue = 0;
+        // K-major im2col with a partial last channel chunk: k16 steps with real channels
+        const bool partial = AM == A_IM2COL_K && (p.i2c_C % BK) != 0;
+        int mchunk = partial ? tc.kb_begin % p.i2c_cpt : 0;
         for (int it = 0; it < tc.nkb; ++it, ++git) {
+          int nk16 = BK / 16;
+          if (partial) {
+            const int left = p.i2c_C - mchunk * BK;
+            if (left < BK) nk16 = (left + 15) / 16;
+            if (++mchunk == p.i2c_cpt) mchunk = 0;
+          }
           const int s = git % STAGES;
           const uint32_t ph = (git / STAGES) & 1;
           const long long c0 = p.trace ? clk() : 0;
@@ -784,7 +798,8 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
             const uint64_t bd = b0 + (uint64_t)((s * B_STAGE_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
-              tc_mma<CG>(tacc, ad + kk * A_KSTEP, bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+              if (kk < nk16)
+                tc_mma<CG>(tacc, ad + kk * A_KSTEP, bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
             tc_commit<CG>(&empty[s]);
           }
           __syncwarp();
@@ -888,7 +903,8 @@ static int make_im2col_map(CUtensorMap* map, const void* ptr, int cs, int W, int
       g_encode_i2c = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(fn);
   });
   PC_REQUIRE(g_encode_i2c != nullptr, PC_ECUDA, "cuTensorMapEncodeIm2col unavailable");
-  PC_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && cs % 64 == 0, PC_EVALUE, "im2col view misaligned");
+  PC_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && cs % 8 == 0 && cs >= 64, PC_EVALUE,
+             "im2col view misaligned");
   cuuint64_t dims[5] = {(cuuint64_t)cs, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)nblk};
   cuuint64_t strides[4] = {(cuuint64_t)cs * 2, (cuuint64_t)W * cs * 2, (cuuint64_t)H * W * cs * 2,
                            (cuuint64_t)(nblk > 1 ? cstride : (long long)B * H * W * cs) * 2};
@@ -1080,12 +1096,21 @@ bool umma_available() {
 }
 
 // TMA im2col needs 64-channel (128 B) pixel rows within one channel block.
-static bool im2col_ok(int cs, int C, long long cstride) {
+static bool im2col_enabled() {
   static const int enabled = [] {
     const char* e = getenv("PC_IM2COL");
     return e ? atoi(e) : 1;
   }();
-  return enabled && cs % 64 == 0 && C % cs == 0 && (C == cs || cstride % 8 == 0);
+  return enabled != 0;
+}
+static bool im2col_ok(int cs, int C, long long cstride) {
+  return im2col_enabled() && cs % 64 == 0 && C % cs == 0 && (C == cs || cstride % 8 == 0);
+}
+
+// K-major im2col (forward): also a single (unblocked) channel block of any
+// multiple of 8 channels — the last 64-channel chunk is zero-filled by TMA.
+static bool im2col_k_ok(int cs, int C, long long cstride) {
+  return im2col_ok(cs, C, cstride) || (im2col_enabled() && C == cs && C % 8 == 0 && C >= 64);
 }
 
 static void set_i2c(Params& p, int C, int cs, int k, int s, int lo, int Wo, int Ho) {
@@ -1096,6 +1121,13 @@ static void set_i2c(Params& p, int C, int cs, int k, int s, int lo, int Wo, int 
   p.i2c_lw = p.i2c_lh = lo;
   p.i2c_Wo = Wo;
   p.i2c_Ho = Ho;
+  p.i2c_cpt = (C + BK - 1) / BK;
+}
+
+// K-major im2col GEMM over k*k taps x ceil(C/64) channel chunks.
+static void set_i2c_kloop(Params& p, int C, int k) {
+  p.num_kb = k * k * ((C + BK - 1) / BK);
+  p.kb_per_split = p.num_kb;
 }
 
 static bool conv_tc_shape(const pc_conv_geom& g) {
@@ -1110,7 +1142,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   }
   int M = g.B * g.Ho * g.Wo, K = g.k * g.k * g.C;
   Params p = base_params(M, g.N, K);
-  const bool i2c = im2col_ok(g.cs, g.C, g.cstride);
+  const bool i2c = im2col_k_ok(g.cs, g.C, g.cstride);
   const Tile t = pick_k(M, g.N, i2c);
   int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, t.bn / t.cg);
   if (rc) return rc;
@@ -1126,6 +1158,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
                          g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
     if (rc) return rc;
     set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
+    set_i2c_kloop(p, g.C, g.k);
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
   return launch_kb<A_GATHER_FWD, EPI_BF16>(p, t, 1, st);
@@ -1186,6 +1219,7 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
                          lo + g.H - g.Ho, 1);
     if (rc) return rc;
     set_i2c(p, g.N, g.N, g.k, 1, lo, g.W, g.H);
+    set_i2c_kloop(p, g.N, g.k);
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
   return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, t, 1, st);
