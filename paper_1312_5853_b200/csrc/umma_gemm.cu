@@ -292,6 +292,10 @@ constexpr int tmem_cols() {
 }
 
 template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM <= A_GATHER_WGRAD; }
+// cp.async gather producers (warps 6..): 8 warps, each thread 16 B per row for
+// 1024 / GATHER_THREADS rows of the 128 x 64 stage.
+constexpr int GATHER_THREADS = 256;
+constexpr int GR = 1024 / GATHER_THREADS;  // rows (fwd/dgrad) or pixel rows (wgrad) per gather thread
 template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN; }
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
@@ -438,8 +442,10 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
   }
 }
 
+template <int AM> constexpr int kernel_threads() { return a_is_gather<AM>() ? 192 + GATHER_THREADS : 320; }
+
 template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
-__global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __grid_constant__ Params p) {
   constexpr bool GATHER = a_is_gather<AM>();
   constexpr int EPW = GATHER ? 1 : 2;  // epilogue warps per TMEM lane quadrant (warps 0-3, and 6-9 unless gathering)
   static_assert(!(GATHER && CG == 2), "the cp.async gather producers are single-CTA");
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
   if (warp == 4) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
-        mbar_init(&full[s], 1 + (GATHER ? 128 : 0));
+        mbar_init(&full[s], 1 + (GATHER ? GATHER_THREADS : 0));
         mbar_init(&empty[s], 1);
       }
       for (int a = 0; a < ACC; ++a) {
@@ -643,11 +649,12 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
         const int m0 = tc.m0;
         if constexpr (AM == A_GATHER_FWD || AM == A_GATHER_DGRAD) {
           // K-major rows = pixels; thread owns 16B chunk q of rows rb + 16*r8
+          constexpr int RS = GATHER_THREADS / 8;  // row stride between a thread's rows
           const int q = gt & 7, rb = gt >> 3;
-          int rb_b[8], ry[8], rx[8];
+          int rb_b[GR], ry[GR], rx[GR];
 #pragma unroll
-          for (int r8 = 0; r8 < 8; ++r8) {
-            int m = m0 + rb + 16 * r8;
+          for (int r8 = 0; r8 < GR; ++r8) {
+            int m = m0 + rb + RS * r8;
             int W_ = AM == A_GATHER_FWD ? g.Wo : g.W, H_ = AM == A_GATHER_FWD ? g.Ho : g.H;
             if (m < p.M) {
               int x = m % W_, q2 = m / W_;
@@ -681,8 +688,8 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
               int blk = c / g.cs, coff = c - blk * g.cs;
               const __nv_bfloat16* src0 = p.gsrc + blk * g.cstride + coff;
 #pragma unroll
-              for (int r8 = 0; r8 < 8; ++r8) {
-                int r = rb + 16 * r8;
+              for (int r8 = 0; r8 < GR; ++r8) {
+                int r = rb + RS * r8;
                 int iy = ry[r8] + i, ix = rx[r8] + j;
                 bool ok = kvalid && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
                 const __nv_bfloat16* src =
@@ -695,8 +702,8 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
               int i = ij / g.k, j = ij - (ij / g.k) * g.k;
               const __nv_bfloat16* src0 = p.gsrc + n;
 #pragma unroll
-              for (int r8 = 0; r8 < 8; ++r8) {
-                int r = rb + 16 * r8;
+              for (int r8 = 0; r8 < GR; ++r8) {
+                int r = rb + RS * r8;
                 int ny = ry[r8] - i, nx = rx[r8] - j;
                 bool ok = kvalid && ny >= 0 && nx >= 0;
                 int oy = 0, ox = 0;
@@ -716,6 +723,7 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
           }
         } else {
           // A_GATHER_WGRAD: MN-major rows = pixels (K), chunk q = 8 consecutive (i,j,c) of this M tile
+          constexpr int PS = GATHER_THREADS / 16;  // pixel stride between a thread's rows
           const int q = gt & 15, rb = gt >> 4;
           const int kc = m0 + q * 8;
           const bool mvalid = kc < p.M;
@@ -738,14 +746,14 @@ __global__ void __launch_bounds__(320, 1) umma_gemm_k(const __grid_constant__ Pa
             int oy = rem / g.Wo;
             int ox = rem - oy * g.Wo;
 #pragma unroll
-            for (int r8 = 0; r8 < 8; ++r8) {
-              int r = rb + 8 * r8;
-              bool ok = mvalid && (int)pix0 + 8 * r8 < p.K;
+            for (int r8 = 0; r8 < GR; ++r8) {
+              int r = rb + PS * r8;
+              bool ok = mvalid && (int)pix0 + PS * r8 < p.K;
               int iy = oy * g.stride + i - g.pad, ix = ox * g.stride + j - g.pad;
               ok = ok && (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
               const __nv_bfloat16* src = ok ? src0 + ((long long)(b * g.H + iy) * g.W + ix) * g.cs : p.gsrc;
               cp_async16(base + r * 128 + (((q & 7) ^ (r & 7)) << 4), src, ok);
-              ox += 8;
+              ox += PS;
               while (ox >= g.Wo) {
                 ox -= g.Wo;
                 if (++oy == g.Ho) { oy = 0; ++b; }
@@ -926,7 +934,7 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
   auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES, CG>;
   constexpr int smem = smem_bytes<BN, STAGES, CG>();
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
-  constexpr int threads = 320;
+  constexpr int threads = kernel_threads<AM>();
   static int resident = 0;  // persistent CTAs the device holds at once
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
