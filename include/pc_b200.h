@@ -97,6 +97,12 @@ PC_API int pc_conv2d_backward(const pc_conv_geom* g, const void* x, const void* 
  * when the FC consumes a cross concatenation). y is plain [B][U]. */
 PC_API int pc_fc_forward(int B, int D, int U, const pc_mat* x, const void* w, const float* bias,
                   void* y, int prec, int flags, pc_stream_t stream);
+/* Same with a caller workspace of pc_fc_forward_workspace() bytes: small-batch
+ * calls then split the K loop over the machine and sum the fp32 partials in a
+ * fixed order (bias/ReLU applied after the sum). pc_fc_forward == _ex without one. */
+PC_API size_t pc_fc_forward_workspace(int B, int D, int U, int prec);
+PC_API int pc_fc_forward_ex(int B, int D, int U, const pc_mat* x, const void* w, const float* bias, void* y,
+                            int prec, int flags, void* workspace, size_t workspace_bytes, pc_stream_t stream);
 /* gx(b, d) = sum_u gy[b][u] w[u][d] (written through the pc_mat view, masked
  * by `mask` viewed identically when PC_MASK_DX); gw[u][d] = sum_b gy[b][u] x(b, d);
  * gb[u] = sum_b gy[b][u]. */

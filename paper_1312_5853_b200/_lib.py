@@ -48,6 +48,8 @@ SIGNATURES = {
     "pc_conv2d_backward": (_i, [_P(ConvGeom), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _sz, _vp]),
     "pc_fc_forward": (_i, [_i, _i, _i, _P(Mat), _vp, _vp, _vp, _i, _i, _vp]),
     "pc_fc_backward_workspace": (_sz, [_i, _i, _i, _i]),
+    "pc_fc_forward_workspace": (_sz, [_i, _i, _i, _i]),
+    "pc_fc_forward_ex": (_i, [_i, _i, _i, _P(Mat), _vp, _vp, _vp, _i, _i, _vp, _sz, _vp]),
     "pc_fc_backward": (_i, [_i, _i, _i, _P(Mat), _vp, _vp, _P(Mat), _vp, _vp, _vp, _i, _i, _vp, _sz, _vp]),
     "pc_relu_forward": (_i, [_ll, _vp, _vp, _i, _vp]),
     "pc_relu_backward": (_i, [_ll, _vp, _vp, _vp, _i, _vp]),

@@ -1,6 +1,7 @@
 // extern "C" entry points for the contractions (conv / FC) and the shared
 // reductions; dispatches PC_FP32 to the exact-fp32 SIMT path and PC_BF16 to
 // the tcgen05 tensor-core path (umma_gemm.cu).
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -49,14 +50,16 @@ int reduce_partials(const float* ws, int splits, long long n, float* out, cudaSt
 
 // Bias gradients: pass 1 sums rows [r*RB, (r+1)*RB) per column block; pass 2
 // sums the row-block partials in ascending order. Fixed order => deterministic.
-// Row blocks are sized so pass 1 runs ~2 CTA waves and pass 2 reads <= 296
-// partial rows per column.
-static long long cs_rb(long long P) {
-  // ~296 row blocks (two waves of pass-1 CTAs), at least 64 rows each
-  long long rb = (P + 295) / 296;
-  return rb < 64 ? 64 : rb;
+// Row blocks are sized so pass 1 keeps ~8 CTAs per SM in flight; pass 2 gives
+// each column a warp (fixed-order strided sums, then a fixed shuffle tree).
+// Rows per pass-1 block: each of the CTA's row lanes (256 threads / 8-column groups)
+// sums ~24 rows, so pass 1 has many CTAs with many 16-byte loads in flight.
+static long long cs_rb(long long P, int N) {
+  const int groups = N % 8 == 0 ? N / 8 : 0;
+  const int lanes = groups ? 256 / (groups < 256 ? groups : 256) : 1;
+  return groups ? (long long)lanes * 24 : 512;
 }
-long long colsum_ws(long long P, int N) { return ((P + cs_rb(P) - 1) / cs_rb(P)) * (long long)N; }
+long long colsum_ws(long long P, int N) { return ((P + cs_rb(P, N) - 1) / cs_rb(P, N)) * (long long)N; }
 
 template <typename T>
 __global__ void colsum1_k(const T* __restrict__ g, long long P, int N, int RB, float* __restrict__ part) {
@@ -118,26 +121,58 @@ __global__ void __launch_bounds__(256) colsum1_v8_k(const T* __restrict__ g, lon
   }
 }
 
-// 32 columns x 8 row lanes per CTA; lanes combine in a fixed order (deterministic).
+// Pass 2: a CTA per 8 columns, 32 row lanes each (a warp reads 4 rows x 32 B);
+// lane partials are combined in a fixed order (deterministic).
 __global__ void colsum2_k(const float* __restrict__ part, int R, int N, float* __restrict__ out) {
-  __shared__ float sh[8][33];
-  const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + cx;
+  __shared__ float sh[32][9];
+  const int cx = threadIdx.x & 7, ry = threadIdx.x >> 3;
+  const int c = blockIdx.x * 8 + cx;
   float acc = 0.f;
   if (c < N)
-    for (int r = ry; r < R; r += 8) acc += part[(long long)r * N + c];
+#pragma unroll 4
+    for (int r = ry; r < R; r += 32) acc += part[(long long)r * N + c];
   sh[ry][cx] = acc;
   __syncthreads();
   if (ry == 0 && c < N) {
     float t = sh[0][cx];
-    for (int k = 1; k < 8; ++k) t += sh[k][cx];
+    for (int k = 1; k < 32; ++k) t += sh[k][cx];
     out[c] = t;
+  }
+}
+
+// Short reductions (FC: P = batch): one pass, a CTA per 512 columns, 4 row lanes
+// combined in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_short_k(const T* __restrict__ g, int P, int N, float* __restrict__ out) {
+  __shared__ float sh[4][64 * 8];
+  const int grp = blockIdx.x * 64 + (threadIdx.x & 63), lane = threadIdx.x >> 6;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (grp < N / 8) {
+    const T* col = g + (long long)grp * 8;
+#pragma unroll 4
+    for (int r = lane; r < P; r += 4) V8<T>::add(col + (long long)r * N, a);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sh[lane][(threadIdx.x & 63) * 8 + i] = a[i];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 512; t += 256) {
+    const int c = blockIdx.x * 512 + t;
+    if (c < N) out[c] = ((sh[0][t] + sh[1][t]) + sh[2][t]) + sh[3][t];
   }
 }
 
 int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, cudaStream_t st) {
   if (N == 0) return PC_OK;
-  const int RB = (int)cs_rb(P);
+  if (P > 0 && P <= 4096 && N % 8 == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+    const int blocks = (N + 511) / 512;
+    if (prec == PC_FP32)
+      colsum_short_k<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(g), (int)P, N, out);
+    else
+      colsum_short_k<__nv_bfloat16><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(g), (int)P, N, out);
+    PC_CUDA_CHECK_LAUNCH("colsum");
+    return PC_OK;
+  }
+  const int RB = (int)cs_rb(P, N);
   int R = (int)((P + RB - 1) / RB);
   if (R == 0) {
     cudaMemsetAsync(out, 0, sizeof(float) * N, st);
@@ -158,7 +193,7 @@ int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, c
     else
       colsum1_k<__nv_bfloat16><<<g1, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(g), P, N, RB, ws);
   }
-  colsum2_k<<<(N + 31) / 32, 256, 0, st>>>(ws, R, N, out);
+  colsum2_k<<<(N + 7) / 8, 256, 0, st>>>(ws, R, N, out);
   count_launches(1);
   PC_CUDA_CHECK_LAUNCH("colsum");
   return PC_OK;
@@ -253,19 +288,30 @@ static int check_mat(const pc_mat* m, const char* what) {
   return PC_OK;
 }
 
-extern "C" int pc_fc_forward(int B, int D, int U, const pc_mat* x, const void* w, const float* bias,
-                             void* y, int prec, int flags, pc_stream_t st) {
+extern "C" size_t pc_fc_forward_workspace(int B, int D, int U, int prec) {
+  return prec == PC_BF16 && B > 0 && D > 0 && U > 0 ? umma_fc_forward_ws(B, D, U) : 0;
+}
+
+extern "C" int pc_fc_forward_ex(int B, int D, int U, const pc_mat* x, const void* w, const float* bias, void* y,
+                                int prec, int flags, void* workspace, size_t ws_bytes, pc_stream_t st) {
   int rc = check_prec(prec);
   if (rc) return rc;
   PC_REQUIRE(B >= 0 && D > 0 && U > 0, PC_ESHAPE, "fc: bad extents B=%d D=%d U=%d", B, D, U);
   if (B == 0) return PC_OK;
   if ((rc = check_mat(x, "fc_forward x"))) return rc;
-  if (prec == PC_BF16) return umma_fc_forward(B, D, U, *x, w, bias, y, flags, S(st));
+  if (prec == PC_BF16) return umma_fc_forward(B, D, U, *x, w, bias, y, flags, S(st), workspace, ws_bytes);
   return simt_fc_forward(B, D, U, *x, w, bias, y, prec, flags, S(st));
 }
 
+extern "C" int pc_fc_forward(int B, int D, int U, const pc_mat* x, const void* w, const float* bias,
+                             void* y, int prec, int flags, pc_stream_t st) {
+  return pc_fc_forward_ex(B, D, U, x, w, bias, y, prec, flags, nullptr, 0, st);
+}
+
 extern "C" size_t pc_fc_backward_workspace(int B, int D, int U, int prec) {
-  return (size_t)colsum_ws(B, U) * sizeof(float) + umma_fc_extra_ws(B, D, U, prec);
+  // the data gradient's split-K partials run first and reuse the weight gradient's region
+  size_t dg = prec == PC_BF16 && B > 0 ? umma_fc_dgrad_ws(B, D, U) : 0;
+  return (size_t)colsum_ws(B, U) * sizeof(float) + std::max(umma_fc_extra_ws(B, D, U, prec), dg);
 }
 
 extern "C" int pc_fc_backward(int B, int D, int U, const pc_mat* x, const void* w, const void* gy,
@@ -280,7 +326,7 @@ extern "C" int pc_fc_backward(int B, int D, int U, const pc_mat* x, const void* 
     if ((rc = check_mat(gx, "fc_backward gx"))) return rc;
     if (B > 0) {
       const void* mk = (flags & PC_MASK_DX) ? mask : nullptr;
-      rc = prec == PC_BF16 ? umma_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st))
+      rc = prec == PC_BF16 ? umma_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st), workspace, ws_bytes)
                            : simt_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st), prec);
       if (rc) return rc;
     }

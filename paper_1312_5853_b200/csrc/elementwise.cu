@@ -80,6 +80,93 @@ __global__ void relu_bwd_k(long long n, const T* __restrict__ x, const T* __rest
 
 // Max-pool ---------------------------------------------------------------------
 // One thread per (b, oy, ox, 8-channel group) when C % 8 == 0, else per channel.
+// bf16 3x3 / stride-2 max-pool forward (8 channels per thread). Fast path for
+// windows whose 9 x 8 values are all non-negative and not NaN (the network's
+// ReLU outputs): raw bf16 bit patterns are then order-preserving, so one 32-bit
+// integer max over (bits << 16 | 15 - index) gives the maximum and, among equal
+// values, the first window position — np.argmax's rule, bit-exact. Any negative value or NaN in the window falls back to the exact
+// float comparison (first NaN wins, -0 == +0).
+__global__ void maxpool_fwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int Wo,
+                                        const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                        uint8_t* __restrict__ arg) {
+  const unsigned cg = (unsigned)(C >> 3);
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (unsigned)B * Ho * Wo * cg) return;
+  const unsigned pix = t / cg;
+  const int c0 = (int)(t - pix * cg) * 8;
+  const unsigned row = pix / (unsigned)Wo;
+  const int ox = (int)(pix - row * Wo);
+  const int b = (int)(row / (unsigned)Ho);
+  const int oy = (int)(row - (unsigned)b * Ho);
+  uint4 r[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const __nv_bfloat16* xr = x + (((long long)b * H + oy * 2 + i) * W + ox * 2) * C + c0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) r[i * 3 + j] = __ldg(reinterpret_cast<const uint4*>(xr + (long long)j * C));
+  }
+  // keys: (bf16 bits << 16) | (15 - window index): one 32-bit max per channel and
+  // element gives the largest value and, among equal values, the first index
+  uint32_t sign = 0, mk[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) mk[v] = 0u;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    const uint32_t w[4] = {r[e].x, r[e].y, r[e].z, r[e].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      sign |= w[q];
+      mk[2 * q] = max(mk[2 * q], (w[q] << 16) | (uint32_t)(15 - e));
+      mk[2 * q + 1] = max(mk[2 * q + 1], (w[q] & 0xFFFF0000u) | (uint32_t)(15 - e));
+    }
+  }
+  bool nan = false;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) nan |= (mk[v] >> 16) > 0x7F80u;
+  const long long o = (long long)pix * C + c0;
+  if ((sign & 0x80008000u) == 0u && !nan) {
+    uint4 outv;
+    outv.x = (mk[0] >> 16) | (mk[1] & 0xFFFF0000u);
+    outv.y = (mk[2] >> 16) | (mk[3] & 0xFFFF0000u);
+    outv.z = (mk[4] >> 16) | (mk[5] & 0xFFFF0000u);
+    outv.w = (mk[6] >> 16) | (mk[7] & 0xFFFF0000u);
+    *reinterpret_cast<uint4*>(y + o) = outv;
+    uint2 packed;
+    packed.x = (15u - (mk[0] & 15u)) | ((15u - (mk[1] & 15u)) << 8) | ((15u - (mk[2] & 15u)) << 16) |
+               ((15u - (mk[3] & 15u)) << 24);
+    packed.y = (15u - (mk[4] & 15u)) | ((15u - (mk[5] & 15u)) << 8) | ((15u - (mk[6] & 15u)) << 16) |
+               ((15u - (mk[7] & 15u)) << 24);
+    *reinterpret_cast<uint2*>(arg + o) = packed;
+    return;
+  }
+  float best[8];
+  int bi[8];
+  unsigned short bits[8];  // the winner's original bits (NaN payload kept)
+#pragma unroll
+  for (int v = 0; v < 8; ++v) { best[v] = 0.f; bi[v] = -1; bits[v] = 0; }
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    const uint32_t w[4] = {r[e].x, r[e].y, r[e].z, r[e].w};
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const unsigned short hb = (unsigned short)(w[v >> 1] >> (16 * (v & 1)));
+      const float val = __uint_as_float((uint32_t)hb << 16);
+      const bool nan_v = val != val, nan_b = best[v] != best[v];
+      if (bi[v] < 0 || (!nan_b && (val > best[v] || nan_v))) { best[v] = val; bi[v] = e; bits[v] = hb; }
+    }
+  }
+  uint4 outv;
+  outv.x = bits[0] | ((uint32_t)bits[1] << 16);
+  outv.y = bits[2] | ((uint32_t)bits[3] << 16);
+  outv.z = bits[4] | ((uint32_t)bits[5] << 16);
+  outv.w = bits[6] | ((uint32_t)bits[7] << 16);
+  uint2 packed;
+  packed.x = (uint32_t)bi[0] | ((uint32_t)bi[1] << 8) | ((uint32_t)bi[2] << 16) | ((uint32_t)bi[3] << 24);
+  packed.y = (uint32_t)bi[4] | ((uint32_t)bi[5] << 8) | ((uint32_t)bi[6] << 16) | ((uint32_t)bi[7] << 24);
+  *reinterpret_cast<uint4*>(y + o) = outv;
+  *reinterpret_cast<uint2*>(arg + o) = packed;
+}
+
 template <typename T, int V, int KS = 0, int SS = 0>
 __global__ void maxpool_fwd_k(int B, int H, int W, int C, int k_, int s_, int Ho, int Wo,
                               const T* __restrict__ x, T* __restrict__ y, uint8_t* __restrict__ arg) {
@@ -539,7 +626,10 @@ extern "C" int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, cons
   long long work = (long long)B * Ho * Wo * (vec ? C / 8 : C);
   PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
   DISPATCH_PREC(prec, T, {
-    if (vec && k == 3 && s == 2)
+    if (vec && k == 3 && s == 2 && prec == PC_BF16 && aligned(x, 16))
+      maxpool_fwd_bf16_k3s2_k<<<grid_for(work, 256), 256, 0, S(st)>>>(
+          B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), argmax);
+    else if (vec && k == 3 && s == 2)
       maxpool_fwd_k<T, 8, 3, 2><<<grid_for(work, 256), 256, 0, S(st)>>>(
           B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(x), static_cast<T*>(y), argmax);
     else if (vec)

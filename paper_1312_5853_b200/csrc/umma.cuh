@@ -15,9 +15,11 @@ long long umma_wgrad_splits(const pc_conv_geom& g);
 size_t umma_conv_extra_ws(const pc_conv_geom& g, int prec);
 
 int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const float* bias, void* y,
-                    int flags, cudaStream_t st);
+                    int flags, cudaStream_t st, void* ws, size_t ws_bytes);
+size_t umma_fc_forward_ws(int B, int D, int U);
 int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_mat& gx, const void* mask,
-                  cudaStream_t st);
+                  cudaStream_t st, void* ws, size_t ws_bytes);
+size_t umma_fc_dgrad_ws(int B, int D, int U);
 int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* gw, float* part,
                   cudaStream_t st);
 size_t umma_fc_extra_ws(int B, int D, int U, int prec);

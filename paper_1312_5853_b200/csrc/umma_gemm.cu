@@ -1315,8 +1315,83 @@ static bool tma_view_ok(const pc_mat& v, long long inner_total) {
          (!blocked || (v.cb % 64 == 0 && v.bstride % 8 == 0));
 }
 
+// Small-M FC GEMMs (M = batch): the weights must stream through the SMs once,
+// so the K loop is split over enough CTA pairs to fill the machine and the fp32
+// partials are summed (in slice order: deterministic) by a fused epilogue kernel
+// (bias, ReLU, producer mask, bf16 store). Large-M calls keep the direct epilogue.
+struct FcPlan {
+  Tile t;
+  int splits;
+};
+static FcPlan fc_split_plan(int M, int N, int K) {
+  const int cg = (M > BM && cg2_enabled()) ? 2 : 1;
+  const Tile t{256, cg};
+  const long long tiles = (long long)((M + BM * cg - 1) / (BM * cg)) * ((N + t.bn - 1) / t.bn);
+  const int cap = 148 / cg, kbs = (K + BK - 1) / BK;
+  if (tiles * 2 > cap || kbs < 8) return {t, 1};
+  int sp = (int)std::min<long long>(cap / tiles, kbs / 4);
+  if (sp < 2) return {t, 1};
+  const int per = (kbs + sp - 1) / sp;
+  return {t, (kbs + per - 1) / per};
+}
+
+__global__ void fc_reduce_epilogue_k(const float* __restrict__ part, int splits, int M, int N,
+                                     const float* __restrict__ bias, int relu, const __nv_bfloat16* __restrict__ mask,
+                                     __nv_bfloat16* __restrict__ out, long long o_ld, long long o_cb,
+                                     long long o_bstride) {
+  const int groups = N / 8;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)M * groups) return;
+  const int m = (int)(t / groups), n0 = (int)(t - (long long)m * groups) * 8;
+  const size_t stride = (size_t)M * N;
+  const float* src = part + (size_t)m * N + n0;
+  float4 a = __ldg(reinterpret_cast<const float4*>(src)), b = __ldg(reinterpret_cast<const float4*>(src) + 1);
+  for (int z = 1; z < splits; ++z) {
+    const float4 c = __ldg(reinterpret_cast<const float4*>(src + z * stride));
+    const float4 d = __ldg(reinterpret_cast<const float4*>(src + z * stride) + 1);
+    a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+    b.x += d.x; b.y += d.y; b.z += d.z; b.w += d.w;
+  }
+  float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (bias) o[q] += __ldg(bias + n0 + q);
+    if (relu) o[q] = o[q] > 0.f ? o[q] : 0.f;
+  }
+  const long long blk = n0 / o_cb;
+  const long long idx = blk * o_bstride + (long long)m * o_ld + (n0 - blk * o_cb);
+  if (mask) {
+    const uint4 mk = *reinterpret_cast<const uint4*>(mask + idx);
+    const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mk);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = __bfloat162float(mb[q]) > 0.f ? o[q] : 0.f;
+  }
+  uint4 u;
+  __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) hh[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
+  *reinterpret_cast<uint4*>(out + idx) = u;
+}
+
+static int fc_reduce_epilogue(const float* part, int splits, int M, int N, const float* bias, int relu,
+                              const void* mask, void* out, long long o_ld, long long o_cb, long long o_bstride,
+                              cudaStream_t st) {
+  const long long work = (long long)M * (N / 8);
+  fc_reduce_epilogue_k<<<(int)((work + 255) / 256), 256, 0, st>>>(
+      part, splits, M, N, bias, relu, static_cast<const __nv_bfloat16*>(mask), static_cast<__nv_bfloat16*>(out),
+      o_ld, o_cb, o_bstride);
+  PC_CUDA_CHECK_LAUNCH("fc_reduce_epilogue");
+  return PC_OK;
+}
+
+static size_t fc_split_bytes(int M, int N, int K) {
+  const FcPlan fp = fc_split_plan(M, N, K);
+  return fp.splits > 1 && N % 8 == 0 ? (size_t)fp.splits * M * N * sizeof(float) : 0;
+}
+size_t umma_fc_forward_ws(int B, int D, int U) { return fc_split_bytes(B, U, D); }
+
 int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const float* bias, void* y, int flags,
-                    cudaStream_t st) {
+                    cudaStream_t st, void* ws, size_t ws_bytes) {
   if (!(tma_view_ok(x, D) && D % 8 == 0 && U % 8 == 0)) {
     g_simt_launches++;
     return simt_fc_forward(B, D, U, x, w, bias, y, PC_BF16, flags, st);
@@ -1326,6 +1401,19 @@ int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const f
   int rc = make_map(&p.tma_a, x.ptr, cb, B, D / cb, x.ld, x.bstride, BM);
   if (rc) return rc;
   p.a_cb = cb < D ? (int)cb : 0;
+  const size_t need = fc_split_bytes(B, U, D);
+  if (need && ws && ws_bytes >= need) {
+    const FcPlan fp = fc_split_plan(B, U, D);
+    if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, fp.t.bn / fp.t.cg))) return rc;
+    p.b_cb = 0;
+    p.kb_per_split = ceil_div(p.num_kb, fp.splits);
+    p.out = ws;
+    p.o_ld = U;
+    p.split_stride = (long long)B * U;
+    if ((rc = launch_kb<A_TMA_K, EPI_F32>(p, fp.t, fp.splits, st))) return rc;
+    return fc_reduce_epilogue(static_cast<const float*>(ws), fp.splits, B, U, bias, (flags & PC_RELU) != 0, nullptr,
+                              y, U, 1LL << 40, 0, st);
+  }
   const Tile t = pick_k(B, U, true);
   if ((rc = make_map(&p.tma_b, w, D, U, 1, D, 0, t.bn / t.cg))) return rc;
   p.b_cb = 0;
@@ -1336,8 +1424,10 @@ int umma_fc_forward(int B, int D, int U, const pc_mat& x, const void* w, const f
   return launch_kb<A_TMA_K, EPI_BF16>(p, t, 1, st);
 }
 
+size_t umma_fc_dgrad_ws(int B, int D, int U) { return fc_split_bytes(B, D, U); }
+
 int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_mat& gx, const void* mask,
-                  cudaStream_t st) {
+                  cudaStream_t st, void* ws, size_t ws_bytes) {
   if (!(D % 8 == 0 && U % 8 == 0 && gx.ld % 8 == 0 && (gx.cb >= D || gx.cb % 8 == 0))) {
     g_simt_launches++;
     return simt_fc_dgrad(B, D, U, w, gy, gx, mask, st, PC_BF16);
@@ -1346,6 +1436,19 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
   int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, BM);
   if (rc) return rc;
   p.a_cb = 0;
+  const size_t need = fc_split_bytes(B, D, U);
+  if (need && ws && ws_bytes >= need) {
+    const FcPlan fp = fc_split_plan(B, D, U);
+    if ((rc = setup_mn_b(p, w, D, U, 1, D, 0, fp.t))) return rc;
+    p.b_cb = 0;
+    p.kb_per_split = ceil_div(p.num_kb, fp.splits);
+    p.out = ws;
+    p.o_ld = D;
+    p.split_stride = (long long)B * D;
+    if ((rc = launch_mn<A_TMA_K, EPI_F32>(p, fp.t, fp.splits, st))) return rc;
+    return fc_reduce_epilogue(static_cast<const float*>(ws), fp.splits, B, D, nullptr, 0, mask, gx.ptr, gx.ld,
+                              gx.cb, gx.bstride, st);
+  }
   const Tile t = pick_mn(B, D, true);
   if ((rc = setup_mn_b(p, w, D, U, 1, D, 0, t))) return rc;
   p.b_cb = 0;

@@ -242,7 +242,8 @@ class ColumnEngine:
                 ws = max(ws, self.lib.raw("pc_conv2d_backward_workspace")(C.byref(st.geom), self.prec))
             elif st.kind == "fc":
                 d = math.prod(st.in_nhwc)
-                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B, d, st.cl.out_shape[0], self.prec))
+                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B, d, st.cl.out_shape[0], self.prec),
+                         self.lib.raw("pc_fc_forward_workspace")(self.B, d, st.cl.out_shape[0], self.prec))
         self.ws_bytes = int(ws)
         self.ws = torch.empty(max(self.ws_bytes, 16), dtype=torch.uint8, device=self.device)
 
@@ -395,8 +396,9 @@ class ColumnEngine:
             d = math.prod(st.in_nhwc)
             mat = self._in_mat(st)
             flags = L.PC_RELU if st.relu_after else 0
-            self._call(st, "pc_fc_forward", self.B, d, st.cl.out_shape[0], C.byref(mat), self._w_lowp(st),
-                     self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, s)
+            self._call(st, "pc_fc_forward_ex", self.B, d, st.cl.out_shape[0], C.byref(mat), self._w_lowp(st),
+                       self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, self.ws.data_ptr(),
+                       self.ws_bytes, s)
         elif st.kind == "relu":
             if not st.relu_fused_fwd:
                 self._call(st, "pc_relu_forward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),

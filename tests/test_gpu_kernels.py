@@ -180,6 +180,33 @@ def test_maxpool_bf16_argmax_bit_exact():
     assert np.array_equal(y, ry)
 
 
+@pytest.mark.parametrize("case", ["relu_ties", "mixed_sign", "nan_and_negzero"])
+def test_maxpool_bf16_simd_fast_path_bit_exact(case):
+    """The bf16 3x3/s2 pool compares raw bit patterns (16-bit SIMD) when a window
+    holds only non-negative, non-NaN values (ReLU outputs) and falls back to float
+    comparison otherwise; both must give np.argmax's first maximum bit-exactly,
+    including zero ties, NaN (first NaN wins) and -0 == +0."""
+    from paper_1312_5853_b200 import kernels as K
+    rs = np.random.RandomState(11)
+    x = np.round(rs.randn(3, 24, 15, 15) * 3) / 4
+    if case == "relu_ties":
+        x = np.maximum(x, 0.0)                      # many exact zeros and value ties
+    elif case == "nan_and_negzero":
+        x = np.maximum(x, 0.0)
+        x[0, :8, 2, 3] = np.nan
+        x[1, 5, 4, 4] = np.nan
+        x[1, 5, 4, 5] = np.nan
+        x[2, :, 0:3, 0:3] = -0.0
+        x[2, :4, 1, 1] = 0.0
+    x = bf16(x)
+    K.set_precision("bf16")
+    y, arg = K.maxpool_forward(x, 3, 2)
+    ry, rarg = O.maxpool_forward(x, 3, 2)
+    assert np.array_equal(arg, rarg)
+    assert np.array_equal(np.isnan(y), np.isnan(ry))
+    assert np.array_equal(np.nan_to_num(y, nan=7.0), np.nan_to_num(ry, nan=7.0))
+
+
 # ------------------------------------------- tensor-core path coverage (bf16)
 
 def _tc_counts():
