@@ -40,7 +40,7 @@ namespace umma {
 // cp.async gather kept for geometries the im2col box cannot express.
 enum AMode {
   A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FWD = 2, A_GATHER_DGRAD = 3, A_GATHER_WGRAD = 4,
-  A_IM2COL_K = 5, A_IM2COL_MN = 6
+  A_IM2COL_K = 5, A_IM2COL_MN = 6, A_HALO_K = 7
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2 };
@@ -73,6 +73,15 @@ struct alignas(64) Params {
   // chunk past the channel extent — TMA zero-fills it — and the MMA issues only the
   // k16 steps that hold real channels.
   int i2c_cpt;
+  // Halo (shifted-window) A for stride-1 convs: a tile is halo_R output rows x Wv
+  // virtual columns of one image (Wv = Wo rounded up to 8). For each 64-channel
+  // chunk and filter column j, one TMA box brings the tile's input window
+  // (halo_R + k - 1 rows x Wv columns starting at column j + lo, zero outside the
+  // image) into shared memory; the A operand of tap (i, j) is that buffer shifted by
+  // i * Wv rows (a multiple of 8 rows: the tensor core reads such shifted 128B-swizzled
+  // tiles at full rate; odd row shifts work but run ~3x slower, tools/desc_probe.cu).
+  // Columns x >= Wo are discarded.
+  int halo_R, halo_tpi, halo_Wv, halo_lo, halo_bytes;
   unsigned long long* trace;  // debug: per-CTA per-tile clock64 stamps (tools/trace_gemm.py), normally null
 };
 
@@ -291,6 +300,9 @@ constexpr int tmem_cols() {
   return BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
 }
 
+// Halo stage: the input window for (channel chunk, filter column j) (<= 256 rows of
+// 64 channels) plus the B tiles of that column's k filter rows (k <= HALO_KMAX).
+constexpr int HALO_SLOT_BYTES = 256 * 128, HALO_KMAX = 5;
 template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM <= A_GATHER_WGRAD; }
 // cp.async gather producers (warps 6..): 8 warps, each thread 16 B per row for
 // 1024 / GATHER_THREADS rows of the 128 x 64 stage.
@@ -299,9 +311,13 @@ constexpr int GR = 1024 / GATHER_THREADS;  // rows (fwd/dgrad) or pixel rows (wg
 template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN; }
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
-template <int BN, int STAGES, int CG>
+template <int BN, int CG>
+constexpr int halo_stage_bytes() { return HALO_SLOT_BYTES + HALO_KMAX * (BN / CG) * BK * 2; }
+template <int BN, int STAGES, int CG, bool HALO = false>
 constexpr int smem_bytes() {
-  return 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + (BN / CG) * BK * 2) + (2 * STAGES + 4) * 8 + 16;
+  return 1024 /*align slack*/ + (HALO ? STAGES * halo_stage_bytes<BN, CG>()
+                                      : STAGES * (A_STAGE_BYTES + (BN / CG) * BK * 2)) +
+         (2 * STAGES + 4) * 8 + 16;
 }
 
 // ------------------------------------------------------------------- kernel
@@ -343,7 +359,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Epilogue: drain one accumulator (this CTA's 128 rows x BN fp32 in TMEM) per
 // tile. EPW warps per TMEM lane quadrant split the 16-column chunks. Output
 // addressing keeps (channel block, offset) incrementally — no divisions.
-template <int EPI, int BN, int CG, int EPW>
+template <int EPI, int BN, int CG, int EPW, bool HALO>
 __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty, int unit,
                                          int units, uint32_t rank, int quad, int grp, int lane) {
   constexpr int TCOLS = tmem_cols<BN>();
@@ -356,8 +372,15 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
     mbar_wait(&tfull[acc], (lt / ACC) & 1);
     tc_fence_after();
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
-    const long long m = (long long)tc.m0 + (long long)rank * BM + row;
-    const bool mrow = m < p.M;
+    long long m = (long long)tc.m0 + (long long)rank * BM + row;
+    bool mrow = m < p.M;
+    if constexpr (HALO) {  // TMEM row -> (image, output row, column) of this CTA's halo tile
+      const int tile = (tc.m0 + (int)rank * BM) / BM;
+      const int hb = tile / p.halo_tpi, yy = row / p.halo_Wv, xx = row - yy * p.halo_Wv;
+      const int y = (tile - hb * p.halo_tpi) * p.halo_R + yy;
+      mrow = mrow && yy < p.halo_R && y < p.i2c_Ho && xx < p.i2c_Wo;
+      m = ((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx;
+    }
     const uint32_t tbase = tmem + acc * TCOLS + ((uint32_t)(quad * 32) << 16);
     const long long rowoff = m * p.o_ld;
     // (blk, rem) of output column n = n0 + c0 in a channel-blocked view (o_cb % 8 == 0)
@@ -460,9 +483,15 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr bool HALO = AM == A_HALO_K;
+  // stage s: A at sA + s * A_STRIDE, B at sB + s * B_STRIDE (a halo stage holds its
+  // window and its k B tiles contiguously)
+  constexpr int A_STRIDE = HALO ? halo_stage_bytes<BN, CG>() : A_STAGE_BYTES;
+  constexpr int B_STRIDE = HALO ? halo_stage_bytes<BN, CG>() : B_STAGE_BYTES;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  uint8_t* sB = HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (HALO ? halo_stage_bytes<BN, CG>()
+                                                                       : A_STAGE_BYTES + B_STAGE_BYTES));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [ACC]
   uint64_t* tempty = tfull + 2;      // [ACC]
@@ -485,6 +514,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], 4 * EPW * CG);
       }
+
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -528,6 +558,15 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       // A_IM2COL_MN: per-chunk (i, j, blk, coff) of the tile's M rows (fixed) and kb's pixel (b, oy, ox)
       int ci[BM / 64], cj[BM / 64], cblk[BM / 64], ccoff[BM / 64];
       int pb = 0, poy = 0, pox = 0;
+      // A_HALO_K: this CTA's tile (image hb, first output row hy0); K walks chunk-major
+      int hb = 0, hy0 = 0;
+      if constexpr (HALO) {  // k-block = (channel chunk, filter column j), j fastest
+        const int tile = m0 / BM;
+        hb = tile / p.halo_tpi;
+        hy0 = (tile - hb * p.halo_tpi) * p.halo_R;
+        kc = (tc.kb_begin / p.i2c_k) * BK;
+        kj = tc.kb_begin - (tc.kb_begin / p.i2c_k) * p.i2c_k;
+      }
       if constexpr (AM == A_IM2COL_K) {
         t_ox = m0 % p.i2c_Wo;
         const int q = m0 / p.i2c_Wo;
@@ -563,7 +602,15 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         mbar_wait(&empty[s], ph ^ 1);
         const long long c1 = p.trace ? clk() : 0;
         const int kb = tc.kb_begin + it;
-        if (elect_one()) {
+        if (HALO && elect_one()) {
+          // the window for (chunk, column j) and the B tiles of taps (0..k-1, j)
+          if (leader) mbar_arrive_expect_tx(&full[s], CG * (p.halo_bytes + p.i2c_k * B_STAGE_BYTES));
+          const uint32_t st0 = smem_u32(sA + s * A_STRIDE);
+          tma_load_4d<CG>(&p.tma_a, &full[s], st0, kc, p.halo_lo + kj, hy0 + p.halo_lo, hb);
+          for (int i = 0; i < p.i2c_k; ++i)
+            tma_load_3d<CG>(&p.tma_b, &full[s], st0 + HALO_SLOT_BYTES + i * B_STAGE_BYTES,
+                            (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
+        } else if (!HALO && elect_one()) {
           if (leader) mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES)));
           const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
           if constexpr (B_MN) {
@@ -619,6 +666,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             ++ktap;
             if (++kj == p.i2c_k) { kj = 0; ++ki; }
           }
+        } else if constexpr (HALO) {
+          if (++kj == p.i2c_k) { kj = 0; kc += BK; }
         } else if constexpr (AM == A_IM2COL_MN) {
           pox += BK;
           while (pox >= p.i2c_Wo) {
@@ -786,12 +835,18 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         // K-major im2col with a partial last channel chunk: k16 steps with real channels
         const bool partial = AM == A_IM2COL_K && (p.i2c_C % BK) != 0;
         int mchunk = partial ? tc.kb_begin % p.i2c_cpt : 0;
+        // halo: k-block = (channel chunk, filter column j): k filter rows per stage
+        int hj = HALO ? tc.kb_begin % p.i2c_k : 0, hch = HALO ? tc.kb_begin / p.i2c_k : 0;
         for (int it = 0; it < tc.nkb; ++it, ++git) {
           int nk16 = BK / 16;
           if (partial) {
             const int left = p.i2c_C - mchunk * BK;
             if (left < BK) nk16 = (left + 15) / 16;
             if (++mchunk == p.i2c_cpt) mchunk = 0;
+          }
+          if constexpr (HALO) {
+            const int left = p.i2c_C - hch * BK;
+            if (left < BK) nk16 = (left + 15) / 16;
           }
           const int s = git % STAGES;
           const uint32_t ph = (git / STAGES) & 1;
@@ -802,15 +857,31 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           if (it == 0 && lane == 0) trace_stamp(p, lt, 7);
           if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (elect_one()) {
-            const uint64_t ad = a0 + (uint64_t)((s * A_STAGE_BYTES) >> 4);
-            const uint64_t bd = b0 + (uint64_t)((s * B_STAGE_BYTES) >> 4);
+            const uint64_t ad = a0 + (uint64_t)((s * A_STRIDE) >> 4);
+            const uint64_t bd = b0 + (uint64_t)((s * B_STRIDE) >> 4);
+            if constexpr (HALO) {
+              // filter row i: the window shifted by i * Wv rows (multiple of 8), B tile i
+              const int k = p.i2c_k;
+              for (int i = 0; i < k; ++i) {
+                const uint64_t ai = ad + (uint64_t)((i * p.halo_Wv * 128) >> 4);
+                const uint64_t bi = bd + (uint64_t)((i * B_STAGE_BYTES) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              if (kk < nk16)
-                tc_mma<CG>(tacc, ad + kk * A_KSTEP, bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  if (kk < nk16)
+                    tc_mma<CG>(tacc, ai + kk * A_KSTEP, bi + kk * B_KSTEP, IDESC, (it > 0 || i > 0 || kk > 0) ? 1u : 0u);
+              }
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                if (kk < nk16)
+                  tc_mma<CG>(tacc, ad + kk * A_KSTEP, bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+            }
             tc_commit<CG>(&empty[s]);
           }
           __syncwarp();
+          if constexpr (HALO) {
+            if (++hj == p.i2c_k) { hj = 0; ++hch; }
+          }
           if (p.trace) {
             const long long c2 = clk();
             tr_wait += c1 - c0;
@@ -827,7 +898,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       }
     }
   } else {
-    epilogue<EPI, BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, warp & 3, warp >= 6 ? 1 : 0, lane);
+    epilogue<EPI, BN, CG, EPW, HALO>(p, tmem, tfull, tempty, unit, units, rank, warp & 3, warp >= 6 ? 1 : 0, lane);
   }
 
   tc_fence_before();
@@ -932,7 +1003,7 @@ static unsigned long long* g_trace = nullptr;  // pc_debug_trace_gemm
 template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
 static int launch(const Params& p, int splits, cudaStream_t st) {
   auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES, CG>;
-  constexpr int smem = smem_bytes<BN, STAGES, CG>();
+  constexpr int smem = smem_bytes<BN, STAGES, CG, AM == A_HALO_K>();
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   constexpr int threads = kernel_threads<AM>();
   static int resident = 0;  // persistent CTAs the device holds at once
@@ -1032,6 +1103,16 @@ static Tile pick_mn(int M, int N, bool pair_ok, int splits = 1) {
 
 template <int AM, int EPI>
 static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
+  if constexpr (AM == A_HALO_K) {  // stages of (window + k B tiles); N <= 128
+    if (t.cg == 2) {
+      if (t.bn <= 64) return launch<AM, B_TMA_K, EPI, 64, 4, 2>(p, splits, st);
+      if (t.bn <= 96) return launch<AM, B_TMA_K, EPI, 96, 3, 2>(p, splits, st);
+      return launch<AM, B_TMA_K, EPI, 128, 3, 2>(p, splits, st);
+    }
+    if (t.bn <= 64) return launch<AM, B_TMA_K, EPI, 64, 3, 1>(p, splits, st);
+    if (t.bn <= 96) return launch<AM, B_TMA_K, EPI, 96, 2, 1>(p, splits, st);
+    return launch<AM, B_TMA_K, EPI, 128, 2, 1>(p, splits, st);
+  } else {
   if constexpr (!a_is_gather<AM>()) {
     if (t.cg == 2) {
       switch (t.bn) {
@@ -1049,7 +1130,7 @@ static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
     case 128: return launch<AM, B_TMA_K, EPI, 128, 6, 1>(p, splits, st);
     case 192: return launch<AM, B_TMA_K, EPI, 192, 5, 1>(p, splits, st);
     default: return launch<AM, B_TMA_K, EPI, 256, 4, 1>(p, splits, st);
-  }
+  }  }
 }
 template <int AM, int EPI>
 static int launch_mn(const Params& p, Tile t, int splits, cudaStream_t st) {
@@ -1142,6 +1223,48 @@ static bool conv_tc_shape(const pc_conv_geom& g) {
   return g.C % 8 == 0 && g.cs % 8 == 0 && g.N % 8 == 0 && (g.C == g.cs || g.cstride % 8 == 0);
 }
 
+// Halo (shifted-window) A operand for a stride-1 conv whose GEMM N is narrow
+// (N <= 128: the im2col operand dominates the TMA traffic there). IN is the
+// unblocked NHWC input [B][Hi][Wi][Ci]; output pixel (y, x) reads IN(y + i + lo,
+// x + j + lo) for tap (i, j). Returns false when the geometry does not fit.
+// Default: narrow N (<= 128) with >= 16 taps per channel (AlexNet conv2 data
+// gradient: N = 96, 5x5). Few taps (3x3) leave the 128-row epilogue per tile
+// exposed, where the im2col path is faster. PC_HALO=0 off, 2 = whenever it fits.
+static bool halo_wanted(int N, int k) {
+  static const int mode = [] {
+    const char* e = getenv("PC_HALO");
+    return e ? atoi(e) : 1;
+  }();
+  return mode == 2 || (mode == 1 && N <= 128 && k * k >= 16);
+}
+static bool setup_halo(Params& p, const void* in, int B, int Hi, int Wi, int Ci, int k, int lo, int Ho, int Wo) {
+  const int Wv = (Wo + 7) / 8 * 8;
+  if (Wv > 128 || Ci % 8 || Ci < 64 || (reinterpret_cast<uintptr_t>(in) & 15) || !get_encode()) return false;
+  const int R = BM / Wv;
+  if (BM + (k - 1) * Wv > HALO_SLOT_BYTES / 128 || R + k - 1 > 256 || k > HALO_KMAX) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)Ci, (cuuint64_t)Wi, (cuuint64_t)Hi, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)Ci * 2, (cuuint64_t)Wi * Ci * 2, (cuuint64_t)Hi * Wi * Ci * 2};
+  cuuint32_t box[4] = {64u, (cuuint32_t)Wv, (cuuint32_t)(R + k - 1), 1u};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  if (g_encode(&p.tma_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(in), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  p.halo_R = R;
+  p.halo_tpi = (Ho + R - 1) / R;
+  p.halo_Wv = Wv;
+  p.halo_lo = lo;
+  p.halo_bytes = 64 * Wv * (R + k - 1) * 2;
+  p.M = B * p.halo_tpi * BM;  // virtual rows: one 128-row tile per halo tile
+  p.i2c_k = k;
+  p.i2c_C = Ci;
+  p.i2c_Ho = Ho;
+  p.i2c_Wo = Wo;
+  p.num_kb = k * ((Ci + BK - 1) / BK);  // k-blocks = (channel chunk, filter column)
+  p.kb_per_split = p.num_kb;
+  return true;
+}
+
 int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const float* bias, void* y,
                       int flags, cudaStream_t st) {
   if (!conv_tc_shape(g)) {
@@ -1150,8 +1273,10 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   }
   int M = g.B * g.Ho * g.Wo, K = g.k * g.k * g.C;
   Params p = base_params(M, g.N, K);
-  const bool i2c = im2col_k_ok(g.cs, g.C, g.cstride);
-  const Tile t = pick_k(M, g.N, i2c);
+  const bool halo = g.stride == 1 && g.C == g.cs && halo_wanted(g.N, g.k) &&
+                    setup_halo(p, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo);
+  const bool i2c = !halo && im2col_k_ok(g.cs, g.C, g.cstride);
+  const Tile t = pick_k(p.M, g.N, i2c || halo);
   int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, t.bn / t.cg);
   if (rc) return rc;
   p.b_cb = 0;
@@ -1161,6 +1286,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   p.o_ld = g.N;
   p.bias = bias;
   p.relu = (flags & PC_RELU) != 0;
+  if (halo) return launch_kb<A_HALO_K, EPI_BF16>(p, t, 1, st);
   if (i2c) {
     rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, BM, -g.pad, -g.pad,
                          g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
@@ -1204,12 +1330,20 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
       (reinterpret_cast<uintptr_t>(ws) + ws_bytes - need) & ~uintptr_t(127));
   long long total = (long long)g.N * KK * g.C;
   int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
-  const bool i2c = g.stride == 1 && im2col_ok(g.N, g.N, 0) && g.H + 2 * g.pad - g.k + 1 == g.Ho;
-  transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C, i2c ? 1 : 0);
+  const bool rot = g.stride == 1 && g.H + 2 * g.pad - g.k + 1 == g.Ho;  // dgrad = conv of gy with the rotated filter
+  const bool i2c = rot && im2col_ok(g.N, g.N, 0);
+  const bool halo_ok = rot && halo_wanted(g.C, g.k);
+  transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C,
+                                        (i2c || halo_ok) ? 1 : 0);
   PC_CUDA_CHECK_LAUNCH("transpose_w");
   int M = g.B * g.H * g.W, K = KK * g.N;
   Params p = base_params(M, g.C, K);
-  const Tile t = pick_k(M, g.C, i2c);
+  const bool halo = halo_ok && setup_halo(p, gy, g.B, g.Ho, g.Wo, g.N, g.k, g.pad - (g.k - 1), g.H, g.W);
+  if (halo_ok && !halo && !i2c) {  // rotated weights were written for a path that does not apply
+    transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C, 0);
+    PC_CUDA_CHECK_LAUNCH("transpose_w");
+  }
+  const Tile t = pick_k(p.M, g.C, i2c || halo);
   int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, t.bn / t.cg);
   if (rc) return rc;
   p.b_cb = 0;
@@ -1220,6 +1354,7 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
   p.o_cb = g.cs;
   p.o_bstride = g.cstride;
   p.mask = static_cast<const __nv_bfloat16*>(mask);
+  if (halo) return launch_kb<A_HALO_K, EPI_BF16>(p, t, 1, st);
   if (i2c) {
     // dgrad = forward conv of gy with the rotated filter, corner p-(k-1), walking dx's H x W
     const int lo = g.pad - (g.k - 1);

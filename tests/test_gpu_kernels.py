@@ -219,7 +219,10 @@ def _tc_counts():
 
 @pytest.mark.parametrize("geom", [(2, 96, 27, 27, 256, 5, 1, 2), (2, 256, 13, 13, 384, 3, 1, 1),
                                   (2, 384, 13, 13, 256, 3, 1, 1), (1, 8, 67, 67, 96, 11, 4, 0),
-                                  (3, 16, 10, 10, 24, 3, 1, 1)])
+                                  (3, 16, 10, 10, 24, 3, 1, 1),
+                                  # halo (shifted-window) operand: N <= 128, stride 1
+                                  (2, 64, 57, 57, 96, 3, 1, 0), (3, 96, 13, 13, 64, 3, 1, 1),
+                                  (2, 128, 31, 31, 96, 5, 1, 2)])
 def test_conv_bf16_alexnet_shapes_on_tensor_cores(geom):
     from paper_1312_5853_b200 import kernels as K
     b, c, h, w, n, k, s, p = geom
