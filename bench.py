@@ -234,7 +234,7 @@ def main():
     # Gaussian std 0.01 (the paper's cited Krizhevsky init, reference SPEC.md:120): the He-normal
     # default diverges to inf within 4 steps on AlexNet at lr 0.01 in the reference as well
     P.setup_workers(fab, plan, cs, P.init_dense_params(net, 0, std=0.01), P.SgdState())
-    res = P.hybrid_step(fab, plan, cs, x_host, y_host)          # builds engines, first step
+    res = P.hybrid_step(fab, plan, cs, x_e2e, y_host)           # builds engines, first step (resident batch = the pipeline format)
     run = S._runner(fab, plan, cs, gbatch // plan.data_shards)
     stream = torch.cuda.current_stream()
     scale = 1.0 / gbatch

@@ -140,31 +140,34 @@ __global__ void colsum2_k(const float* __restrict__ part, int R, int N, float* _
   }
 }
 
-// Short reductions (FC: P = batch): one pass, a CTA per 512 columns, 4 row lanes
-// combined in a fixed order.
+// Short reductions (FC: P = batch): one pass, a CTA per 64 columns (8 groups of
+// 8) x 32 row lanes; the lanes are combined in a fixed order.
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_short_k(const T* __restrict__ g, int P, int N, float* __restrict__ out) {
-  __shared__ float sh[4][64 * 8];
-  const int grp = blockIdx.x * 64 + (threadIdx.x & 63), lane = threadIdx.x >> 6;
+  __shared__ float sh[32][64 + 1];
+  const int q = threadIdx.x & 7, lane = threadIdx.x >> 3;
+  const int grp = blockIdx.x * 8 + q;
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (grp < N / 8) {
     const T* col = g + (long long)grp * 8;
 #pragma unroll 4
-    for (int r = lane; r < P; r += 4) V8<T>::add(col + (long long)r * N, a);
+    for (int r = lane; r < P; r += 32) V8<T>::add(col + (long long)r * N, a);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) sh[lane][(threadIdx.x & 63) * 8 + i] = a[i];
+  for (int i = 0; i < 8; ++i) sh[lane][q * 8 + i] = a[i];
   __syncthreads();
-  for (int t = threadIdx.x; t < 512; t += 256) {
-    const int c = blockIdx.x * 512 + t;
-    if (c < N) out[c] = ((sh[0][t] + sh[1][t]) + sh[2][t]) + sh[3][t];
+  if (threadIdx.x < 64) {
+    const int c = blockIdx.x * 64 + threadIdx.x;
+    float t = sh[0][threadIdx.x];
+    for (int l = 1; l < 32; ++l) t += sh[l][threadIdx.x];
+    if (c < N) out[c] = t;
   }
 }
 
 int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, cudaStream_t st) {
   if (N == 0) return PC_OK;
   if (P > 0 && P <= 4096 && N % 8 == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
-    const int blocks = (N + 511) / 512;
+    const int blocks = (N + 63) / 64;
     if (prec == PC_FP32)
       colsum_short_k<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(g), (int)P, N, out);
     else

@@ -306,7 +306,7 @@ constexpr int HALO_SLOT_BYTES = 256 * 128, HALO_KMAX = 5;
 template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM <= A_GATHER_WGRAD; }
 // cp.async gather producers (warps 6..): 8 warps, each thread 16 B per row for
 // 1024 / GATHER_THREADS rows of the 128 x 64 stage.
-constexpr int GATHER_THREADS = 256;
+constexpr int GATHER_THREADS = 512;
 constexpr int GR = 1024 / GATHER_THREADS;  // rows (fwd/dgrad) or pixel rows (wgrad) per gather thread
 template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN; }
 
