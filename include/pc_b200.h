@@ -138,6 +138,29 @@ PC_API int pc_softmax_xent(int B, int K, const void* logits, const int32_t* labe
 /* out[0] = sum_i v[i] in ascending order (one block; deterministic). */
 PC_API int pc_sum_f64(int n, const double* v, double* out, pc_stream_t stream);
 
+/* Fused momentum-SGD epilogue for a weight gradient (single-replica plans, where
+ * no cross-replica reduction sits between the gradient and the update): instead
+ * of storing gw, the producing kernel applies v = momentum*v - lr*(g + wd*p),
+ * p += v (and rewrites the bf16 shadow) to the parameters at gw's flat layout —
+ * kernels.sgd_step's arithmetic (kernels.py:319-341) without the gradient round
+ * trip through HBM. */
+typedef struct {
+  float* p;          /* fp32 master weights, same layout as the gradient */
+  float* v;          /* fp32 velocity */
+  void* p_lowp;      /* bf16 shadow of p (NULL: none) */
+  float lr, momentum, weight_decay;
+} pc_sgd_fuse;
+
+/* pc_conv2d_backward / pc_fc_backward with an optional fused update of the
+ * weights (upd != NULL: gw is not written; gb is). */
+PC_API int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const void* w, const void* gy,
+                                 void* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                                 void* workspace, size_t workspace_bytes, const pc_sgd_fuse* upd,
+                                 pc_stream_t stream);
+PC_API int pc_fc_backward_ex(int B, int D, int U, const pc_mat* x, const void* w, const void* gy,
+                             const pc_mat* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                             void* workspace, size_t workspace_bytes, const pc_sgd_fuse* upd, pc_stream_t stream);
+
 /* --- SGD: kernels.sgd_step (kernels.py:319-341), multi-tensor, one launch -- */
 typedef struct {
   float* p;          /* fp32 master parameters (updated in place) */

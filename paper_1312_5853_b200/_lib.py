@@ -35,6 +35,10 @@ class SgdTensor(C.Structure):
     _fields_ = [("p", _vp), ("v", _vp), ("g", _vp), ("p_lowp", _vp), ("n", _ll)]
 
 
+class SgdFuse(C.Structure):
+    _fields_ = [("p", _vp), ("v", _vp), ("p_lowp", _vp), ("lr", _f), ("momentum", _f), ("weight_decay", _f)]
+
+
 _P = C.POINTER
 SIGNATURES = {
     "pc_last_error": (C.c_char_p, []),
@@ -51,6 +55,10 @@ SIGNATURES = {
     "pc_fc_forward_workspace": (_sz, [_i, _i, _i, _i]),
     "pc_fc_forward_ex": (_i, [_i, _i, _i, _P(Mat), _vp, _vp, _vp, _i, _i, _vp, _sz, _vp]),
     "pc_fc_backward": (_i, [_i, _i, _i, _P(Mat), _vp, _vp, _P(Mat), _vp, _vp, _vp, _i, _i, _vp, _sz, _vp]),
+    "pc_fc_backward_ex": (_i, [_i, _i, _i, _P(Mat), _vp, _vp, _P(Mat), _vp, _vp, _vp, _i, _i, _vp, _sz,
+                               _P(SgdFuse), _vp]),
+    "pc_conv2d_backward_ex": (_i, [_P(ConvGeom), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _sz,
+                                   _P(SgdFuse), _vp]),
     "pc_relu_forward": (_i, [_ll, _vp, _vp, _i, _vp]),
     "pc_relu_backward": (_i, [_ll, _vp, _vp, _vp, _i, _vp]),
     "pc_maxpool_forward": (_i, [_i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),

@@ -3,6 +3,7 @@
 // the tcgen05 tensor-core path (umma_gemm.cu).
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -18,7 +19,7 @@ static std::atomic<unsigned long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 __global__ void reduce_partials_k(const float* __restrict__ ws, int splits, long long n,
-                                  float* __restrict__ out) {
+                                  float* __restrict__ out, pc_sgd_fuse upd, int fused) {
   for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n;
        i += (long long)gridDim.x * blockDim.x * 4) {
     if (i + 4 <= n && (n & 3) == 0) {
@@ -27,24 +28,46 @@ __global__ void reduce_partials_k(const float* __restrict__ ws, int splits, long
         float4 b = __ldg(reinterpret_cast<const float4*>(ws + z * n + i));
         a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
       }
-      *reinterpret_cast<float4*>(out + i) = a;
+      if (fused) {
+        sgd_apply4(upd, i, a);
+      } else {
+        *reinterpret_cast<float4*>(out + i) = a;
+      }
     } else {
       for (long long j = i; j < n && j < i + 4; ++j) {
         float a = ws[j];
         for (int z = 1; z < splits; ++z) a += ws[z * n + j];
-        out[j] = a;
+        if (fused) sgd_apply(upd, j, a);
+        else out[j] = a;
       }
     }
   }
 }
 
-int reduce_partials(const float* ws, int splits, long long n, float* out, cudaStream_t st) {
+int reduce_partials(const float* ws, int splits, long long n, float* out, cudaStream_t st, const pc_sgd_fuse* upd) {
   if (n == 0) return PC_OK;
   long long g = (n / 4 + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
   if (g < 1) g = 1;
-  reduce_partials_k<<<(int)g, 256, 0, st>>>(ws, splits, n, out);
+  pc_sgd_fuse u;
+  memset(&u, 0, sizeof(u));
+  if (upd) u = *upd;
+  reduce_partials_k<<<(int)g, 256, 0, st>>>(ws, splits, n, out, u, upd != nullptr);
   PC_CUDA_CHECK_LAUNCH("reduce_partials");
+  return PC_OK;
+}
+
+__global__ void sgd_region_k(const float* __restrict__ g, long long n, pc_sgd_fuse upd) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    sgd_apply(upd, i, g[i]);
+}
+
+// Update from a materialised gradient (paths without a fused epilogue).
+int apply_sgd(const float* g, long long n, const pc_sgd_fuse* upd, cudaStream_t st) {
+  if (n == 0) return PC_OK;
+  long long b = (n + 255) / 256;
+  sgd_region_k<<<(int)(b > 1184 ? 1184 : b), 256, 0, st>>>(g, n, *upd);
+  PC_CUDA_CHECK_LAUNCH("apply_sgd");
   return PC_OK;
 }
 
@@ -253,6 +276,12 @@ extern "C" size_t pc_conv2d_backward_workspace(const pc_conv_geom* g, int prec) 
 extern "C" int pc_conv2d_backward(const pc_conv_geom* g, const void* x, const void* w, const void* gy,
                                   void* gx, const void* mask, float* gw, float* gb, int prec, int flags,
                                   void* workspace, size_t ws_bytes, pc_stream_t st) {
+  return pc_conv2d_backward_ex(g, x, w, gy, gx, mask, gw, gb, prec, flags, workspace, ws_bytes, nullptr, st);
+}
+
+extern "C" int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const void* w, const void* gy,
+                                     void* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                                     void* workspace, size_t ws_bytes, const pc_sgd_fuse* upd, pc_stream_t st) {
   int rc = check_geom(g);
   if (rc || (rc = check_prec(prec))) return rc;
   size_t need = pc_conv2d_backward_workspace(g, prec);
@@ -277,8 +306,9 @@ extern "C" int pc_conv2d_backward(const pc_conv_geom* g, const void* x, const vo
     if (rc) return rc;
     float* part = ws + colsum_ws(P, g->N);
     if (prec == PC_BF16) {
-      rc = umma_conv_wgrad(*g, x, gy, gw, part, S(st));
+      rc = umma_conv_wgrad(*g, x, gy, gw, part, S(st), upd);
     } else {
+      PC_REQUIRE(upd == nullptr, PC_EVALUE, "fused SGD update: bf16 tensor-core path only");
       rc = simt_conv_wgrad(*g, x, gy, gw, part, simt_splits(g->N, g->k * g->k * g->C, P), S(st), prec);
     }
     if (rc) return rc;
@@ -320,6 +350,12 @@ extern "C" size_t pc_fc_backward_workspace(int B, int D, int U, int prec) {
 extern "C" int pc_fc_backward(int B, int D, int U, const pc_mat* x, const void* w, const void* gy,
                               const pc_mat* gx, const void* mask, float* gw, float* gb, int prec, int flags,
                               void* workspace, size_t ws_bytes, pc_stream_t st) {
+  return pc_fc_backward_ex(B, D, U, x, w, gy, gx, mask, gw, gb, prec, flags, workspace, ws_bytes, nullptr, st);
+}
+
+extern "C" int pc_fc_backward_ex(int B, int D, int U, const pc_mat* x, const void* w, const void* gy,
+                                 const pc_mat* gx, const void* mask, float* gw, float* gb, int prec, int flags,
+                                 void* workspace, size_t ws_bytes, const pc_sgd_fuse* upd, pc_stream_t st) {
   int rc = check_prec(prec);
   if (rc) return rc;
   PC_REQUIRE(B >= 0 && D > 0 && U > 0, PC_ESHAPE, "fc: bad extents B=%d D=%d U=%d", B, D, U);
@@ -344,7 +380,8 @@ extern "C" int pc_fc_backward(int B, int D, int U, const pc_mat* x, const void* 
     float* ws = static_cast<float*>(workspace);
     rc = colsum(gy, B, U, prec, gb, ws, S(st));
     if (rc) return rc;
-    rc = prec == PC_BF16 ? umma_fc_wgrad(B, D, U, *x, gy, gw, ws + colsum_ws(B, U), S(st))
+    PC_REQUIRE(upd == nullptr || prec == PC_BF16, PC_EVALUE, "fused SGD update: bf16 tensor-core path only");
+    rc = prec == PC_BF16 ? umma_fc_wgrad(B, D, U, *x, gy, gw, ws + colsum_ws(B, U), S(st), upd)
                          : simt_fc_wgrad(B, D, U, *x, gy, gw, S(st), prec);
     if (rc) return rc;
   }

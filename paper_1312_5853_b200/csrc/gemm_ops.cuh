@@ -98,7 +98,37 @@ struct PartialEpi {
 };
 
 // out[i] = sum_{z < splits} ws[z * n + i], ascending z (deterministic split-K).
-int reduce_partials(const float* ws, int splits, long long n, float* out, cudaStream_t st);
+int reduce_partials(const float* ws, int splits, long long n, float* out, cudaStream_t st,
+                    const pc_sgd_fuse* upd = nullptr);
+
+int apply_sgd(const float* g, long long n, const pc_sgd_fuse* upd, cudaStream_t st);
+
+// Momentum-SGD update of 4 consecutive elements (i % 4 == 0; 16-byte aligned rows).
+__device__ __forceinline__ void sgd_apply4(const pc_sgd_fuse& u, long long i, float4 g) {
+  float4 p = *reinterpret_cast<float4*>(u.p + i), v = *reinterpret_cast<float4*>(u.v + i);
+  v.x = u.momentum * v.x - u.lr * (g.x + u.weight_decay * p.x);
+  v.y = u.momentum * v.y - u.lr * (g.y + u.weight_decay * p.y);
+  v.z = u.momentum * v.z - u.lr * (g.z + u.weight_decay * p.z);
+  v.w = u.momentum * v.w - u.lr * (g.w + u.weight_decay * p.w);
+  p.x += v.x; p.y += v.y; p.z += v.z; p.w += v.w;
+  *reinterpret_cast<float4*>(u.v + i) = v;
+  *reinterpret_cast<float4*>(u.p + i) = p;
+  if (u.p_lowp) {
+    __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(u.p_lowp) + i);
+    q[0] = __floats2bfloat162_rn(p.x, p.y);
+    q[1] = __floats2bfloat162_rn(p.z, p.w);
+  }
+}
+
+// Momentum-SGD update of one element (kernels.sgd_step arithmetic).
+__device__ __forceinline__ void sgd_apply(const pc_sgd_fuse& u, long long i, float g) {
+  float p = u.p[i], v = u.v[i];
+  v = u.momentum * v - u.lr * (g + u.weight_decay * p);
+  p += v;
+  u.v[i] = v;
+  u.p[i] = p;
+  if (u.p_lowp) static_cast<__nv_bfloat16*>(u.p_lowp)[i] = __float2bfloat16_rn(p);
+}
 // Bias gradient: out[c] = sum_r g[r * N + c] (two-pass, fixed order). ws >= colsum_ws(P, N) floats.
 long long colsum_ws(long long P, int N);
 int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, cudaStream_t st);

@@ -1410,11 +1410,12 @@ static WgradPlan wgrad_plan(const pc_conv_geom& g) {
 long long umma_wgrad_splits(const pc_conv_geom& g) { return wgrad_plan(g).splits; }
 
 int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float* gw, float* part,
-                    cudaStream_t st) {
+                    cudaStream_t st, const pc_sgd_fuse* upd) {
   if (!conv_tc_shape(g)) {
     g_simt_launches++;
     long long P = (long long)g.B * g.Ho * g.Wo;
-    return simt_conv_wgrad(g, x, gy, gw, part, simt_splits(g.N, g.k * g.k * g.C, P), st, PC_BF16);
+    int rc = simt_conv_wgrad(g, x, gy, gw, part, simt_splits(g.N, g.k * g.k * g.C, P), st, PC_BF16);
+    return rc || !upd ? rc : apply_sgd(gw, (long long)g.N * g.k * g.k * g.C, upd, st);
   }
   int Kc = g.k * g.k * g.C;
   long long P = (long long)g.B * g.Ho * g.Wo;
@@ -1438,10 +1439,12 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   }
   p.out = splits > 1 ? static_cast<void*>(part) : static_cast<void*>(gw);
   p.split_stride = splits > 1 ? (long long)g.N * Kc : 0;
+
   rc = i2c ? launch_mn<A_IM2COL_MN, EPI_F32_T>(p, wp.t, splits, st)
            : launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, wp.t, splits, st);
-  if (rc || splits == 1) return rc;
-  return reduce_partials(part, splits, (long long)g.N * Kc, gw, st);
+  if (rc) return rc;
+  if (splits == 1) return upd ? apply_sgd(gw, (long long)g.N * Kc, upd, st) : PC_OK;
+  return reduce_partials(part, splits, (long long)g.N * Kc, gw, st, upd);
 }
 
 static bool tma_view_ok(const pc_mat& v, long long inner_total) {
@@ -1603,10 +1606,12 @@ static int fc_wgrad_splits(int B, int D, int U) {
   return (int)choose_splits(tiles, (B + BK - 1) / BK, bn);
 }
 
-int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* gw, float* part, cudaStream_t st) {
+int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* gw, float* part, cudaStream_t st,
+                  const pc_sgd_fuse* upd) {
   if (!(tma_view_ok(x, D) && D % 8 == 0 && U % 8 == 0)) {
     g_simt_launches++;
-    return simt_fc_wgrad(B, D, U, x, gy, gw, st, PC_BF16);
+    int rc = simt_fc_wgrad(B, D, U, x, gy, gw, st, PC_BF16);
+    return rc || !upd ? rc : apply_sgd(gw, (long long)U * D, upd, st);
   }
   Params p = base_params(U, D, B);
   int rc = make_map(&p.tma_a, gy, U, B, 1, U, 0, 64);
@@ -1621,15 +1626,18 @@ int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* g
   p.kb_per_split = ceil_div(p.num_kb, splits);
   splits = ceil_div(p.num_kb, p.kb_per_split);
   if (splits == 1 || part == nullptr) {
+    // direct epilogue (row-per-thread fp32 stores): a per-element read-modify-write
+    // of p and v there is uncoalesced, so the update runs as a pass over this layer
     p.kb_per_split = p.num_kb;
     p.out = gw;
-    return launch_mn<A_TMA_MN, EPI_F32>(p, t, 1, st);
+    rc = launch_mn<A_TMA_MN, EPI_F32>(p, t, 1, st);
+    return rc || !upd ? rc : apply_sgd(gw, (long long)U * D, upd, st);
   }
   p.out = part;
   p.split_stride = (long long)U * D;
   rc = launch_mn<A_TMA_MN, EPI_F32>(p, t, splits, st);
   if (rc) return rc;
-  return reduce_partials(part, splits, (long long)U * D, gw, st);
+  return reduce_partials(part, splits, (long long)U * D, gw, st, upd);
 }
 
 size_t umma_fc_extra_ws(int B, int D, int U, int prec) {

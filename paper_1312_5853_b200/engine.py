@@ -251,6 +251,35 @@ class ColumnEngine:
         """Point the SGD launch at a (possibly reduced, shared) gradient buffer."""
         self._sgd_host.g = g.data_ptr()
         self._sgd_dev.copy_(torch.frombuffer(bytearray(bytes(self._sgd_host)), dtype=torch.uint8))
+        self._sgd_regions = None
+
+    def configure_fused_sgd(self, on: bool):
+        """Single-replica plans (no gradient reduction between backward and update):
+        the bf16 weight-gradient kernels of conv/FC layers apply the momentum-SGD
+        update in their epilogue (pc_*_backward_ex) and never store the weight
+        gradient; one SGD launch then covers only the remaining regions (biases and
+        the masked input layer). ``grads_host`` is then valid for those regions only."""
+        self.fuse_sgd = bool(on) and self.prec == L.PC_BF16
+        self._fuse = {}
+        if not self.fuse_sgd:
+            self._sgd_regions = None
+            return
+        rest = []
+        for st in self.layers:
+            if st.w_off < 0:
+                continue
+            nw = layout.numel(st.w_shape)
+            if st.kind in ("conv", "fc") and not st.s2d and not st.col:
+                self._fuse[id(st)] = L.SgdFuse(self.p32[st.w_off:].data_ptr(), self.v32[st.w_off:].data_ptr(),
+                                               self.plow[st.w_off:].data_ptr(), self.lr, self.mom, self.wd)
+            else:
+                rest.append((st.w_off, nw))
+            rest.append((st.b_off, st.cl.bias_shape[0]))
+        tabs = [L.SgdTensor(self.p32[o:].data_ptr(), self.v32[o:].data_ptr(), self.g32[o:].data_ptr(),
+                            self.plow[o:].data_ptr(), n) for o, n in rest]
+        arr = (L.SgdTensor * len(tabs))(*tabs)
+        self._sgd_regions = (len(tabs), max(n for _, n in rest),
+                             torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.device))
 
     # ------------------------------------------------------ parameter transfer
     def _w_lowp(self, st):
@@ -431,21 +460,23 @@ class ColumnEngine:
                        self.ws_bytes, s)
         elif st.kind == "conv":
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
-            self._call(st, "pc_conv2d_backward", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
-                     st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
-                     st.inp.data_ptr() if st.mask_dx else None,
-                     self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
-                     self.ws.data_ptr(), self.ws_bytes, s)
+            upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
+            self._call(st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
+                       st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
+                       st.inp.data_ptr() if st.mask_dx else None,
+                       self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
+                       self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s)
         elif st.kind == "fc":
             d = math.prod(st.in_nhwc)
             u = st.cl.out_shape[0]
             xm = self._in_mat(st)
             gm = L.Mat(st.gin.data_ptr() if want_dx else st.inp.data_ptr(), xm.ld, xm.cb, xm.bstride)
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
-            self._call(st, "pc_fc_backward", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
-                     C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
-                     self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
-                     self.ws.data_ptr(), self.ws_bytes, s)
+            upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
+            self._call(st, "pc_fc_backward_ex", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
+                       C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
+                       self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
+                       self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s)
         elif st.kind == "relu":
             if not st.skip_bwd and want_dx:
                 self._call(st, "pc_relu_backward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),
@@ -464,6 +495,10 @@ class ColumnEngine:
             self._call(st, "pc_scale", n, st.gin.data_ptr(), st.gin.data_ptr(), 1.0 / self.m, self.prec, s)
 
     def sgd(self):
+        if getattr(self, "_sgd_regions", None) is not None:
+            n, mx, tab = self._sgd_regions
+            self.lib.call("pc_sgd_step", n, tab.data_ptr(), mx, self.lr, self.mom, self.wd, self.stream)
+            return
         self.lib.call("pc_sgd_step", 1, self._sgd_dev.data_ptr(), self.n_flat, self.lr, self.mom, self.wd,
                       self.stream)
 

@@ -266,3 +266,30 @@ def test_alexnet_input_layer_space_to_depth_bf16():
     keep = st0.keep.cpu().numpy().astype(bool)
     wdev = eng.p32[st0.w_off: st0.w_off + keep.size].cpu().numpy()
     assert np.all(wdev[~keep] == 0.0) and np.any(wdev[keep] != 0.0)
+
+
+def test_fused_sgd_epilogue_matches_separate_update():
+    """Opt-in fused momentum-SGD (single-replica plans): the weight-gradient kernels
+    update p/v in place (split-K reduction epilogue, or a per-layer pass) instead of
+    the one multi-tensor SGD launch; parameters after two steps match the unfused
+    run (same fp32 update arithmetic, up to FMA contraction)."""
+    import paper_1312_5853_b200 as P
+    net = P.load_network(CONFIGS / "alexnet_small64.net")
+    plan = P.ParallelPlan(1, 1)
+    cs = P.columnize(net, 1)
+    dense = f32_params(P.init_dense_params(net, 5))
+    tr, _ = P.gen_synthetic(100, 1, net.input_shape, seed=4)
+    x, y = tr.images[:16], tr.labels[:16]
+    out = []
+    for fuse in (False, True):
+        fab = P.spawn(1, precision="bf16")
+        fab.fuse_sgd = fuse
+        P.setup_workers(fab, plan, cs, dense, P.SgdState())
+        losses = [P.hybrid_step(fab, plan, cs, x, y).loss for _ in range(2)]
+        assert fab._engines[0].fuse_sgd == fuse
+        out.append((losses, P.gather_dense_params(fab, plan, cs)))
+    (l0, p0), (l1, p1) = out
+    assert abs(l0[1] - l1[1]) <= 1e-6 * abs(l0[1])
+    for i in p0:
+        for k in ("w", "b"):
+            assert rel(p1[i][k] - dense[i][k], p0[i][k] - dense[i][k]) < 1e-5, (i, k)
