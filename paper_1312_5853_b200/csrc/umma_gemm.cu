@@ -40,7 +40,11 @@ namespace umma {
 // cp.async gather kept for geometries the im2col box cannot express.
 enum AMode {
   A_TMA_K = 0, A_TMA_MN = 1, A_GATHER_FWD = 2, A_GATHER_DGRAD = 3, A_GATHER_WGRAD = 4,
-  A_IM2COL_K = 5, A_IM2COL_MN = 6, A_HALO_K = 7
+  A_IM2COL_K = 5, A_IM2COL_MN = 6, A_HALO_K = 7,
+  // weight gradient with M <= 640 and N <= 128 (the input layer: 9 taps x 64
+  // channels x 96 filters): one CTA holds MACC = 5 accumulators (all of M) x N in
+  // TMEM, so each split-K slice streams the upstream gradient (B) exactly once
+  A_IM2COL_MN5 = 8
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2 };
@@ -82,6 +86,8 @@ struct alignas(64) Params {
   // tiles at full rate; odd row shifts work but run ~3x slower, tools/desc_probe.cu).
   // Columns x >= Wo are discarded.
   int halo_R, halo_tpi, halo_Wv, halo_lo, halo_bytes;
+  int macc_chunks;  // A_IM2COL_MN5: 64-row A chunks with real rows (<= 10)
+  int mt_rows;      // rows per M tile: 128 * CTA-group size * accumulators (set at launch)
   unsigned long long* trace;  // debug: per-CTA per-tile clock64 stamps (tools/trace_gemm.py), normally null
 };
 
@@ -308,15 +314,18 @@ template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM
 // 1024 / GATHER_THREADS rows of the 128 x 64 stage.
 constexpr int GATHER_THREADS = 512;
 constexpr int GR = 1024 / GATHER_THREADS;  // rows (fwd/dgrad) or pixel rows (wgrad) per gather thread
-template <int AM> constexpr bool a_is_mn() { return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN; }
+template <int AM> constexpr bool a_is_mn() {
+  return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN || AM == A_IM2COL_MN5;
+}
+template <int AM> constexpr int macc_of() { return AM == A_IM2COL_MN5 ? 5 : 1; }
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
 template <int BN, int CG>
 constexpr int halo_stage_bytes() { return HALO_SLOT_BYTES + HALO_KMAX * (BN / CG) * BK * 2; }
-template <int BN, int STAGES, int CG, bool HALO = false>
+template <int BN, int STAGES, int CG, bool HALO = false, int MACC = 1>
 constexpr int smem_bytes() {
   return 1024 /*align slack*/ + (HALO ? STAGES * halo_stage_bytes<BN, CG>()
-                                      : STAGES * (A_STAGE_BYTES + (BN / CG) * BK * 2)) +
+                                      : STAGES * (MACC * A_STAGE_BYTES + (BN / CG) * BK * 2)) +
          (2 * STAGES + 4) * 8 + 16;
 }
 
@@ -340,7 +349,7 @@ struct TileCoord {
 
 template <int CG>
 __device__ __forceinline__ TileCoord tile_coord(const Params& p, int t, int bn) {
-  const int bmt = BM * CG;
+  const int bmt = p.mt_rows;
   const int tn = (p.N + bn - 1) / bn, tm = (p.M + bmt - 1) / bmt;
   TileCoord c;
   c.z = t / (tm * tn);
@@ -359,11 +368,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Epilogue: drain one accumulator (this CTA's 128 rows x BN fp32 in TMEM) per
 // tile. EPW warps per TMEM lane quadrant split the 16-column chunks. Output
 // addressing keeps (channel block, offset) incrementally — no divisions.
-template <int EPI, int BN, int CG, int EPW, bool HALO>
+template <int EPI, int BN, int CG, int EPW, bool HALO, int MACC = 1>
 __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty, int unit,
                                          int units, uint32_t rank, int quad, int grp, int lane) {
-  constexpr int TCOLS = tmem_cols<BN>();
-  constexpr int ACC = acc_count<BN>();
+  constexpr int TCOLS = MACC > 1 ? 512 : tmem_cols<BN>();
+  constexpr int ACC = MACC > 1 ? 1 : acc_count<BN>();
   const int row = quad * 32 + lane;
   int lt = 0;
   for (int t = unit; t < p.tiles; t += units, ++lt) {
@@ -372,7 +381,8 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
     mbar_wait(&tfull[acc], (lt / ACC) & 1);
     tc_fence_after();
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
-    long long m = (long long)tc.m0 + (long long)rank * BM + row;
+    for (int a = 0; a < MACC; ++a) {  // MACC > 1: accumulator a = rows [128 a, 128 a + 128), TMEM column a * N
+    long long m = (long long)tc.m0 + (long long)rank * BM + a * BM + row;
     bool mrow = m < p.M;
     if constexpr (HALO) {  // TMEM row -> (image, output row, column) of this CTA's halo tile
       const int tile = (tc.m0 + (int)rank * BM) / BM;
@@ -381,7 +391,7 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
       mrow = mrow && yy < p.halo_R && y < p.i2c_Ho && xx < p.i2c_Wo;
       m = ((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx;
     }
-    const uint32_t tbase = tmem + acc * TCOLS + ((uint32_t)(quad * 32) << 16);
+    const uint32_t tbase = tmem + acc * TCOLS + (MACC > 1 ? a * p.N : 0) + ((uint32_t)(quad * 32) << 16);
     const long long rowoff = m * p.o_ld;
     // (blk, rem) of output column n = n0 + c0 in a channel-blocked view (o_cb % 8 == 0)
     long long n = (long long)tc.n0 + grp * 16;
@@ -451,6 +461,7 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
         while (rem >= p.o_cb) { rem -= p.o_cb; ++blk; }
       }
     }
+    }  // accumulators
     // accumulator drained: let the (leader's) MMA warp reuse it
     tc_fence_before();
     __syncwarp();
@@ -477,21 +488,25 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   constexpr int BNC = BN / CG;  // B rows (N) this CTA loads
   static_assert(!B_MN || BNC % 64 == 0, "MN-major B is loaded in 64-column chunks");
   constexpr int B_STAGE_BYTES = BNC * BK * 2;
-  constexpr uint32_t IDESC = make_idesc<BN, A_MN, B_MN, CG>();
-  constexpr int TCOLS = tmem_cols<BN>();
-  constexpr int ACC = acc_count<BN>();
+  constexpr int MACC = macc_of<AM>();
+  // MACC > 1: MMA N = p.N (<= BN, the B load width), accumulator a at TMEM column a * p.N
+  const uint32_t IDESC = MACC > 1 ? ((make_idesc<BN, A_MN, B_MN, CG>() & ~(0x3Fu << 17)) | ((uint32_t)(p.N >> 3) << 17))
+                                  : make_idesc<BN, A_MN, B_MN, CG>();
+  constexpr int TCOLS = MACC > 1 ? 512 : tmem_cols<BN>();
+  constexpr int ACC = MACC > 1 ? 1 : acc_count<BN>();
+  constexpr int A_STAGE = MACC * A_STAGE_BYTES;  // this kernel's A bytes per stage (allocated)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr bool HALO = AM == A_HALO_K;
   // stage s: A at sA + s * A_STRIDE, B at sB + s * B_STRIDE (a halo stage holds its
   // window and its k B tiles contiguously)
-  constexpr int A_STRIDE = HALO ? halo_stage_bytes<BN, CG>() : A_STAGE_BYTES;
+  constexpr int A_STRIDE = HALO ? halo_stage_bytes<BN, CG>() : A_STAGE;
   constexpr int B_STRIDE = HALO ? halo_stage_bytes<BN, CG>() : B_STAGE_BYTES;
   uint8_t* sA = smem;
-  uint8_t* sB = HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE_BYTES;
+  uint8_t* sB = HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (HALO ? halo_stage_bytes<BN, CG>()
-                                                                       : A_STAGE_BYTES + B_STAGE_BYTES));
+                                                                       : A_STAGE + B_STAGE_BYTES));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [ACC]
   uint64_t* tempty = tfull + 2;      // [ACC]
@@ -556,7 +571,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       // A_IM2COL_K: tile's first output pixel (fixed) and the K position (c, i, j) of kb
       int t_b = 0, t_oy = 0, t_ox = 0, kc = 0, ki = 0, kj = 0, kblk = 0, kcoff = 0, ktap = 0;
       // A_IM2COL_MN: per-chunk (i, j, blk, coff) of the tile's M rows (fixed) and kb's pixel (b, oy, ox)
-      int ci[BM / 64], cj[BM / 64], cblk[BM / 64], ccoff[BM / 64];
+      constexpr int ACH = MACC * BM / 64;  // A chunks per stage
+      int ci[ACH], cj[ACH], cblk[ACH], ccoff[ACH];
       int pb = 0, poy = 0, pox = 0;
       // A_HALO_K: this CTA's tile (image hb, first output row hy0); K walks chunk-major
       int hb = 0, hy0 = 0;
@@ -578,9 +594,9 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         kj = ktap - ki * p.i2c_k;
         kblk = kc / p.i2c_cs;
         kcoff = kc - kblk * p.i2c_cs;
-      } else if constexpr (AM == A_IM2COL_MN) {
+      } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5) {
 #pragma unroll
-        for (int cch = 0; cch < BM / 64; ++cch) {
+        for (int cch = 0; cch < ACH; ++cch) {
           int kk = m0 + 64 * cch;
           if (kk >= p.M) kk = 0;  // rows past M are discarded by the epilogue
           const int c = kk % p.i2c_C, ij = kk / p.i2c_C;
@@ -611,7 +627,9 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             tma_load_3d<CG>(&p.tma_b, &full[s], st0 + HALO_SLOT_BYTES + i * B_STAGE_BYTES,
                             (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
         } else if (!HALO && elect_one()) {
-          if (leader) mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + (GATHER ? 0 : A_STAGE_BYTES)));
+          if (leader)
+            mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + (GATHER ? 0 : MACC > 1 ? p.macc_chunks * 64 * BK * 2
+                                                                                       : A_STAGE_BYTES)));
           const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
           if constexpr (B_MN) {
             if (p.b_chunked) {  // one op: {64 cols, BK rows, BNC/64 chunks} of the chunked view
@@ -633,11 +651,12 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             tma_im2col_5d<CG>(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
                               t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
                               (uint16_t)ki);
-          } else if constexpr (AM == A_IM2COL_MN) {
-            // K block = 64 consecutive pixels; M = (i, j, c): two 64-channel chunks
+          } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5) {
+            // K block = 64 consecutive pixels; M = (i, j, c): 64-channel chunks
 #pragma unroll
-            for (int cch = 0; cch < BM / 64; ++cch)
-              tma_im2col_5d<CG>(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES) + cch * (64 * BK * 2),
+            for (int cch = 0; cch < ACH; ++cch)
+              if (MACC == 1 || cch < p.macc_chunks)
+              tma_im2col_5d<CG>(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE) + cch * (64 * BK * 2),
                                 ccoff[cch], pox * p.i2c_s + p.i2c_lw, poy * p.i2c_s + p.i2c_lh, pb, cblk[cch],
                                 (uint16_t)cj[cch], (uint16_t)ci[cch]);
           } else if constexpr (!GATHER) {
@@ -668,7 +687,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           }
         } else if constexpr (HALO) {
           if (++kj == p.i2c_k) { kj = 0; kc += BK; }
-        } else if constexpr (AM == A_IM2COL_MN) {
+        } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5) {
           pox += BK;
           while (pox >= p.i2c_Wo) {
             pox -= p.i2c_Wo;
@@ -870,6 +889,15 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
                   if (kk < nk16)
                     tc_mma<CG>(tacc, ai + kk * A_KSTEP, bi + kk * B_KSTEP, IDESC, (it > 0 || i > 0 || kk > 0) ? 1u : 0u);
               }
+            } else if constexpr (MACC > 1) {
+              // accumulator a: A rows [128 a, 128 a + 128) of the stage (two 64-row chunks)
+              for (int a = 0; a < MACC; ++a) {
+                if (2 * a >= p.macc_chunks) break;
+                const uint64_t aa = ad + (uint64_t)((a * A_STAGE_BYTES) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  tc_mma<CG>(tacc + a * p.N, aa + kk * A_KSTEP, bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+              }
             } else {
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk)
@@ -898,7 +926,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       }
     }
   } else {
-    epilogue<EPI, BN, CG, EPW, HALO>(p, tmem, tfull, tempty, unit, units, rank, warp & 3, warp >= 6 ? 1 : 0, lane);
+    epilogue<EPI, BN, CG, EPW, HALO, MACC>(p, tmem, tfull, tempty, unit, units, rank, warp & 3, warp >= 6 ? 1 : 0,
+                                           lane);
   }
 
   tc_fence_before();
@@ -1003,7 +1032,7 @@ static unsigned long long* g_trace = nullptr;  // pc_debug_trace_gemm
 template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
 static int launch(const Params& p, int splits, cudaStream_t st) {
   auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES, CG>;
-  constexpr int smem = smem_bytes<BN, STAGES, CG, AM == A_HALO_K>();
+  constexpr int smem = smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>()>();
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   constexpr int threads = kernel_threads<AM>();
   static int resident = 0;  // persistent CTAs the device holds at once
@@ -1027,7 +1056,7 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (CG == 1) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-      const int tmem_cap = 512 / (tmem_cols<BN>() * acc_count<BN>());
+      const int tmem_cap = macc_of<AM>() > 1 ? 1 : 512 / (tmem_cols<BN>() * acc_count<BN>());
       per_sm = std::max(1, std::min(per_sm, tmem_cap));
       resident = sms * per_sm;
     } else {
@@ -1042,7 +1071,8 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
   }
   Params q = p;
   q.trace = g_trace;
-  q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, BM * CG) * splits;
+  q.mt_rows = BM * CG * macc_of<AM>();
+  q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, q.mt_rows) * splits;
   const int units = std::min(q.tiles, resident / CG);
   cfg.gridDim = dim3(units * CG);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, q);
@@ -1407,7 +1437,27 @@ static WgradPlan wgrad_plan(const pc_conv_geom& g) {
   return {t, (int)((kbs + per - 1) / per)};
 }
 
-long long umma_wgrad_splits(const pc_conv_geom& g) { return wgrad_plan(g).splits; }
+static bool macc_wgrad_ok(const pc_conv_geom& g);
+static int macc_splits(const pc_conv_geom& g);
+long long umma_wgrad_splits(const pc_conv_geom& g) {
+  return macc_wgrad_ok(g) ? macc_splits(g) : wgrad_plan(g).splits;
+}
+
+// Multi-accumulator weight gradient (A_IM2COL_MN5): M = k*k*C in (256, 640], N <= 128.
+static bool macc_wgrad_ok(const pc_conv_geom& g) {
+  static const int on = [] {
+    const char* e = getenv("PC_MACC");
+    return e ? atoi(e) : 1;
+  }();
+  const int Kc = g.k * g.k * g.C;
+  return on && Kc > 2 * BM && Kc <= 5 * BM && g.N <= 128 && g.N % 16 == 0 && im2col_ok(g.cs, g.C, g.cstride);
+}
+static int macc_splits(const pc_conv_geom& g) {
+  const long long kbs = ((long long)g.B * g.Ho * g.Wo + BK - 1) / BK;
+  long long sp = std::min<long long>(148, std::max<long long>(1, kbs / 16));
+  const long long per = (kbs + sp - 1) / sp;
+  return (int)((kbs + per - 1) / per);
+}
 
 int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float* gw, float* part,
                     cudaStream_t st, const pc_sgd_fuse* upd) {
@@ -1420,6 +1470,29 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   int Kc = g.k * g.k * g.C;
   long long P = (long long)g.B * g.Ho * g.Wo;
   Params p = base_params(Kc, g.N, (int)P);
+  if (macc_wgrad_ok(g)) {
+    int splits = macc_splits(g);
+    p.kb_per_split = ceil_div(p.num_kb, splits);
+    splits = ceil_div(p.num_kb, p.kb_per_split);
+    const Tile t{128, 1};
+    int rc = setup_mn_b(p, gy, g.N, P, 1, g.N, 0, t);
+    if (rc) return rc;
+    p.b_cb = 0;
+    p.gsrc = static_cast<const __nv_bfloat16*>(x);
+    p.g = g;
+    p.o_ld = Kc;
+    rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, 64, -g.pad, -g.pad,
+                         g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
+    if (rc) return rc;
+    set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
+    p.macc_chunks = (Kc + 63) / 64;
+    p.out = splits > 1 ? static_cast<void*>(part) : static_cast<void*>(gw);
+    p.split_stride = splits > 1 ? (long long)g.N * Kc : 0;
+    rc = launch<A_IM2COL_MN5, B_TMA_MN, EPI_F32_T, 128, 2, 1>(p, splits, st);
+    if (rc) return rc;
+    if (splits == 1) return upd ? apply_sgd(gw, (long long)g.N * Kc, upd, st) : PC_OK;
+    return reduce_partials(part, splits, (long long)g.N * Kc, gw, st, upd);
+  }
   const WgradPlan wp = wgrad_plan(g);
   int splits = wp.splits;
   p.kb_per_split = ceil_div(p.num_kb, splits);
