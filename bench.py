@@ -295,23 +295,28 @@ def main():
         return
 
     burst, sustained, hbm, peak_src = measured_peaks()
-    contr = {k: v for k, v in t_by.items() if k[3] in ("pc_conv2d_forward", "pc_conv2d_backward",
-                                                      "pc_fc_forward", "pc_fc_backward")}
+    # contractions, timed per pass (the profiling step issues data and weight gradients separately)
+    contr = {k: v for k, v in t_by.items() if k[3].startswith(("pc_conv2d_", "pc_fc_"))}
     top = max(contr.items(), key=lambda kv: kv[1]) if contr else None
     roof = None
     if top is not None:
         (wid, idx, kind, name), tms = top
         cl = next(c for c in cs.col_layers if c.index == idx)
         fl = layer_flops(cl, gbatch // plan.data_shards)
-        passes = 1 if name.endswith("forward") else 2       # backward call = dgrad + wgrad
-        if name == "pc_conv2d_backward" and idx == cs.col_layers[0].index:
+        passes = 1 if (name.endswith("]") or "forward" in name) else 2   # untagged backward = dgrad + wgrad
+        if "backward" in name and not name.endswith("]") and idx == cs.col_layers[0].index:
             passes = 1                                      # layer 0: no data gradient
         achieved = fl * passes / (tms * 1e-3) / 1e12
+        traffic = None
+        tf = ROOT / "profiles" / "r01_roofline_traffic.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get(f"{name} layer {idx}")
         roof = {"bound": "tensor", "kernel": f"{name} layer {idx}", "achieved": achieved,
-                "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained, "traffic": None,
+                "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained, "traffic": traffic,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
                 "share_of_step": tms / step_prof_ms if step_prof_ms else None,
-                "algorithmic_flop_per_launch": fl * passes}
+                "algorithmic_flop_per_launch": fl * passes,
+                "traffic_source": "profiles/r01_roofline_traffic.json (ncu --set full dram bytes)" if traffic else None}
     shard = gbatch // plan.data_shards
     # reference convention (netdef.shape_report) minus layer 0's data gradient, which is never needed
     step_flops = plan.workers * (P.shape_report(cs, shard).total_flops - layer_flops(cs.col_layers[0], shard))

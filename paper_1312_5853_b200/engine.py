@@ -378,7 +378,7 @@ class ColumnEngine:
     def stream(self):
         return torch.cuda.current_stream(self.device).cuda_stream
 
-    def _call(self, st, name: str, *args):
+    def _call(self, st, name: str, *args, tag: str = ""):
         """C-ABI call of one layer pass; with ``PROFILE`` set, bracketed by CUDA
         events on the launching stream (bench.py's per-kernel roofline)."""
         if PROFILE is None:
@@ -387,7 +387,15 @@ class ColumnEngine:
         a.record()
         self.lib.call(name, *args)
         b.record()
-        PROFILE.append((self.wid, st.cl.index, st.kind, name, a, b))
+        PROFILE.append((self.wid, st.cl.index, st.kind, name + tag, a, b))
+
+    def _split_backward(self, st, name: str, flags: int, call):
+        """Under ``PROFILE``, issue a backward pass as its data-gradient and its
+        weight-gradient halves (separately timed); otherwise one call."""
+        if PROFILE is None or not (flags & L.PC_WANT_DX) or not (flags & L.PC_WANT_DW):
+            return call(flags, "")
+        call(flags & ~L.PC_WANT_DW, "[dx]")
+        call(flags & ~(L.PC_WANT_DX | L.PC_MASK_DX), "[dw]")
 
     def load_batch(self, x_nchw: torch.Tensor, labels_i32: torch.Tensor):
         """x_nchw: device (B, C, H, W) slice of the global batch: float32, or bf16
@@ -461,11 +469,12 @@ class ColumnEngine:
         elif st.kind == "conv":
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
-            self._call(st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
-                       st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
-                       st.inp.data_ptr() if st.mask_dx else None,
-                       self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
-                       self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s)
+            self._split_backward(st, "pc_conv2d_backward_ex", flags, lambda f, tag: self._call(
+                st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
+                st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
+                st.inp.data_ptr() if st.mask_dx else None,
+                self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, f,
+                self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s, tag=tag))
         elif st.kind == "fc":
             d = math.prod(st.in_nhwc)
             u = st.cl.out_shape[0]
@@ -473,10 +482,11 @@ class ColumnEngine:
             gm = L.Mat(st.gin.data_ptr() if want_dx else st.inp.data_ptr(), xm.ld, xm.cb, xm.bstride)
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
-            self._call(st, "pc_fc_backward_ex", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
-                       C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
-                       self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, flags,
-                       self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s)
+            self._split_backward(st, "pc_fc_backward_ex", flags, lambda f, tag: self._call(
+                st, "pc_fc_backward_ex", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
+                C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
+                self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, f,
+                self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s, tag=tag))
         elif st.kind == "relu":
             if not st.skip_bwd and want_dx:
                 self._call(st, "pc_relu_backward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),
