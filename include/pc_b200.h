@@ -173,6 +173,27 @@ typedef struct {
 PC_API int pc_sgd_step(int n_tensors, const pc_sgd_tensor* table, long long max_numel, float lr,
                 float momentum, float weight_decay, pc_stream_t stream);
 
+/* --- extensions beyond the reference (the reference has no such
+ * layers, netdef.py:219-220): definitions in oracle/ref_kernels.py ----------- */
+/* Local response normalisation across the C channels of each of P NHWC pixels:
+ * y = x * (k + alpha * sum_{|c'-c| <= size/2} x_c'^2)^-beta (lrn_forward). */
+PC_API int pc_lrn_forward(long long P, int C, int size, float k, float alpha, float beta, const void* x, void* y,
+                          int prec, pc_stream_t stream);
+/* gx from x and gy (lrn_backward; the scale is recomputed from x). */
+PC_API int pc_lrn_backward(long long P, int C, int size, float k, float alpha, float beta, const void* x,
+                           const void* gy, void* gx, int prec, pc_stream_t stream);
+/* Dropout on an NHWC slice [B][H][W][C] of a dense NCHW activation with C_dense
+ * channels (slice channels c_off.., global rows row0..): y = x / (1 - p) where
+ * kept, else 0. Element i of the dense activation is kept iff
+ * (mix64(state + (i+1)*GOLDEN) >> 11) >= thresh, state = rng.dropout_state(seed,
+ * *step, layer), thresh = rng.dropout_threshold(p); *step is a DEVICE counter.
+ * The same call computes the backward (x = gy, y = gx). */
+PC_API int pc_dropout(int B, int H, int W, int C, int C_dense, int c_off, long long row0, unsigned long long seed,
+                      const unsigned long long* step, int layer, unsigned long long thresh, float p, const void* x,
+                      void* y, int prec, pc_stream_t stream);
+/* *counter += delta (device; advances the dropout step inside a CUDA graph). */
+PC_API int pc_counter_add(unsigned long long* counter, long long delta, pc_stream_t stream);
+
 /* --- layout / reduction helpers used by the engine -------------------------- */
 /* Explicit im2col of the NCHW network input (float32 or bf16 in, bf16 out):
  * col[(b*Ho + oy)*Wo + ox][(c*k + i)*k + j] = x[b][c][oy*s+i-p][ox*s+j-p] (0 outside),

@@ -22,7 +22,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from paper_1312_5853_b200.netdef import FC, Conv, MaxPool, ReLU, SoftmaxXent, columnize
+from paper_1312_5853_b200.netdef import FC, LRN, Conv, Dropout, MaxPool, ReLU, SoftmaxXent, columnize
+from paper_1312_5853_b200 import rng
 from paper_1312_5853_b200.plan import (
     params_as_lists,
     lists_as_params,
@@ -34,8 +35,47 @@ from paper_1312_5853_b200.plan import (
 from . import ref_kernels as K
 
 
-def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argmax=None):
+def dropout_index(cs, cl, batch_rows, row0, column):
+    """Dense-activation element indices (NCHW flatten, global batch row-major) of
+    column ``column``'s slice of dropout layer ``cl``'s input for global sample
+    rows row0 .. row0 + batch_rows - 1 (the mask contract of rng.dropout_state)."""
+    m = cs.columns
+    split = column_split_before(cs, cl.index)
+    shape = cl.in_shape
+    per = int(np.prod(shape))
+    cols = m if split else 1
+    dense = per * cols
+    j = column if split else 0
+    rows = (row0 + np.arange(batch_rows, dtype=np.int64)).reshape(-1, *([1] * len(shape)))
+    if len(shape) == 3:
+        c, h, w = shape
+        cc = (j * c + np.arange(c)).reshape(c, 1, 1)
+        f = (cc * h + np.arange(h).reshape(1, h, 1)) * w + np.arange(w).reshape(1, 1, w)
+    else:
+        f = j * shape[0] + np.arange(shape[0])
+    return rows * dense + f
+
+
+def column_split_before(cs, index):
+    """True when the activation entering layer ``index`` is split across columns
+    (a non-shared conv/fc upstream, no cross point since), False when replicated."""
+    rep = True
+    for cl in cs.col_layers:
+        if cl.index == index:
+            return cs.columns > 1 and not rep
+        if cl.cross:
+            rep = True
+        if isinstance(cl.layer, (Conv, FC)):
+            rep = cl.shared
+    raise ValueError(index)
+
+
+def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argmax=None, dropout=None):
     """All m columns of one replica; returns (per-column losses, per-column grads).
+
+    ``dropout`` = (seed, step, row0): the training step's dropout stream and the
+    replica's first global sample row (rng.dropout_state); None: no dropout
+    layers may be present.
 
     ``force_argmax`` ({layer: [per-column argmax]}) replays another engine's
     max-pool decisions ("teacher forcing"): where a window holds a near-tie
@@ -61,6 +101,13 @@ def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argm
                 o = K.fc_forward(cache[j]["flat"], p["w"], p["b"])
             elif isinstance(L, ReLU):
                 o = K.relu_forward(a)
+            elif isinstance(L, LRN):
+                o = K.lrn_forward(a, L.size, L.k, L.alpha, L.beta)
+            elif isinstance(L, Dropout):
+                seed, step, row0 = dropout
+                idx = dropout_index(cs, cl, a.shape[0], row0, j)
+                cache[j]["keep"] = rng.dropout_keep(seed, step, cl.index, idx, L.p)
+                o = K.dropout_forward(a, cache[j]["keep"], L.p)
             elif isinstance(L, MaxPool):
                 o, cache[j]["arg"] = K.maxpool_forward(a, L.kernel, L.stride)
                 if force_argmax is not None and cl.index in force_argmax:
@@ -95,6 +142,10 @@ def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argm
                 gi = gi.reshape(c["in"].shape)
             elif isinstance(L, ReLU):
                 gi = K.relu_backward(c["in"], g[j])
+            elif isinstance(L, LRN):
+                gi = K.lrn_backward(c["in"], g[j], L.size, L.k, L.alpha, L.beta)
+            elif isinstance(L, Dropout):
+                gi = K.dropout_backward(g[j], c["keep"], L.p)
             else:
                 gi = K.maxpool_backward(c["in"].shape, L.kernel, L.stride, g[j], c["arg"])
             gin.append(gi)
@@ -116,11 +167,12 @@ def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argm
     return losses, grads
 
 
-def reference_step(net, params, batch, velocity=None, lr=0.01, momentum=0.9, weight_decay=0.0005):
+def reference_step(net, params, batch, velocity=None, lr=0.01, momentum=0.9, weight_decay=0.0005,
+                   dropout_seed=0, step=0):
     """Dense single-worker step; returns (loss, new_params, new_velocity)."""
     cs = columnize(net, 1)
     x, y = batch
-    losses, grads = column_fwd_bwd(cs, [params], x, y, 1.0 / x.shape[0])
+    losses, grads = column_fwd_bwd(cs, [params], x, y, 1.0 / x.shape[0], dropout=(dropout_seed, step, 0))
     plist = params_as_lists(params, cs)
     vlist = velocity if velocity is not None else [np.zeros_like(p) for p in plist]
     newp, newv = K.sgd_step(plist, params_as_lists(grads[0], cs), vlist, lr, momentum, weight_decay)
@@ -139,6 +191,7 @@ class OracleFabric:
         self.velocity = [[np.zeros_like(p) for p in params_as_lists(self.params[j], self.cs)]
                          for j in range(m)]
         self.hyper = (lr, momentum, weight_decay)
+        self.dropout_seed, self.steps = 0, 0   # dropout stream (rng.dropout_state): seed, step counter
 
     def step(self, x, y, trace=None, force_argmax=None):
         """force_argmax: {layer: [replica][column] argmax arrays} (see column_fwd_bwd)."""
@@ -154,7 +207,8 @@ class OracleFabric:
             lo, hi = r * shard, (r + 1) * shard
             fa = None if force_argmax is None else {k: v[r] for k, v in force_argmax.items()}
             losses, grads = column_fwd_bwd(self.cs, self.params, x[lo:hi], labels[lo:hi], scale,
-                                           trace=trace if r == 0 else None, force_argmax=fa)
+                                           trace=trace if r == 0 else None, force_argmax=fa,
+                                           dropout=(self.dropout_seed, self.steps, lo))
             per_replica.append(grads)
             total += losses[0]
         for j in range(m):
@@ -169,6 +223,7 @@ class OracleFabric:
                                     self.velocity[j], *self.hyper)
             self.params[j] = lists_as_params(newp, self.cs)
             self.velocity[j] = newv
+        self.steps += 1
         return total
 
     def dense_params(self):

@@ -131,3 +131,49 @@ def sgd_step(params, grads, velocity, lr=0.01, momentum=0.9, weight_decay=0.0005
     """`kernels.py:319-341`: v <- mu v - lr (g + wd p); p <- p + v."""
     new_v = [momentum * v - lr * (g + weight_decay * p) for p, g, v in zip(params, grads, velocity)]
     return [p + v for p, v in zip(params, new_v)], new_v
+
+
+# --- extensions beyond the reference (SURVEY §8 f1): the reference has no LRN or
+# dropout (`netdef.py:219-220`, SPEC.md:129). These float64 definitions ARE the
+# specification the device kernels are checked against ("parity unpinned" with
+# respect to the reference itself; pinned by finite differences in tests/).
+
+def _lrn_scale(x, size, k, alpha):
+    """S[b,c] = k + alpha * sum_{|c'-c| <= size//2} x[b,c']^2 (channels clipped at the edges)."""
+    h = size // 2
+    sq = np.asarray(x, np.float64) ** 2
+    c = x.shape[1]
+    csum = np.concatenate([np.zeros_like(sq[:, :1]), np.cumsum(sq, axis=1)], axis=1)
+    lo = np.clip(np.arange(c) - h, 0, c)
+    hi = np.clip(np.arange(c) + h + 1, 0, c)
+    win = np.take(csum, hi, axis=1) - np.take(csum, lo, axis=1)
+    return k + alpha * win
+
+
+def lrn_forward(x, size=5, k=2.0, alpha=1e-4, beta=0.75):
+    """Krizhevsky local response normalisation across channels (NCHW)."""
+    x = np.asarray(x, np.float64)
+    return x * _lrn_scale(x, size, k, alpha) ** (-beta)
+
+
+def lrn_backward(x, grad_out, size=5, k=2.0, alpha=1e-4, beta=0.75):
+    """gx_c = g_c S_c^-b - 2 a b x_c sum_{c': |c-c'| <= size//2} g_c' x_c' S_c'^(-b-1)."""
+    x = np.asarray(x, np.float64)
+    g = np.asarray(grad_out, np.float64)
+    s = _lrn_scale(x, size, k, alpha)
+    t = g * x * s ** (-beta - 1.0)
+    h = size // 2
+    c = x.shape[1]
+    tsum = np.concatenate([np.zeros_like(t[:, :1]), np.cumsum(t, axis=1)], axis=1)
+    lo = np.clip(np.arange(c) - h, 0, c)
+    hi = np.clip(np.arange(c) + h + 1, 0, c)
+    win = np.take(tsum, hi, axis=1) - np.take(tsum, lo, axis=1)
+    return g * s ** (-beta) - 2.0 * alpha * beta * x * win
+
+
+def dropout_forward(x, keep, p):
+    return np.asarray(x, np.float64) * keep / (1.0 - p)
+
+
+def dropout_backward(grad_out, keep, p):
+    return np.asarray(grad_out, np.float64) * keep / (1.0 - p)

@@ -68,6 +68,10 @@ SIGNATURES = {
     "pc_sgd_step": (_i, [_i, _vp, _ll, _f, _f, _f, _vp]),
     "pc_space_to_depth": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "pc_mask_f32": (_i, [_ll, _vp, _vp, _vp]),
+    "pc_lrn_forward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _i, _vp]),
+    "pc_lrn_backward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _vp, _i, _vp]),
+    "pc_dropout": (_i, [_i, _i, _i, _i, _i, _i, _ll, C.c_ulonglong, _vp, _i, C.c_ulonglong, _f, _vp, _vp, _i, _vp]),
+    "pc_counter_add": (_i, [_vp, _ll, _vp]),
     "pc_nchw_to_nhwc": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i, _vp]),
     "pc_im2col": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "pc_sum_buffers": (_i, [_i, _ll, _vp, _vp, _i, _vp]),

@@ -31,7 +31,8 @@ import torch
 from . import _lib as L
 from . import layout
 from .errors import ValidationError
-from .netdef import FC, ColumnizedSpec, Conv, MaxPool, ReLU, SoftmaxXent
+from . import rng
+from .netdef import FC, LRN, ColumnizedSpec, Conv, Dropout, MaxPool, ReLU, SoftmaxXent
 
 ALIGN = 32  # elements; every flat-buffer slice starts 128-byte aligned in fp32
 PROFILE: list | None = None  # set to a list to record per-call CUDA events
@@ -67,6 +68,7 @@ class LayerState:
     row_loss: torch.Tensor | None = None
     col: int = 0                         # explicit-im2col input conv: padded K (0 = implicit GEMM)
     s2d: int = 0                         # space-to-depth input conv: block size (= reference stride)
+    drop: tuple = ()                     # dropout: (H, W, C, C_dense, c_off, threshold) of this column's slice
     keep: torch.Tensor | None = None     # s2d: uint8 mask of real filter taps in the device weights
 
 
@@ -86,6 +88,11 @@ class ColumnEngine:
         self._build_params()
         self._build_grads()
         self.labels = torch.zeros(max(shard, 1), dtype=torch.int32, device=device)
+        # dropout stream (rng.dropout_state): seed, device step counter (advanced in the step program)
+        self.dropout_seed = 0
+        self.training = True
+        self.step_ctr = torch.zeros(1, dtype=torch.int64, device=device)
+        self.has_dropout = any(st.kind == "dropout" for st in self.layers)
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=device)
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
 
@@ -126,7 +133,8 @@ class ColumnEngine:
         n = len(cs.col_layers)
         for i, cl in enumerate(cs.col_layers):
             layer = cl.layer
-            kind = {Conv: "conv", FC: "fc", ReLU: "relu", MaxPool: "pool", SoftmaxXent: "softmax"}[type(layer)]
+            kind = {Conv: "conv", FC: "fc", ReLU: "relu", MaxPool: "pool", SoftmaxXent: "softmax", LRN: "lrn",
+                    Dropout: "dropout"}[type(layer)]
             st = LayerState(cl, kind)
             per = math.prod(prev_shape)
             if cl.cross:
@@ -160,6 +168,14 @@ class ColumnEngine:
                 st.out_nhwc = (cl.out_shape[0],)
                 st.out = self._new(B * cl.out_shape[0])
                 st.perm = layout.fc_row_perm(cl.in_shape, m, cl.cross)
+            elif kind in ("lrn", "dropout"):
+                st.out_nhwc = st.in_nhwc
+                st.out = self._new(B * per)
+                if kind == "dropout":
+                    hh, ww, cc = st.in_nhwc if len(st.in_nhwc) == 3 else (1, 1, st.in_nhwc[0])
+                    split = self._split_before(i)
+                    st.drop = (hh, ww, cc, cc * (m if split else 1), cc * self.column if split else 0,
+                               rng.dropout_threshold(layer.p))
             elif kind == "relu":
                 prev = self.layers[-1] if self.layers else None
                 st.out_nhwc = st.in_nhwc
@@ -201,6 +217,18 @@ class ColumnEngine:
         for i in range(1, n):
             st, prv = self.layers[i], self.layers[i - 1]
             st.mask_dx = st.kind in ("conv", "fc", "pool") and prv.kind == "relu" and prv.skip_bwd
+
+    def _split_before(self, i: int) -> bool:
+        """Is the activation entering layer position i split across columns?"""
+        rep = True
+        for cl in self.cs.col_layers[:i]:
+            if cl.cross:
+                rep = True
+            if isinstance(cl.layer, (Conv, FC)):
+                rep = cl.shared
+        if self.cs.col_layers[i].cross:
+            rep = True
+        return self.m > 1 and not rep
 
     def _build_params(self):
         off = 0
@@ -440,6 +468,16 @@ class ColumnEngine:
             if not st.relu_fused_fwd:
                 self._call(st, "pc_relu_forward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),
                          st.out.data_ptr(), self.prec, s)
+        elif st.kind == "lrn":
+            lay = st.cl.layer
+            hh, ww, cc = st.in_nhwc
+            self._call(st, "pc_lrn_forward", self.B * hh * ww, cc, lay.size, lay.k, lay.alpha, lay.beta,
+                       st.inp.data_ptr(), st.out.data_ptr(), self.prec, s)
+        elif st.kind == "dropout":
+            if self.training:
+                self._dropout(st, st.inp, st.out)
+            else:
+                st.out[: st.inp.numel()].copy_(st.inp)
         elif st.kind == "pool":
             hh, ww, cc = st.in_nhwc
             self._call(st, "pc_maxpool_forward", self.B, hh, ww, cc, st.cl.layer.kernel, st.cl.layer.stride,
@@ -450,6 +488,12 @@ class ColumnEngine:
                      float(loss_scale), st.out.data_ptr(), st.row_loss.data_ptr(),
                      self.bad_label.data_ptr(), self.prec, s)
             self._call(st, "pc_sum_f64", self.B, st.row_loss.data_ptr(), self.loss.data_ptr(), s)
+
+    def _dropout(self, st, src, dst):
+        hh, ww, cc, cdense, coff, thresh = st.drop
+        self._call(st, "pc_dropout", self.B, hh, ww, cc, cdense, coff, self.replica * self.B, self.dropout_seed,
+                   self.step_ctr.data_ptr(), st.cl.index, thresh, st.cl.layer.p, src.data_ptr(), dst.data_ptr(),
+                   self.prec, self.stream)
 
     def _in_mat(self, st) -> L.Mat:
         d = math.prod(st.in_nhwc)
@@ -491,6 +535,15 @@ class ColumnEngine:
             if not st.skip_bwd and want_dx:
                 self._call(st, "pc_relu_backward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),
                          st.gout.data_ptr(), st.gin.data_ptr(), self.prec, s)
+        elif st.kind == "lrn":
+            if want_dx:
+                lay = st.cl.layer
+                hh, ww, cc = st.in_nhwc
+                self._call(st, "pc_lrn_backward", self.B * hh * ww, cc, lay.size, lay.k, lay.alpha, lay.beta,
+                           st.inp.data_ptr(), st.gout.data_ptr(), st.gin.data_ptr(), self.prec, s)
+        elif st.kind == "dropout":
+            if want_dx:
+                self._dropout(st, st.gout, st.gin)
         elif st.kind == "pool":
             if want_dx:
                 hh, ww, cc = st.in_nhwc
@@ -505,6 +558,8 @@ class ColumnEngine:
             self._call(st, "pc_scale", n, st.gin.data_ptr(), st.gin.data_ptr(), 1.0 / self.m, self.prec, s)
 
     def sgd(self):
+        if self.has_dropout:  # next step draws fresh masks
+            self.lib.call("pc_counter_add", self.step_ctr.data_ptr(), 1, self.stream)
         if getattr(self, "_sgd_regions", None) is not None:
             n, mx, tab = self._sgd_regions
             self.lib.call("pc_sgd_step", n, tab.data_ptr(), mx, self.lr, self.mom, self.wd, self.stream)

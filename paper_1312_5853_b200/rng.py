@@ -27,6 +27,7 @@ DOMAIN_SHUFFLE = 2
 DOMAIN_TEMPLATE = 3
 DOMAIN_TRAIN = 4
 DOMAIN_TEST = 5
+DOMAIN_DROPOUT = 6   # extension: dropout keep masks
 
 _U = np.uint64
 
@@ -109,3 +110,26 @@ def permutation(seed: int, epoch: int, n: int) -> np.ndarray:
     order = np.arange(n, dtype=np.int64)
     derive(seed, DOMAIN_SHUFFLE, epoch).shuffle(order)
     return order
+
+
+def dropout_state(seed: int, step: int, layer: int) -> int:
+    """SplitMix64 state of the dropout stream of (seed, training step, layer):
+    element i of the dense activation (NCHW flatten, global batch row-major)
+    draws u_i = mix(state + (i + 1) * GOLDEN) — counter based, so any slice of
+    the activation (a replica's rows, a column's channels) draws independently
+    and every plan sees the same mask as the dense single-worker run."""
+    return derive(seed, DOMAIN_DROPOUT, ((step & 0xFFFFFFFFFFFF) << 16) | (layer & 0xFFFF)).state
+
+
+def dropout_threshold(p: float) -> int:
+    """keep iff (u >> 11) >= threshold, i.e. uniform(u) >= p with uniform = top53 * 2^-53."""
+    import math
+    return int(math.ceil(p * 2.0**53))
+
+
+def dropout_keep(seed: int, step: int, layer: int, index: np.ndarray, p: float) -> np.ndarray:
+    """Keep mask (bool) of the dense-activation elements ``index`` (int64)."""
+    state = _U(dropout_state(seed, step, layer))
+    with np.errstate(over="ignore"):
+        u = _mix_vec(state + (np.asarray(index, dtype=np.uint64) + _U(1)) * _U(GOLDEN))
+    return (u >> _U(11)) >= _U(dropout_threshold(p))

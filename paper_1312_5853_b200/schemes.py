@@ -14,6 +14,7 @@ replaced by bit-identical local updates; the ledger still books it).
 
 from __future__ import annotations
 
+import gc
 import os
 from dataclasses import dataclass
 
@@ -86,9 +87,11 @@ class _Runner:
                 replica, column = divmod(wid, m)
                 old = fabric._engines.get(wid)
                 eng = ColumnEngine(cs, wid, replica, column, shard, fabric.prec, dev, fabric._hyper)
+                eng.dropout_seed = int(getattr(fabric, "dropout_seed", 0))
                 if old is not None:
                     eng.p32.copy_(old.p32)
                     eng.v32.copy_(old.v32)
+                    eng.step_ctr.copy_(old.step_ctr)
                     if eng.plow is not None:
                         eng.plow.copy_(old.plow)
                 else:
@@ -176,10 +179,13 @@ class _Runner:
             if key not in self._seen:
                 self._seen.add(key)
                 return self._launch(loss_scale)
+            # free garbage first: a collection during capture can release blocks that
+            # other streams used, and the allocator's event calls would invalidate it
+            gc.collect()
             torch.cuda.synchronize(self.fabric.torch_device)
             g = torch.cuda.CUDAGraph()
             l0 = L.lib().dll.pc_launch_count()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 self._launch(loss_scale)
             self.graph_launches = int(L.lib().dll.pc_launch_count() - l0)
             self._graphs[key] = g
@@ -334,6 +340,7 @@ def evaluation_errors(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, x,
         for j in range(m):
             src = fabric._engines.get(j)
             eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, dev, fabric._hyper)
+            eng.training = False   # dropout is the identity at evaluation
             if src is not None:
                 eng.p32.copy_(src.p32)
                 if eng.plow is not None:
