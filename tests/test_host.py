@@ -75,7 +75,7 @@ def test_parse_errors():
     with pytest.raises(ValidationError):
         parse_network("input 3 224 224\nconv 96 11 4 0\nsoftmax 10\n")
     with pytest.raises(ValidationError, match="unknown layer keyword"):
-        parse_network("input 1 4 4\nlrn 5\nsoftmax 16\n")
+        parse_network("input 1 4 4\nbatchnorm 5\nsoftmax 16\n")   # lrn / dropout are extensions now
     with pytest.raises(ValidationError):
         parse_plan("gpus 4\n")
     assert parse_plan("data_shards 2\nmodel_columns 2\ncross_layers 3\n") == ParallelPlan(2, 2, (3,))
