@@ -218,6 +218,13 @@ class ColumnEngine:
             st, prv = self.layers[i], self.layers[i - 1]
             st.mask_dx = st.kind in ("conv", "fc", "pool") and prv.kind == "relu" and prv.skip_bwd
 
+    def param_region(self, i: int) -> tuple:
+        """[lo, hi) of layer position i's weights + bias in the flat buffers (up to the
+        next parameter layer, alignment padding included)."""
+        st = self.layers[i]
+        nxt = [t.w_off for t in self.layers[i + 1:] if t.w_off >= 0]
+        return st.w_off, (nxt[0] if nxt else self.n_flat)
+
     def _split_before(self, i: int) -> bool:
         """Is the activation entering layer position i split across columns?"""
         rep = True

@@ -322,15 +322,32 @@ class LocalReducer:
 
 
 class NcclReducer:
-    """One replica per rank: sum the flat gradient over the replica group."""
+    """One replica per rank: sum the flat gradient over the replica group.
+
+    Overlapped with the backward: the flat gradient is in ascending layer order
+    and the backward runs in descending order, so as soon as a layer's weight
+    gradient kernels are enqueued its region is final. ``layer_done`` then
+    issues an asynchronous all-reduce of that region (NCCL's stream waits for
+    the compute stream at the call, then runs beside the rest of the backward);
+    ``reduce`` makes the compute stream wait for every bucket before the SGD.
+    Buckets are layers (AlexNet: fc8 4.1M, fc7 16.8M, fc6 37.7M, then the convs)."""
 
     def __init__(self, group):
         self.group = group
+        self.works = []
+
+    def layer_done(self, e, lo: int, hi: int):
+        self.works.append(torch.distributed.all_reduce(e.g32[lo:hi], group=self.group, async_op=True))
 
     def reduce(self, per_column: dict):
-        for engines in per_column.values():
-            for e in engines:
-                torch.distributed.all_reduce(e.g32, group=self.group)
+        if not self.works:   # nothing was bucketed (no layer_done calls): one all-reduce per engine
+            for engines in per_column.values():
+                for e in engines:
+                    torch.distributed.all_reduce(e.g32, group=self.group)
+            return
+        for w in self.works:
+            w.wait()
+        self.works = []
 
 
 def book_step(fabric: Fabric, plan, cs, shard: int) -> None:

@@ -203,6 +203,7 @@ class _Runner:
             lo = eng.replica * shard
             eng.load_batch(self.x_dev[lo:lo + shard], self.y_dev[lo:lo + shard])
         n = len(self.cs.col_layers)
+        overlap = self.reducer is not None and hasattr(self.reducer, "layer_done")
         for engines in self.replicas.values():
             for i in range(n):
                 if self.cs.col_layers[i].cross and self.exchange is not None:
@@ -212,6 +213,8 @@ class _Runner:
             for i in range(n - 1, -1, -1):
                 for e in engines:
                     e.backward(i)
+                    if overlap and e.layers[i].w_off >= 0:
+                        self.reducer.layer_done(e, *e.param_region(i))
                 if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
                     self.exchange.reduce_scatter(i, engines)
         if self.reducer is not None:

@@ -133,3 +133,41 @@ def test_booked_ledger_equals_comm_volume(d, m, cross):
     vol = P.comm_volume(plan, net, 4 * d)
     assert fab.ledger.total_bytes == vol.bytes
     assert fab.ledger.total_messages == vol.messages
+
+
+def _bucket_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1312_5853_b200.fabric import NcclReducer, make_groups
+        _, rep_g = make_groups(world, 1, rank)
+        rs = np.random.default_rng(100 + rank)
+        eng = types.SimpleNamespace(g32=torch.from_numpy(rs.standard_normal(64).astype(np.float32)))
+        red = NcclReducer(rep_g)
+        for lo, hi in ((40, 64), (16, 40), (0, 16)):      # backward order: last layer first
+            red.layer_done(eng, lo, hi)
+        red.reduce({0: [eng]})
+        q.put((rank, eng.g32.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bucketed_gradient_allreduce_overlapped_with_backward():
+    """Data-parallel reduction issued per layer region as the backward finishes it
+    (async all-reduce buckets, waited before the SGD) sums the replicas exactly
+    like one all-reduce of the flat gradient."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = sum(np.random.default_rng(100 + r).standard_normal(64).astype(np.float32).astype(np.float64)
+               for r in range(world))
+    for r in range(world):
+        np.testing.assert_allclose(got[r], want, rtol=1e-6, atol=1e-6)
