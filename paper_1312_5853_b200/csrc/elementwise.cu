@@ -272,6 +272,84 @@ __global__ void maxpool_bwd_k(int B, int H, int W, int C, int k, int s, int Ho, 
   if constexpr (V == 8) Vec8<T>::store(gx + o, acc); else gx[o] = cvt<T>(acc[0]);
 }
 
+// bf16 k=3, s=2 backward with byte-SIMD routing: for each covering window and
+// each of its (at most 4) window positions inside this 2x2 block, one __vcmpeq4
+// per 4 channels selects the channels whose argmax is that position, the byte
+// masks are widened to 16-bit lanes (prmt) and AND the packed bf16 gradient, so
+// a contribution costs two integer ops and an fp32 add per channel instead of a
+// compare/select/add per (pixel, window, channel). Same fixed order (ascending
+// (oy, ox) per pixel) and fp32 accumulation as maxpool_bwd_k3s2_k.
+__global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int Wo,
+                                                               const __nv_bfloat16* __restrict__ gy,
+                                                               const uint8_t* __restrict__ arg,
+                                                               const __nv_bfloat16* __restrict__ mask,
+                                                               __nv_bfloat16* __restrict__ gx) {
+  const int H2 = (H + 1) >> 1, W2 = (W + 1) >> 1;
+  const unsigned cg = (unsigned)(C >> 3);
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (unsigned)B * H2 * W2 * cg) return;
+  const unsigned blk = t / cg;
+  const int c0 = (int)(t - blk * cg) * 8;
+  const unsigned r = blk / (unsigned)W2;
+  const int X = (int)(blk - r * W2);
+  const int b = (int)(r / (unsigned)H2);
+  const int Y = (int)(r - (unsigned)b * H2);
+  float acc[4][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[q][v] = 0.f;
+#pragma unroll
+  for (int dy = -1; dy <= 0; ++dy) {
+    const int oy = Y + dy;
+    if (oy < 0 || oy >= Ho) continue;
+#pragma unroll
+    for (int dx = -1; dx <= 0; ++dx) {
+      const int ox = X + dx;
+      if (ox < 0 || ox >= Wo) continue;
+      const long long o = (((long long)b * Ho + oy) * Wo + ox) * C + c0;
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + o));
+      const uint4 g = __ldg(reinterpret_cast<const uint4*>(gy + o));
+#pragma unroll
+      for (int qy = 0; qy < 2; ++qy) {
+        const int li = qy - 2 * dy;  // row of pixel (2Y + qy) inside window oy
+        if (li > 2) continue;
+#pragma unroll
+        for (int qx = 0; qx < 2; ++qx) {
+          const int lj = qx - 2 * dx;
+          if (lj > 2) continue;
+          const unsigned want = 0x01010101u * (unsigned)(li * 3 + lj);
+          const unsigned m0 = __vcmpeq4(a.x, want), m1 = __vcmpeq4(a.y, want);
+          const unsigned s0 = g.x & __byte_perm(m0, 0, 0x1100), s1 = g.y & __byte_perm(m0, 0, 0x3322);
+          const unsigned s2 = g.z & __byte_perm(m1, 0, 0x1100), s3 = g.w & __byte_perm(m1, 0, 0x3322);
+          float* ac = acc[qy * 2 + qx];
+          ac[0] += __uint_as_float(s0 << 16);
+          ac[1] += __uint_as_float(s0 & 0xFFFF0000u);
+          ac[2] += __uint_as_float(s1 << 16);
+          ac[3] += __uint_as_float(s1 & 0xFFFF0000u);
+          ac[4] += __uint_as_float(s2 << 16);
+          ac[5] += __uint_as_float(s2 & 0xFFFF0000u);
+          ac[6] += __uint_as_float(s3 << 16);
+          ac[7] += __uint_as_float(s3 & 0xFFFF0000u);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int y = 2 * Y + (q >> 1), x = 2 * X + (q & 1);
+    if (y >= H || x >= W) continue;
+    const long long o = (((long long)b * H + y) * W + x) * C + c0;
+    if (mask) {
+      float mk[8];
+      Vec8<__nv_bfloat16>::load(mask + o, mk);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[q][v] = mk[v] > 0.f ? acc[q][v] : 0.f;
+    }
+    Vec8<__nv_bfloat16>::store(gx + o, acc[q]);
+  }
+}
+
 // k=3, s=2 (every AlexNet pool): one thread per 2x2 input block (Y, X) and 8
 // channels. The block is covered exactly by windows {Y-1, Y} x {X-1, X}, so the
 // thread reads those <= 4 windows' gradient + argmax once and writes 4 pixels
@@ -655,7 +733,11 @@ extern "C" int pc_maxpool_backward(int B, int H, int W, int C, int k, int s, con
   PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
   const long long work22 = (long long)B * ((H + 1) / 2) * ((W + 1) / 2) * (C / 8);
   DISPATCH_PREC(prec, T, {
-    if (vec && k == 3 && s == 2)
+    if (vec && k == 3 && s == 2 && prec == PC_BF16)
+      maxpool_bwd_bf16_k3s2_k<<<grid_for(work22, 256), 256, 0, S(st)>>>(
+          B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(gy), argmax,
+          static_cast<const __nv_bfloat16*>(mask), static_cast<__nv_bfloat16*>(gx));
+    else if (vec && k == 3 && s == 2)
       maxpool_bwd_k3s2_k<T><<<grid_for(work22, 256), 256, 0, S(st)>>>(
           B, H, W, C, Ho, Wo, static_cast<const T*>(gy), argmax, static_cast<const T*>(mask),
           static_cast<T*>(gx));
