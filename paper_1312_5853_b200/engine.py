@@ -288,6 +288,32 @@ class ColumnEngine:
         self._sgd_dev.copy_(torch.frombuffer(bytearray(bytes(self._sgd_host)), dtype=torch.uint8))
         self._sgd_regions = None
 
+    def sgd_split_table(self, first: int):
+        """Two SGD launch tables over the flat buffers: parameters of layer positions
+        >= ``first`` (the FC head: final once the backward has passed it, so their
+        update can run on a side stream beside the convolutions' backward) and the
+        rest. Returns ((n, max_numel, device table), same) or None."""
+        groups = ([], [])
+        for i, st in enumerate(self.layers):
+            if st.w_off < 0:
+                continue
+            lo, hi = self.param_region(i)
+            groups[0 if i >= first else 1].append((lo, hi - lo))
+        if not groups[0] or not groups[1]:
+            return None
+        out = []
+        for regs in groups:
+            tabs = [L.SgdTensor(self.p32[o:].data_ptr(), self.v32[o:].data_ptr(), self.g32[o:].data_ptr(),
+                                self.plow[o:].data_ptr() if self.plow is not None else None, n) for o, n in regs]
+            arr = (L.SgdTensor * len(tabs))(*tabs)
+            out.append((len(tabs), max(n for _, n in regs),
+                        torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.device)))
+        return tuple(out)
+
+    def sgd_table(self, tab):
+        n, mx, dev = tab
+        self.lib.call("pc_sgd_step", n, dev.data_ptr(), mx, self.lr, self.mom, self.wd, self.stream)
+
     def configure_fused_sgd(self, on: bool):
         """Single-replica plans (no gradient reduction between backward and update):
         the bf16 weight-gradient kernels of conv/FC layers apply the momentum-SGD

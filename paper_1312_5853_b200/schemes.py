@@ -25,7 +25,7 @@ from . import _lib as L
 from .engine import ColumnEngine
 from .errors import ValidationError
 from .fabric import (Fabric, LocalExchange, LocalReducer, NcclExchange, NcclReducer, book_step)
-from .netdef import ColumnizedSpec, NetworkSpec, columnize, column_footprint_elements
+from .netdef import FC, ColumnizedSpec, NetworkSpec, columnize, column_footprint_elements
 from .plan import (  # noqa: F401  (re-exported API)
     CommPhase, CommVolume, ParallelPlan, ParamSet, comm_phases, comm_volume, init_dense_params,
     lists_as_params, load_plan, merge_params, pack_tree, params_as_lists, parse_plan, plan_columnized,
@@ -121,6 +121,17 @@ class _Runner:
         self.y_dev = None
         self._graphs, self._seen = {}, set()
         self.graph_launches, self.replays = 0, 0
+        # single replica, unfused SGD: the FC head's update runs on a side stream as soon
+        # as the backward has passed the first FC layer, overlapping the conv backward
+        self.head_pos = next((i for i, cl in enumerate(cs.col_layers) if isinstance(cl.layer, FC)), None)
+        self.split_sgd = {}
+        if d == 1 and self.head_pos is not None and os.environ.get("PC_SGD_OVERLAP", "1") != "0":
+            for wid, eng in self.engines.items():
+                if not getattr(eng, "fuse_sgd", False) and not eng.has_dropout:
+                    tabs = eng.sgd_split_table(self.head_pos)
+                    if tabs is not None:
+                        self.split_sgd[wid] = tabs
+        self.side = torch.cuda.Stream(device=dev) if self.split_sgd else None
 
     def upload(self, batch_x, batch_y):
         """Host -> device copy of the global batch (float32 NCHW, int32 labels).
@@ -215,12 +226,21 @@ class _Runner:
                     e.backward(i)
                     if overlap and e.layers[i].w_off >= 0:
                         self.reducer.layer_done(e, *e.param_region(i))
+                    if i == self.head_pos and e.wid in self.split_sgd:   # fork: head update on the side stream
+                        self.side.wait_stream(torch.cuda.current_stream())
+                        with torch.cuda.stream(self.side):
+                            e.sgd_table(self.split_sgd[e.wid][0])
                 if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
                     self.exchange.reduce_scatter(i, engines)
         if self.reducer is not None:
             self.reducer.reduce(self.columns)
         for eng in self.engines.values():
-            eng.sgd()
+            if eng.wid in self.split_sgd:
+                eng.sgd_table(self.split_sgd[eng.wid][1])
+            else:
+                eng.sgd()
+        if self.side is not None:   # join
+            torch.cuda.current_stream().wait_stream(self.side)
 
     def loss(self) -> float:
         """Sum over replicas of column 0's loss (host read-back; raises on bad labels)."""
