@@ -558,6 +558,10 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
 // consecutive X, so each (c, row) read is coalesced across the warp) and writes
 // the Cs-channel row, ch = (dy*s + dx)*C + c, with 16-byte stores (zero for
 // padding and ch >= s*s*C). Each input element is read exactly once.
+// read-only (non-coherent) scalar load of an input written by an earlier kernel
+__device__ __forceinline__ float ldg_ro(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float ldg_ro(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+
 template <typename TS, int CS, int SS, int CC>  // SS, CC > 0: compile-time stride / channels
 __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_, int p, int Hs, int Ws,
                                              const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst) {
@@ -580,7 +584,7 @@ __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_
         const bool ok = iy >= 0 && iy < H && ix >= 0 && ix < W;
 #pragma unroll
         for (int c = 0; c < CC; ++c)
-          v[(dy * SS + dx) * CC + c] = ok ? ld(x + (((long long)b * CC + c) * H + iy) * W + ix) : 0.f;
+          v[(dy * SS + dx) * CC + c] = ok ? ldg_ro(x + (((long long)b * CC + c) * H + iy) * W + ix) : 0.f;
       }
     }
   } else {
