@@ -293,3 +293,32 @@ def test_fused_sgd_epilogue_matches_separate_update():
     for i in p0:
         for k in ("w", "b"):
             assert rel(p1[i][k] - dense[i][k], p0[i][k] - dense[i][k]) < 1e-5, (i, k)
+
+
+def test_train_device_resident_feed_matches_host_feed_and_oracle():
+    """trainer.train (reference `trainer.py:99-154`) with the batch gathered on the
+    device from an HBM-resident copy of the dataset gives the
+    same trajectory as the host-gathered feed, and both follow the float64
+    oracle over the same rng.permutation batch order (fp32 mode, 1e-5)."""
+    import paper_1312_5853_b200 as P
+    from oracle.ref_engine import OracleFabric
+    from paper_1312_5853_b200 import rng
+    net = P.load_network(CONFIGS / "tinynet.net")
+    train_set, _ = P.gen_synthetic(10, 4, net.input_shape, seed=3)
+    plan = P.ParallelPlan(2, 1)
+    runs = []
+    for dev in (True, False):
+        cfg = P.TrainConfig(net=net, plan=plan, epochs=2, batch=8, seed=5, train_data=train_set,
+                            precision="fp32", device_data=dev)
+        runs.append([r.train_loss for r in P.train(cfg).records])
+    assert runs[0] == runs[1]
+    of = OracleFabric(net, plan, P.init_dense_params(net, 5))
+    want = []
+    for epoch in range(2):
+        order = rng.permutation(5, epoch, train_set.size)
+        for step in range(train_set.size // 8):
+            idx = order[step * 8:(step + 1) * 8]
+            want.append(of.step(train_set.images[idx], train_set.labels[idx]))
+    assert len(want) == len(runs[0])
+    for got, ref in zip(runs[0], want):
+        assert abs(got - ref) / abs(ref) < 1e-5
