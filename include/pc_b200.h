@@ -172,6 +172,11 @@ typedef struct {
 /* `table` is a DEVICE array of n_tensors descriptors. */
 PC_API int pc_sgd_step(int n_tensors, const pc_sgd_tensor* table, long long max_numel, float lr,
                 float momentum, float weight_decay, pc_stream_t stream);
+/* Same update as a background launch: at most ctas_per_sm 256-thread CTAs per SM
+ * in total, so it can run on a side stream beside a persistent GEMM that holds
+ * one CTA per SM (ctas_per_sm <= 0: identical to pc_sgd_step). */
+PC_API int pc_sgd_step_ex(int n_tensors, const pc_sgd_tensor* table, long long max_numel, float lr,
+                   float momentum, float weight_decay, int ctas_per_sm, pc_stream_t stream);
 
 /* --- extensions beyond the reference (the reference has no such
  * layers, netdef.py:219-220): definitions in oracle/ref_kernels.py ----------- */

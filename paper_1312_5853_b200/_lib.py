@@ -66,6 +66,7 @@ SIGNATURES = {
     "pc_softmax_xent": (_i, [_i, _i, _vp, _vp, _d, _vp, _vp, _vp, _i, _vp]),
     "pc_sum_f64": (_i, [_i, _vp, _vp, _vp]),
     "pc_sgd_step": (_i, [_i, _vp, _ll, _f, _f, _f, _vp]),
+    "pc_sgd_step_ex": (_i, [_i, _vp, _ll, _f, _f, _f, _i, _vp]),
     "pc_space_to_depth": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "pc_mask_f32": (_i, [_ll, _vp, _vp, _vp]),
     "pc_lrn_forward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _i, _vp]),

@@ -499,6 +499,53 @@ __global__ void sgd_k(const pc_sgd_tensor* __restrict__ tab, float lr, float mom
   }
 }
 
+// Background variant (a few CTAs per SM beside a running GEMM): grid-stride with
+// two float4 groups in flight per thread, same arithmetic as sgd_k.
+__global__ void __launch_bounds__(256) sgd_bg_k(const pc_sgd_tensor* __restrict__ tab, float lr, float mom,
+                                                float wd) {
+  const pc_sgd_tensor t = tab[blockIdx.y];
+  const bool vec = ((reinterpret_cast<uintptr_t>(t.p) | reinterpret_cast<uintptr_t>(t.v) |
+                     reinterpret_cast<uintptr_t>(t.g)) & 15) == 0 &&
+                   (t.p_lowp == nullptr || (reinterpret_cast<uintptr_t>(t.p_lowp) & 7) == 0);
+  const long long stride = (long long)gridDim.x * blockDim.x * 4;
+  const long long n4 = vec ? t.n / 4 * 4 : 0;
+  long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4;
+  for (; i + stride < n4; i += 2 * stride) {
+    float4 p[2], v[2], g[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      p[u] = *reinterpret_cast<const float4*>(t.p + i + u * stride);
+      v[u] = *reinterpret_cast<const float4*>(t.v + i + u * stride);
+      g[u] = __ldg(reinterpret_cast<const float4*>(t.g + i + u * stride));
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      v[u].x = mom * v[u].x - lr * (g[u].x + wd * p[u].x);
+      v[u].y = mom * v[u].y - lr * (g[u].y + wd * p[u].y);
+      v[u].z = mom * v[u].z - lr * (g[u].z + wd * p[u].z);
+      v[u].w = mom * v[u].w - lr * (g[u].w + wd * p[u].w);
+      p[u].x += v[u].x; p[u].y += v[u].y; p[u].z += v[u].z; p[u].w += v[u].w;
+      *reinterpret_cast<float4*>(t.v + i + u * stride) = v[u];
+      *reinterpret_cast<float4*>(t.p + i + u * stride) = p[u];
+      if (t.p_lowp) {
+        __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(t.p_lowp) + i + u * stride);
+        q[0] = __floats2bfloat162_rn(p[u].x, p[u].y);
+        q[1] = __floats2bfloat162_rn(p[u].z, p[u].w);
+      }
+    }
+  }
+  for (; i < t.n; i += stride) {
+    for (long long j = i; j < t.n && j < i + 4; ++j) {
+      float p = t.p[j], v = t.v[j], g = t.g[j];
+      v = mom * v - lr * (g + wd * p);
+      p += v;
+      t.v[j] = v;
+      t.p[j] = p;
+      if (t.p_lowp) static_cast<__nv_bfloat16*>(t.p_lowp)[j] = __float2bfloat16_rn(p);
+    }
+  }
+}
+
 // Layout helpers ---------------------------------------------------------------------
 template <typename T>
 __global__ void nchw_to_nhwc_k(int B, int C, int H, int W, int Cp, const float* __restrict__ src,
@@ -782,6 +829,25 @@ extern "C" int pc_sgd_step(int n_tensors, const pc_sgd_tensor* table, long long 
   if (gx > 1184) gx = 1184;  // 8 CTAs per SM on 148 SMs; grid-stride beyond that
   sgd_k<<<dim3(gx, n_tensors), 256, 0, S(st)>>>(table, lr, momentum, weight_decay);
   PC_CUDA_CHECK_LAUNCH("sgd_step");
+  return PC_OK;
+}
+
+extern "C" int pc_sgd_step_ex(int n_tensors, const pc_sgd_tensor* table, long long max_numel, float lr,
+                              float momentum, float weight_decay, int ctas_per_sm, pc_stream_t st) {
+  if (ctas_per_sm <= 0) return pc_sgd_step(n_tensors, table, max_numel, lr, momentum, weight_decay, st);
+  PC_REQUIRE(n_tensors >= 0 && n_tensors <= 65535, PC_EVALUE, "sgd: bad tensor count %d", n_tensors);
+  if (n_tensors == 0 || max_numel <= 0) return PC_OK;
+  static int sms = [] {
+    int d = 0, n = 148;
+    if (cudaGetDevice(&d) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n;
+  }();
+  int gx = sms * ctas_per_sm / n_tensors;
+  const int need = grid_for((max_numel + 3) / 4, 256);
+  if (gx > need) gx = need;
+  if (gx < 1) gx = 1;
+  sgd_bg_k<<<dim3(gx, n_tensors), 256, 0, S(st)>>>(table, lr, momentum, weight_decay);
+  PC_CUDA_CHECK_LAUNCH("sgd_step_ex");
   return PC_OK;
 }
 

@@ -89,6 +89,9 @@ struct alignas(64) Params {
   int macc_chunks;  // A_IM2COL_MN5: 64-row A chunks with real rows (<= 10)
   int mt_rows;      // rows per M tile: 128 * CTA-group size * accumulators (set at launch)
   unsigned long long* trace;  // debug: per-CTA per-tile clock64 stamps (tools/trace_gemm.py), normally null
+  // EPI_F32 through TMA stores: fp32 view {N, M, split slices} of p.out, box {32, 32, 1}, 128B swizzle
+  int out_tma;
+  CUtensorMap tma_out;
 };
 
 // Debug timeline: slot s of tile lt of CTA b (first TRACE_TILES tiles).
@@ -329,6 +332,7 @@ constexpr int smem_bytes() {
          (2 * STAGES + 4) * 8 + 16;
 }
 
+
 // ------------------------------------------------------------------- kernel
 // Persistent: each CTA (CG == 1) or CTA pair (CG == 2, a 2-SM cluster issuing
 // tcgen05.mma.cta_group::2 with M = 256) walks tiles t = unit, unit + units, ...
@@ -476,6 +480,94 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
   }
 }
 
+// fp32 epilogue by TMA store: each epilogue warp drains 32 accumulator columns
+// of its 32 TMEM lanes into a 4 KB 128B-swizzled box in SMEM (conflict-free: lane
+// r writes 16 B chunk j at r * 128 + ((j ^ r % 8) << 4)) and one lane issues a
+// bulk tensor store of the box; the TMA engine writes whole 128-byte lines. The
+// direct path (each lane storing its own row, 32 rows per warp instruction)
+// reaches ~2 TB/s on the 151 MB fc6 weight gradient.
+constexpr int F32_BOX_BYTES = 32 * 128;
+constexpr int F32_STAGE_BYTES = 8 * F32_BOX_BYTES;  // one box per epilogue warp
+template <int EPI, int BN, int STAGES, int CG, int AM>
+constexpr bool f32_tma_epi() {
+  return EPI == EPI_F32 && !a_is_gather<AM>() && macc_of<AM>() == 1 && AM != A_HALO_K && BN % 32 == 0 &&
+         smem_bytes<BN, STAGES, CG, false, 1>() + 1024 + F32_STAGE_BYTES <= 227 * 1024;
+}
+template <int EPI, int BN, int STAGES, int CG, int AM>
+constexpr int kernel_smem() {
+  return smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>()>() +
+         (f32_tma_epi<EPI, BN, STAGES, CG, AM>() ? 1024 + F32_STAGE_BYTES : 0);
+}
+
+template <int BN, int CG, int EPW>
+__device__ __forceinline__ void epilogue_f32_tma(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
+                                                 int unit, int units, uint32_t rank, int quad, int grp, int lane,
+                                                 uint8_t* box) {
+  constexpr int TCOLS = tmem_cols<BN>();
+  constexpr int ACC = acc_count<BN>();
+  const uint32_t sbox = smem_u32(box);
+  int lt = 0;
+  for (int t = unit; t < p.tiles; t += units, ++lt) {
+    const TileCoord tc = tile_coord<CG>(p, t, BN);
+    const int acc = lt % ACC;
+    mbar_wait(&tfull[acc], (lt / ACC) & 1);
+    tc_fence_after();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
+    const uint32_t tbase = tmem + acc * TCOLS + ((uint32_t)(quad * 32) << 16);
+    const int row0 = tc.m0 + (int)rank * BM + quad * 32;
+#pragma unroll 1
+    for (int c0 = grp * 32; c0 < BN; c0 += 32 * EPW) {
+      float v[32];
+      if (tc.nkb > 0) {
+        tmem_ld16(tbase + c0, v);
+        tmem_ld16(tbase + c0 + 16, v + 16);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = 0.f;
+      }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // box free again
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sbox + lane * 128 + ((j ^ (lane & 7)) << 4)),
+                     "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                     : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                reinterpret_cast<uint64_t>(&p.tma_out)),
+            "r"(tc.n0 + c0), "r"(row0), "r"(tc.z), "r"(sbox)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    // accumulator drained (the stores read SMEM, not TMEM): release it
+    tc_fence_before();
+    __syncwarp();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
+    if (lane == 0) {
+      if constexpr (CG == 1) {
+        mbar_arrive(&tempty[acc]);
+      } else {
+        mbar_arrive_cluster(&tempty[acc], 0);
+      }
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
+// Stage count for a (BN, CG) ring: one stage fewer for an fp32 output when that
+// makes room for the TMA-store boxes.
+template <int EPI, int BN, int S, int CG>
+constexpr int fst() {
+  return EPI == EPI_F32 && BN % 32 == 0 && smem_bytes<BN, S, CG, false, 1>() + 1024 + F32_STAGE_BYTES > 227 * 1024
+             ? S - 1
+             : S;
+}
+
 template <int AM> constexpr int kernel_threads() { return a_is_gather<AM>() ? 192 + GATHER_THREADS : 320; }
 
 template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
@@ -511,6 +603,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   uint64_t* tfull = empty + STAGES;  // [ACC]
   uint64_t* tempty = tfull + 2;      // [ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr bool F32TMA = f32_tma_epi<EPI, BN, STAGES, CG, AM>();
+  uint8_t* f32_boxes = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot) + 4 + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.tiles;
@@ -555,6 +649,11 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   }
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, descriptor prefetch) may overlap the previous kernel's tail;
+  // no global memory is touched before the previous grid has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 5) {
     // ------------------------------------------------------------ TMA producer
@@ -926,8 +1025,17 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       }
     }
   } else {
-    epilogue<EPI, BN, CG, EPW, HALO, MACC>(p, tmem, tfull, tempty, unit, units, rank, warp & 3, warp >= 6 ? 1 : 0,
-                                           lane);
+    const int quad = warp & 3, grp = warp >= 6 ? 1 : 0;
+    if constexpr (F32TMA) {
+      if (p.out_tma) {
+        epilogue_f32_tma<BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
+                                      f32_boxes + (grp * 4 + quad) * F32_BOX_BYTES);
+      } else {
+        epilogue<EPI, BN, CG, EPW, HALO, MACC>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane);
+      }
+    } else {
+      epilogue<EPI, BN, CG, EPW, HALO, MACC>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane);
+    }
   }
 
   tc_fence_before();
@@ -1027,27 +1135,61 @@ static int make_im2col_map(CUtensorMap* map, const void* ptr, int cs, int W, int
 }
 
 static std::atomic<unsigned long long> g_tc_launches{0}, g_simt_launches{0};
+
+// Programmatic dependent launch for the GEMM kernels (PC_PDL=0 disables): a
+// GEMM's prologue overlaps the tail of the kernel before it on the stream.
+static bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("PC_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
 static unsigned long long* g_trace = nullptr;  // pc_debug_trace_gemm
+
+// fp32 output view for the TMA-store epilogue: {N, M, splits} with row stride
+// o_ld and slice stride split_stride (elements). 0 = not expressible (or
+// PC_F32_TMA=0): the kernel falls back to per-lane row stores.
+static int f32_out_map(CUtensorMap* map, const Params& p, int splits) {
+  static const int on = [] {
+    const char* e = getenv("PC_F32_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  if (!on || !get_encode() || (reinterpret_cast<uintptr_t>(p.out) & 15) || p.o_ld % 4 ||
+      (splits > 1 && p.split_stride % 4) || p.N < 1 || p.M < 1)
+    return 0;
+  cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)p.M, (cuuint64_t)std::max(splits, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)p.o_ld * 4,
+                           (cuuint64_t)(splits > 1 ? p.split_stride : p.o_ld * (long long)p.M) * 4};
+  cuuint32_t box[3] = {32u, 32u, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, p.out, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
 
 template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
 static int launch(const Params& p, int splits, cudaStream_t st) {
   auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES, CG>;
-  constexpr int smem = smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>()>();
+  constexpr int smem = kernel_smem<EPI, BN, STAGES, CG, AM>();
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   constexpr int threads = kernel_threads<AM>();
   static int resident = 0;  // persistent CTAs the device holds at once
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1072,6 +1214,7 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
   Params q = p;
   q.trace = g_trace;
   q.mt_rows = BM * CG * macc_of<AM>();
+  if constexpr (f32_tma_epi<EPI, BN, STAGES, CG, AM>()) q.out_tma = f32_out_map(&q.tma_out, q, splits);
   q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, q.mt_rows) * splits;
   const int units = std::min(q.tiles, resident / CG);
   cfg.gridDim = dim3(units * CG);
@@ -1146,35 +1289,35 @@ static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
   if constexpr (!a_is_gather<AM>()) {
     if (t.cg == 2) {
       switch (t.bn) {
-        case 64: return launch<AM, B_TMA_K, EPI, 64, 8, 2>(p, splits, st);
-        case 96: return launch<AM, B_TMA_K, EPI, 96, 8, 2>(p, splits, st);
-        case 128: return launch<AM, B_TMA_K, EPI, 128, 8, 2>(p, splits, st);
-        case 192: return launch<AM, B_TMA_K, EPI, 192, 7, 2>(p, splits, st);
-        default: return launch<AM, B_TMA_K, EPI, 256, 6, 2>(p, splits, st);
+        case 64: return launch<AM, B_TMA_K, EPI, 64, fst<EPI, 64, 8, 2>(), 2>(p, splits, st);
+        case 96: return launch<AM, B_TMA_K, EPI, 96, fst<EPI, 96, 8, 2>(), 2>(p, splits, st);
+        case 128: return launch<AM, B_TMA_K, EPI, 128, fst<EPI, 128, 8, 2>(), 2>(p, splits, st);
+        case 192: return launch<AM, B_TMA_K, EPI, 192, fst<EPI, 192, 7, 2>(), 2>(p, splits, st);
+        default: return launch<AM, B_TMA_K, EPI, 256, fst<EPI, 256, 6, 2>(), 2>(p, splits, st);
       }
     }
   }
   switch (t.bn) {
-    case 64: return launch<AM, B_TMA_K, EPI, 64, 8, 1>(p, splits, st);
-    case 96: return launch<AM, B_TMA_K, EPI, 96, 7, 1>(p, splits, st);
-    case 128: return launch<AM, B_TMA_K, EPI, 128, 6, 1>(p, splits, st);
-    case 192: return launch<AM, B_TMA_K, EPI, 192, 5, 1>(p, splits, st);
-    default: return launch<AM, B_TMA_K, EPI, 256, 4, 1>(p, splits, st);
+    case 64: return launch<AM, B_TMA_K, EPI, 64, fst<EPI, 64, 8, 1>(), 1>(p, splits, st);
+    case 96: return launch<AM, B_TMA_K, EPI, 96, fst<EPI, 96, 7, 1>(), 1>(p, splits, st);
+    case 128: return launch<AM, B_TMA_K, EPI, 128, fst<EPI, 128, 6, 1>(), 1>(p, splits, st);
+    case 192: return launch<AM, B_TMA_K, EPI, 192, fst<EPI, 192, 5, 1>(), 1>(p, splits, st);
+    default: return launch<AM, B_TMA_K, EPI, 256, fst<EPI, 256, 4, 1>(), 1>(p, splits, st);
   }  }
 }
 template <int AM, int EPI>
 static int launch_mn(const Params& p, Tile t, int splits, cudaStream_t st) {
   if constexpr (!a_is_gather<AM>()) {
     if (t.cg == 2) {
-      if (t.bn == 128) return launch<AM, B_TMA_MN, EPI, 128, 8, 2>(p, splits, st);
-      return launch<AM, B_TMA_MN, EPI, 256, 6, 2>(p, splits, st);
+      if (t.bn == 128) return launch<AM, B_TMA_MN, EPI, 128, fst<EPI, 128, 8, 2>(), 2>(p, splits, st);
+      return launch<AM, B_TMA_MN, EPI, 256, fst<EPI, 256, 6, 2>(), 2>(p, splits, st);
     }
   }
   switch (t.bn) {
-    case 64: return launch<AM, B_TMA_MN, EPI, 64, 8, 1>(p, splits, st);
-    case 128: return launch<AM, B_TMA_MN, EPI, 128, 6, 1>(p, splits, st);
-    case 192: return launch<AM, B_TMA_MN, EPI, 192, 5, 1>(p, splits, st);
-    default: return launch<AM, B_TMA_MN, EPI, 256, 4, 1>(p, splits, st);
+    case 64: return launch<AM, B_TMA_MN, EPI, 64, fst<EPI, 64, 8, 1>(), 1>(p, splits, st);
+    case 128: return launch<AM, B_TMA_MN, EPI, 128, fst<EPI, 128, 6, 1>(), 1>(p, splits, st);
+    case 192: return launch<AM, B_TMA_MN, EPI, 192, fst<EPI, 192, 5, 1>(), 1>(p, splits, st);
+    default: return launch<AM, B_TMA_MN, EPI, 256, fst<EPI, 256, 4, 1>(), 1>(p, splits, st);
   }
 }
 

@@ -301,8 +301,17 @@ class ColumnEngine:
             groups[0 if i >= first else 1].append((lo, hi - lo))
         if not groups[0] or not groups[1]:
             return None
+        merged = []
+        for regs in groups:  # adjacent regions -> one descriptor (one long grid-stride range)
+            m = []
+            for o, n in sorted(regs):
+                if m and m[-1][0] + m[-1][1] == o:
+                    m[-1] = (m[-1][0], m[-1][1] + n)
+                else:
+                    m.append((o, n))
+            merged.append(m)
         out = []
-        for regs in groups:
+        for regs in merged:
             tabs = [L.SgdTensor(self.p32[o:].data_ptr(), self.v32[o:].data_ptr(), self.g32[o:].data_ptr(),
                                 self.plow[o:].data_ptr() if self.plow is not None else None, n) for o, n in regs]
             arr = (L.SgdTensor * len(tabs))(*tabs)
@@ -310,9 +319,11 @@ class ColumnEngine:
                         torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.device)))
         return tuple(out)
 
-    def sgd_table(self, tab):
+    def sgd_table(self, tab, ctas_per_sm: int = 0, stream=None):
+        """ctas_per_sm > 0: background launch (pc_sgd_step_ex) for a side stream."""
         n, mx, dev = tab
-        self.lib.call("pc_sgd_step", n, dev.data_ptr(), mx, self.lr, self.mom, self.wd, self.stream)
+        self.lib.call("pc_sgd_step_ex", n, dev.data_ptr(), mx, self.lr, self.mom, self.wd, ctas_per_sm,
+                      self.stream if stream is None else stream)
 
     def configure_fused_sgd(self, on: bool):
         """Single-replica plans (no gradient reduction between backward and update):

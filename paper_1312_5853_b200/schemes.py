@@ -132,6 +132,9 @@ class _Runner:
                     if tabs is not None:
                         self.split_sgd[wid] = tabs
         self.side = torch.cuda.Stream(device=dev) if self.split_sgd else None
+        # background CTAs per SM for the side-stream update: few enough that each
+        # backward GEMM still finds room for its one persistent CTA per SM
+        self.sgd_bg_ctas = int(os.environ.get("PC_SGD_BG_CTAS", "2"))
 
     def upload(self, batch_x, batch_y):
         """Host -> device copy of the global batch (float32 NCHW, int32 labels).
@@ -229,7 +232,7 @@ class _Runner:
                     if i == self.head_pos and e.wid in self.split_sgd:   # fork: head update on the side stream
                         self.side.wait_stream(torch.cuda.current_stream())
                         with torch.cuda.stream(self.side):
-                            e.sgd_table(self.split_sgd[e.wid][0])
+                            e.sgd_table(self.split_sgd[e.wid][0], ctas_per_sm=self.sgd_bg_ctas)
                 if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
                     self.exchange.reduce_scatter(i, engines)
         if self.reducer is not None:
