@@ -47,7 +47,7 @@ enum AMode {
   A_IM2COL_MN5 = 8
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
-enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2 };
+enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
 
 constexpr int BM = 128, BK = 64;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
@@ -92,6 +92,10 @@ struct alignas(64) Params {
   // EPI_F32 through TMA stores: fp32 view {N, M, split slices} of p.out, box {32, 32, 1}, 128B swizzle
   int out_tma;
   CUtensorMap tma_out;
+  // EPI_SGD: the weight gradient never leaves the SM — fp32 p and v {N, M} and
+  // the bf16 shadow of p, updated in place (v = mom v - lr (g + wd p); p += v)
+  CUtensorMap tma_p, tma_v, tma_pl;
+  float lr, mom, wd;
 };
 
 // Debug timeline: slot s of tile lt of CTA b (first TRACE_TILES tiles).
@@ -493,10 +497,138 @@ constexpr bool f32_tma_epi() {
   return EPI == EPI_F32 && !a_is_gather<AM>() && macc_of<AM>() == 1 && AM != A_HALO_K && BN % 32 == 0 &&
          smem_bytes<BN, STAGES, CG, false, 1>() + 1024 + F32_STAGE_BYTES <= 227 * 1024;
 }
+// EPI_SGD boxes per epilogue warp: p (fp32 32x32, 128B swizzle), v (same), bf16
+// shadow (32x32, 64B swizzle); then one transaction barrier per warp.
+constexpr int SGD_WARP_BYTES = 4096 + 4096 + 2048;
+constexpr int SGD_STAGE_BYTES = 8 * SGD_WARP_BYTES + 8 * 8;
 template <int EPI, int BN, int STAGES, int CG, int AM>
 constexpr int kernel_smem() {
   return smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>()>() +
-         (f32_tma_epi<EPI, BN, STAGES, CG, AM>() ? 1024 + F32_STAGE_BYTES : 0);
+         (f32_tma_epi<EPI, BN, STAGES, CG, AM>() ? 1024 + F32_STAGE_BYTES : 0) +
+         (EPI == EPI_SGD ? 1024 + SGD_STAGE_BYTES : 0);
+}
+
+// Fused momentum-SGD epilogue: per 32-column group a warp TMA-loads the p and v
+// boxes of its 32 rows (issued before its TMEM reads, so the load overlaps
+// them), applies the update with the fp32 gradient straight from TMEM, and
+// TMA-stores p, v and the bf16 shadow. Per parameter: 8 B read + 10 B written,
+// against 4 B gradient store + 12 B read + 10 B written for a separate pass.
+template <int BN, int CG, int EPW>
+__device__ __forceinline__ void epilogue_sgd_tma(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
+                                                 int unit, int units, uint32_t rank, int quad, int grp, int lane,
+                                                 uint8_t* area, uint64_t* lbar) {
+  constexpr int TCOLS = tmem_cols<BN>();
+  constexpr int ACC = acc_count<BN>();
+  const uint32_t sp = smem_u32(area), sv = sp + 4096, sl = sp + 8192;
+  uint32_t phase = 0;
+  int lt = 0;
+  for (int t = unit; t < p.tiles; t += units, ++lt) {
+    const TileCoord tc = tile_coord<CG>(p, t, BN);
+    const int acc = lt % ACC;
+    mbar_wait(&tfull[acc], (lt / ACC) & 1);
+    tc_fence_after();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
+    const uint32_t tbase = tmem + acc * TCOLS + ((uint32_t)(quad * 32) << 16);
+    const int row0 = tc.m0 + (int)rank * BM + quad * 32;
+#pragma unroll 1
+    for (int c0 = grp * 32; c0 < BN; c0 += 32 * EPW) {
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous stores have read the boxes
+        mbar_arrive_expect_tx(lbar, 8192);
+        tma_load_3d<1>(&p.tma_p, lbar, sp, tc.n0 + c0, row0, 0);
+        tma_load_3d<1>(&p.tma_v, lbar, sv, tc.n0 + c0, row0, 0);
+        // L2 prefetch of this warp's next group (next tile's first group at the
+        // end of a tile): its loads then wait on L2, not HBM
+        int nn = tc.n0 + c0 + 32 * EPW, nr = row0;
+        if (c0 + 32 * EPW >= BN) {
+          if (t + units < p.tiles) {
+            const TileCoord nx = tile_coord<CG>(p, t + units, BN);
+            nn = nx.n0 + grp * 32;
+            nr = nx.m0 + (int)rank * BM + quad * 32;
+          } else {
+            nn = -1;
+          }
+        }
+        if (nn >= 0) {
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                           reinterpret_cast<uint64_t>(&p.tma_p)),
+                       "r"(nn), "r"(nr), "r"(0)
+                       : "memory");
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                           reinterpret_cast<uint64_t>(&p.tma_v)),
+                       "r"(nn), "r"(nr), "r"(0)
+                       : "memory");
+        }
+      }
+      float g[32];
+      if (tc.nkb > 0) {
+        tmem_ld16(tbase + c0, g);
+        tmem_ld16(tbase + c0 + 16, g + 16);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) g[q] = 0.f;
+      }
+      mbar_wait(lbar, phase);
+      phase ^= 1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t off = lane * 128 + ((j ^ (lane & 7)) << 4);
+        float4 pp, vv;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(pp.x), "=f"(pp.y), "=f"(pp.z), "=f"(pp.w)
+                     : "r"(sp + off)
+                     : "memory");
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(vv.x), "=f"(vv.y), "=f"(vv.z), "=f"(vv.w)
+                     : "r"(sv + off)
+                     : "memory");
+        vv.x = p.mom * vv.x - p.lr * (g[4 * j] + p.wd * pp.x);
+        vv.y = p.mom * vv.y - p.lr * (g[4 * j + 1] + p.wd * pp.y);
+        vv.z = p.mom * vv.z - p.lr * (g[4 * j + 2] + p.wd * pp.z);
+        vv.w = p.mom * vv.w - p.lr * (g[4 * j + 3] + p.wd * pp.w);
+        pp.x += vv.x; pp.y += vv.y; pp.z += vv.z; pp.w += vv.w;
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sp + off), "f"(pp.x), "f"(pp.y), "f"(pp.z),
+                     "f"(pp.w)
+                     : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sv + off), "f"(vv.x), "f"(vv.y), "f"(vv.z),
+                     "f"(vv.w)
+                     : "memory");
+        __nv_bfloat162 lo = __floats2bfloat162_rn(pp.x, pp.y), hi = __floats2bfloat162_rn(pp.z, pp.w);
+        const uint32_t loff = lane * 64 + (((j >> 1) ^ ((lane >> 1) & 3)) << 4) + (j & 1) * 8;
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(sl + loff), "r"(*reinterpret_cast<uint32_t*>(&lo)),
+                     "r"(*reinterpret_cast<uint32_t*>(&hi))
+                     : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const uint64_t mp = reinterpret_cast<uint64_t>(&p.tma_p), mv = reinterpret_cast<uint64_t>(&p.tma_v),
+                       ml = reinterpret_cast<uint64_t>(&p.tma_pl);
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(mp),
+                     "r"(tc.n0 + c0), "r"(row0), "r"(0), "r"(sp)
+                     : "memory");
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(mv),
+                     "r"(tc.n0 + c0), "r"(row0), "r"(0), "r"(sv)
+                     : "memory");
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(ml),
+                     "r"(tc.n0 + c0), "r"(row0), "r"(0), "r"(sl)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
+    if (lane == 0) {
+      if constexpr (CG == 1) {
+        mbar_arrive(&tempty[acc]);
+      } else {
+        mbar_arrive_cluster(&tempty[acc], 0);
+      }
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
 }
 
 template <int BN, int CG, int EPW>
@@ -563,9 +695,11 @@ __device__ __forceinline__ void epilogue_f32_tma(const Params& p, uint32_t tmem,
 // makes room for the TMA-store boxes.
 template <int EPI, int BN, int S, int CG>
 constexpr int fst() {
-  return EPI == EPI_F32 && BN % 32 == 0 && smem_bytes<BN, S, CG, false, 1>() + 1024 + F32_STAGE_BYTES > 227 * 1024
-             ? S - 1
-             : S;
+  const int extra = EPI == EPI_SGD ? 1024 + SGD_STAGE_BYTES : EPI == EPI_F32 && BN % 32 == 0 ? 1024 + F32_STAGE_BYTES : 0;
+  int s = S;
+  while (s > 2 && smem_bytes<BN, S, CG, false, 1>() - (S - s) * (BM * BK * 2 + (BN / CG) * BK * 2) + extra > 227 * 1024)
+    --s;
+  return s;
 }
 
 template <int AM> constexpr int kernel_threads() { return a_is_gather<AM>() ? 192 + GATHER_THREADS : 320; }
@@ -605,6 +739,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   constexpr bool F32TMA = f32_tma_epi<EPI, BN, STAGES, CG, AM>();
   uint8_t* f32_boxes = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot) + 4 + 1023) & ~uintptr_t(1023));
+  uint64_t* sgd_bars = reinterpret_cast<uint64_t*>(f32_boxes + 8 * SGD_WARP_BYTES);  // EPI_SGD
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.tiles;
@@ -624,6 +759,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         mbar_init(&tempty[a], 4 * EPW * CG);
       }
 
+      if constexpr (EPI == EPI_SGD)
+        for (int w = 0; w < 8; ++w) mbar_init(&sgd_bars[w], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -1026,7 +1163,11 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
     }
   } else {
     const int quad = warp & 3, grp = warp >= 6 ? 1 : 0;
-    if constexpr (F32TMA) {
+    if constexpr (EPI == EPI_SGD) {
+      static_assert(EPW == 2 && BN % 32 == 0, "fused SGD epilogue: 8 epilogue warps, 32-column groups");
+      epilogue_sgd_tma<BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
+                                    f32_boxes + (grp * 4 + quad) * SGD_WARP_BYTES, &sgd_bars[grp * 4 + quad]);
+    } else if constexpr (F32TMA) {
       if (p.out_tma) {
         epilogue_f32_tma<BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
                                       f32_boxes + (grp * 4 + quad) * F32_BOX_BYTES);
@@ -1814,6 +1955,35 @@ int umma_fc_dgrad(int B, int D, int U, const void* w, const void* gy, const pc_m
   return launch_mn<A_TMA_K, EPI_BF16>(p, t, 1, st);
 }
 
+// EPI_SGD views of the parameters {D, U}: fp32 p and v (128B-swizzled 32x32
+// boxes) and the bf16 shadow (64B-swizzled). false: not expressible (or
+// PC_SGD_EPI=0) -> gradient store + separate update pass.
+static bool sgd_epilogue_maps(Params& p, const pc_sgd_fuse* u, int U, int D) {
+  static const int on = [] {
+    const char* e = getenv("PC_SGD_EPI");
+    return e ? atoi(e) : 1;
+  }();
+  if (!on || !get_encode() || !u->p || !u->v || !u->p_lowp || D % 8 ||
+      ((reinterpret_cast<uintptr_t>(u->p) | reinterpret_cast<uintptr_t>(u->v) |
+        reinterpret_cast<uintptr_t>(u->p_lowp)) & 15))
+    return false;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)U, 1};
+  cuuint64_t s32[2] = {(cuuint64_t)D * 4, (cuuint64_t)D * U * 4}, s16[2] = {(cuuint64_t)D * 2, (cuuint64_t)D * U * 2};
+  cuuint32_t box[3] = {32u, 32u, 1u}, estr[3] = {1u, 1u, 1u};
+  auto enc = [&](CUtensorMap* m, void* ptr, CUtensorMapDataType dt, cuuint64_t* str, CUtensorMapSwizzle sw) {
+    return g_encode(m, dt, 3, ptr, dims, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!enc(&p.tma_p, u->p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, s32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !enc(&p.tma_v, u->v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, s32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !enc(&p.tma_pl, u->p_lowp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, s16, CU_TENSOR_MAP_SWIZZLE_64B))
+    return false;
+  p.lr = u->lr;
+  p.mom = u->momentum;
+  p.wd = u->weight_decay;
+  return true;
+}
+
 // Split-K for the weight gradient when the reduction (the batch, or the pixel
 // count of an explicit-im2col convolution) is long and the output tiles few.
 static int fc_wgrad_splits(int B, int D, int U) {
@@ -1842,9 +2012,8 @@ int umma_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* g
   p.kb_per_split = ceil_div(p.num_kb, splits);
   splits = ceil_div(p.num_kb, p.kb_per_split);
   if (splits == 1 || part == nullptr) {
-    // direct epilogue (row-per-thread fp32 stores): a per-element read-modify-write
-    // of p and v there is uncoalesced, so the update runs as a pass over this layer
     p.kb_per_split = p.num_kb;
+    if (upd && sgd_epilogue_maps(p, upd, U, D)) return launch_mn<A_TMA_MN, EPI_SGD>(p, t, 1, st);
     p.out = gw;
     rc = launch_mn<A_TMA_MN, EPI_F32>(p, t, 1, st);
     return rc || !upd ? rc : apply_sgd(gw, (long long)U * D, upd, st);

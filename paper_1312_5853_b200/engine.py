@@ -413,6 +413,9 @@ class ColumnEngine:
         return self._unflatten(self.v32.cpu().numpy())
 
     def grads_host(self, g: torch.Tensor | None = None) -> dict:
+        if g is None and getattr(self, "fuse_sgd", False):
+            raise RuntimeError("weight gradients were consumed by the fused update; "
+                               "set fabric.fuse_sgd = False before setup_workers to read them")
         return self._unflatten((self.g32 if g is None else g).cpu().numpy())
 
     def activation_host(self, i: int, which: str = "out") -> np.ndarray:

@@ -98,10 +98,11 @@ class _Runner:
                     st = fabric._local[wid]
                     eng.load_params(dict.__getitem__(st, "host_params"), dict.get(st, "host_velocity"))
                 self.engines[wid] = eng
-        # single-replica plans may fuse the weight updates into the gradient kernels
-        # (opt-in: fabric.fuse_sgd = True or PC_FUSE_SGD=1; measured no faster on AlexNet,
-        # the FC weight gradients come from a direct epilogue and update in a pass anyway)
-        fuse = d == 1 and getattr(fabric, "fuse_sgd", os.environ.get("PC_FUSE_SGD", "0") == "1")
+        # single-replica plans fuse the weight updates into the gradient kernels (the FC
+        # weight gradient's epilogue updates p/v in place, the split-K reductions of the
+        # convolutions do the same), so those gradients never reach HBM. Off with
+        # fabric.fuse_sgd = False or PC_FUSE_SGD=0 (e.g. to read gradients back).
+        fuse = d == 1 and getattr(fabric, "fuse_sgd", os.environ.get("PC_FUSE_SGD", "1") == "1")
         for eng in self.engines.values():
             eng.configure_fused_sgd(fuse)
         fabric._engines.update(self.engines)

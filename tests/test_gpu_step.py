@@ -243,6 +243,7 @@ def test_alexnet_input_layer_space_to_depth_bf16():
     tr, _ = P.gen_synthetic(4, 1, net.input_shape, seed=2)
     x, y = tr.images, np.array([3, 1, 2, 0])
     fab = P.spawn(1, precision="bf16")
+    fab.fuse_sgd = False   # gradients are read back below
     P.setup_workers(fab, plan, cs, dense, P.SgdState())
     P.hybrid_step(fab, plan, cs, x, y)
     eng = fab._engines[0]
@@ -269,10 +270,11 @@ def test_alexnet_input_layer_space_to_depth_bf16():
 
 
 def test_fused_sgd_epilogue_matches_separate_update():
-    """Opt-in fused momentum-SGD (single-replica plans): the weight-gradient kernels
-    update p/v in place (split-K reduction epilogue, or a per-layer pass) instead of
-    the one multi-tensor SGD launch; parameters after two steps match the unfused
-    run (same fp32 update arithmetic, up to FMA contraction)."""
+    """Fused momentum-SGD (single-replica plans, the default): the weight-gradient
+    kernels update p/v in place (FC: TMA epilogue on the fp32 accumulator; conv:
+    split-K reduction epilogue) instead of the multi-tensor SGD launch; parameters
+    after two steps match the unfused run (same fp32 update arithmetic, up to FMA
+    contraction)."""
     import paper_1312_5853_b200 as P
     net = P.load_network(CONFIGS / "alexnet_small64.net")
     plan = P.ParallelPlan(1, 1)
