@@ -87,6 +87,10 @@ struct alignas(64) Params {
   // Columns x >= Wo are discarded.
   int halo_R, halo_tpi, halo_Wv, halo_lo, halo_bytes;
   int macc_chunks;  // A_IM2COL_MN5: 64-row A chunks with real rows (<= 10)
+  // A_IM2COL_MN with C % 64 != 0 (conv2's 96 channels): M rows walk (tap, m_cp
+  // padded channels); the last 64-channel chunk of a tap is zero-filled by TMA
+  // and the epilogue maps row (tap, c < C) to tap * C + c, dropping c >= C.
+  int m_cp;
   int mt_rows;      // rows per M tile: 128 * CTA-group size * accumulators (set at launch)
   unsigned long long* trace;  // debug: per-CTA per-tile clock64 stamps (tools/trace_gemm.py), normally null
   // EPI_F32 through TMA stores: fp32 view {N, M, split slices} of p.out, box {32, 32, 1}, 128B swizzle
@@ -392,6 +396,11 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
     for (int a = 0; a < MACC; ++a) {  // MACC > 1: accumulator a = rows [128 a, 128 a + 128), TMEM column a * N
     long long m = (long long)tc.m0 + (long long)rank * BM + a * BM + row;
     bool mrow = m < p.M;
+    if (p.m_cp) {
+      const long long tap = m / p.m_cp, c = m - tap * p.m_cp;
+      mrow = mrow && c < p.i2c_C;
+      m = tap * p.i2c_C + c;
+    }
     if constexpr (HALO) {  // TMEM row -> (image, output row, column) of this CTA's halo tile
       const int tile = (tc.m0 + (int)rank * BM) / BM;
       const int hb = tile / p.halo_tpi, yy = row / p.halo_Wv, xx = row - yy * p.halo_Wv;
@@ -708,7 +717,8 @@ template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
 __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __grid_constant__ Params p) {
   constexpr bool GATHER = a_is_gather<AM>();
   constexpr int EPW = GATHER ? 1 : 2;  // epilogue warps per TMEM lane quadrant (warps 0-3, and 6-9 unless gathering)
-  static_assert(!(GATHER && CG == 2), "the cp.async gather producers are single-CTA");
+  // CTA-pair gather: each CTA gathers its own 128 A rows; the peer's gather
+  // completions are relayed to the leader's full barrier by the peer's (idle) MMA warp.
   constexpr bool A_MN = a_is_mn<AM>();
   constexpr bool B_MN = BMODE == B_TMA_MN;
   constexpr int BNC = BN / CG;  // B rows (N) this CTA loads
@@ -751,7 +761,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   if (warp == 4) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
-        mbar_init(&full[s], 1 + (GATHER ? GATHER_THREADS : 0));
+        mbar_init(&full[s], !GATHER ? 1 : leader ? 1 + GATHER_THREADS + (CG - 1) : GATHER_THREADS);
         mbar_init(&empty[s], 1);
       }
       for (int a = 0; a < ACC; ++a) {
@@ -835,7 +845,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         for (int cch = 0; cch < ACH; ++cch) {
           int kk = m0 + 64 * cch;
           if (kk >= p.M) kk = 0;  // rows past M are discarded by the epilogue
-          const int c = kk % p.i2c_C, ij = kk / p.i2c_C;
+          const int cpt = p.m_cp ? p.m_cp : p.i2c_C;  // M rows per tap
+          const int c = kk % cpt, ij = kk / cpt;
           ci[cch] = ij / p.i2c_k;
           cj[cch] = ij - ci[cch] * p.i2c_k;
           cblk[cch] = c / p.i2c_cs;
@@ -950,7 +961,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       int git = 0;
       for (int t = unit; t < total; t += units) {
         const TileCoord tc = tile_coord<CG>(p, t, BN);
-        const int m0 = tc.m0;
+        const int m0 = tc.m0 + (int)rank * BM;
         if constexpr (AM == A_GATHER_FWD || AM == A_GATHER_DGRAD) {
           // K-major rows = pixels; thread owns 16B chunk q of rows rb + 16*r8
           constexpr int RS = GATHER_THREADS / 8;  // row stride between a thread's rows
@@ -1160,6 +1171,21 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           trace_put(p, lt, 11, tr_issue);
         }
       }
+    } else if constexpr (GATHER && CG == 2) {
+      // peer CTA: relay each stage's gather completion to the leader's full barrier
+      if (lane == 0) {
+        int git = 0;
+        for (int t = unit; t < total; t += units) {
+          const TileCoord tc = tile_coord<CG>(p, t, BN);
+          for (int it = 0; it < tc.nkb; ++it, ++git) {
+            const int s = git % STAGES;
+            mbar_wait(&full[s], (git / STAGES) & 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_cluster(&full[s], 0);
+          }
+        }
+      }
+      __syncwarp();
     }
   } else {
     const int quad = warp & 3, grp = warp >= 6 ? 1 : 0;
@@ -1448,6 +1474,12 @@ static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
 }
 template <int AM, int EPI>
 static int launch_mn(const Params& p, Tile t, int splits, cudaStream_t st) {
+  if constexpr (AM == A_GATHER_WGRAD) {
+    if (t.cg == 2) {
+      if (t.bn == 128) return launch<AM, B_TMA_MN, EPI, 128, 8, 2>(p, splits, st);
+      return launch<AM, B_TMA_MN, EPI, 256, 6, 2>(p, splits, st);
+    }
+  }
   if constexpr (!a_is_gather<AM>()) {
     if (t.cg == 2) {
       if (t.bn == 128) return launch<AM, B_TMA_MN, EPI, 128, fst<EPI, 128, 8, 2>(), 2>(p, splits, st);
@@ -1710,10 +1742,27 @@ struct WgradPlan {
   Tile t;
   int splits;
 };
+// Weight gradient of an unblocked input whose channel count is not a multiple
+// of 64 (conv2: 96) by TMA im2col with zero-filled padding channels: a third more
+// MMA rows than the cp.async gather, but the operand arrives at TMA rate.
+static bool wgrad_pad_ok(const pc_conv_geom& g) {
+  static const int on = [] {
+    const char* e = getenv("PC_WGRAD_PAD");
+    return e ? atoi(e) : 1;
+  }();
+  return on && im2col_enabled() && g.C == g.cs && g.C % 64 != 0 && g.C % 8 == 0 && g.C >= 64;
+}
+
 static WgradPlan wgrad_plan(const pc_conv_geom& g) {
-  const long long Kc = (long long)g.k * g.k * g.C, P = (long long)g.B * g.Ho * g.Wo;
-  const bool i2c = im2col_ok(g.cs, g.C, g.cstride);
-  const Tile t = (i2c && cg2_enabled()) ? Tile{g.N <= 128 ? 128 : 256, 2} : Tile{bn_for_mn(g.N), 1};
+  const bool padded = wgrad_pad_ok(g);
+  const long long Kc = (long long)g.k * g.k * (padded ? (g.C + 63) / 64 * 64 : g.C), P = (long long)g.B * g.Ho * g.Wo;
+  const bool i2c = im2col_ok(g.cs, g.C, g.cstride) || padded;
+  static const int gather_cg2 = [] {
+    const char* e = getenv("PC_GATHER_CG2");
+    return e ? atoi(e) : 1;
+  }();
+  const bool pair = cg2_enabled() && (i2c || (gather_cg2 && g.N % 128 == 0));
+  const Tile t = pair ? Tile{g.N <= 128 ? 128 : 256, 2} : Tile{bn_for_mn(g.N), 1};
   const long long tiles = ((Kc + BM * t.cg - 1) / (BM * t.cg)) * ((g.N + t.bn - 1) / t.bn);
   const long long kbs = (P + BK - 1) / BK;
   long long sp = choose_splits(tiles, kbs, t.bn, t.cg);
@@ -1787,7 +1836,12 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   p.gsrc = static_cast<const __nv_bfloat16*>(x);
   p.g = g;
   p.o_ld = Kc;
-  const bool i2c = im2col_ok(g.cs, g.C, g.cstride);
+  const bool padded = wgrad_pad_ok(g);
+  const bool i2c = im2col_ok(g.cs, g.C, g.cstride) || padded;
+  if (padded) {
+    p.m_cp = (g.C + 63) / 64 * 64;
+    p.M = g.k * g.k * p.m_cp;
+  }
   if (i2c) {
     rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, 64, -g.pad, -g.pad,
                          g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
