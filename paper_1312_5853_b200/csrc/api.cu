@@ -144,21 +144,31 @@ __global__ void __launch_bounds__(256) colsum1_v8_k(const T* __restrict__ g, lon
   }
 }
 
-// Pass 2: a CTA per 8 columns, 32 row lanes each (a warp reads 4 rows x 32 B);
-// lane partials are combined in a fixed order (deterministic).
-__global__ void colsum2_k(const float* __restrict__ part, int R, int N, float* __restrict__ out) {
-  __shared__ float sh[32][9];
+// Pass 2: a CTA per 8 columns, 128 row lanes each (a warp reads 4 rows x 32 B);
+// lane partials are combined in a fixed order (deterministic). Wide lanes keep
+// each lane's chain of dependent L2 loads short (R is ~1000-1500 row blocks).
+constexpr int CS2_LANES = 128;
+__global__ void __launch_bounds__(8 * CS2_LANES) colsum2_k(const float* __restrict__ part, int R, int N,
+                                                           float* __restrict__ out) {
+  __shared__ float sh[CS2_LANES][9];
+  __shared__ float sh2[8][9];
   const int cx = threadIdx.x & 7, ry = threadIdx.x >> 3;
   const int c = blockIdx.x * 8 + cx;
   float acc = 0.f;
   if (c < N)
 #pragma unroll 4
-    for (int r = ry; r < R; r += 32) acc += part[(long long)r * N + c];
+    for (int r = ry; r < R; r += CS2_LANES) acc += part[(long long)r * N + c];
   sh[ry][cx] = acc;
   __syncthreads();
+  if (ry < 8) {  // 8 x 8 threads: each sums 16 lanes of one column, then lane ry == 0 combines
+    float t = 0.f;
+    for (int k = 0; k < CS2_LANES / 8; ++k) t += sh[ry * (CS2_LANES / 8) + k][cx];
+    sh2[ry][cx] = t;
+  }
+  __syncthreads();
   if (ry == 0 && c < N) {
-    float t = sh[0][cx];
-    for (int k = 1; k < 32; ++k) t += sh[k][cx];
+    float t = sh2[0][cx];
+    for (int k = 1; k < 8; ++k) t += sh2[k][cx];
     out[c] = t;
   }
 }
@@ -219,7 +229,7 @@ int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, c
     else
       colsum1_k<__nv_bfloat16><<<g1, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(g), P, N, RB, ws);
   }
-  colsum2_k<<<(N + 7) / 8, 256, 0, st>>>(ws, R, N, out);
+  colsum2_k<<<(N + 7) / 8, 8 * CS2_LANES, 0, st>>>(ws, R, N, out);
   count_launches(1);
   PC_CUDA_CHECK_LAUNCH("colsum");
   return PC_OK;

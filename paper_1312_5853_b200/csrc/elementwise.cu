@@ -655,6 +655,67 @@ __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_
   for (int q = 0; q < CS / 8; ++q) Vec8<__nv_bfloat16>::store(out + q * 8, v + q * 8);
 }
 
+// bf16 source, one CTA per output block row (b, Y): for each channel the SS input
+// rows of that block row are one contiguous span of the NCHW plane; it is staged
+// into SMEM with 16-byte loads (aligned down, the tail clamped to the tensor),
+// then each thread assembles one SS x SS block and writes its CS channels as
+// 16-byte stores. Rows/columns outside the image are zero.
+template <int CS, int SS, int CC>
+__global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, int Ws, long long total,
+                                                 const __nv_bfloat16* __restrict__ x,
+                                                 __nv_bfloat16* __restrict__ dst) {
+  extern __shared__ __align__(16) uint8_t s2d_sm[];
+  const int span = SS * W;                    // elements of SS consecutive rows
+  const int slot = ((span + 7) / 8 + 1) * 8;  // per-channel staging (aligned-down start)
+  __nv_bfloat16* lin = reinterpret_cast<__nv_bfloat16*>(s2d_sm);
+  const int b = blockIdx.x / Hs, Y = blockIdx.x - b * Hs;
+  const int iy0 = Y * SS - p;
+  int sh[CC];
+#pragma unroll
+  for (int c = 0; c < CC; ++c) {
+    // rows iy0 .. iy0+SS-1 of plane (b, c), clipped to the image
+    const int r0 = iy0 < 0 ? 0 : iy0, r1 = iy0 + SS > H ? H : iy0 + SS;
+    const long long e0 = (((long long)b * CC + c) * H + iy0) * W;  // may precede the plane (top padding)
+    const long long a0 = e0 & ~7LL;
+    sh[c] = (int)(e0 - a0);
+    if (r1 <= r0) continue;
+    const long long lo = (((long long)b * CC + c) * H + r0) * W, hi = (((long long)b * CC + c) * H + r1) * W;
+    const int k0 = (int)((lo - a0) >> 3), k1 = (int)((hi - a0 + 7) >> 3);
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      const long long e = a0 + 8LL * k;
+      uint4 u;
+      if (e + 8 <= total) {
+        u = __ldg(reinterpret_cast<const uint4*>(x + e));
+      } else {
+        __nv_bfloat16* ub = reinterpret_cast<__nv_bfloat16*>(&u);
+        for (int q = 0; q < 8; ++q) ub[q] = e + q < total ? x[e + q] : __float2bfloat16(0.f);
+      }
+      *reinterpret_cast<uint4*>(lin + c * slot + 8 * k) = u;
+    }
+  }
+  __syncthreads();
+  for (int X = threadIdx.x; X < Ws; X += blockDim.x) {
+    float v[CS];
+#pragma unroll
+    for (int i = 0; i < CS; ++i) v[i] = 0.f;
+#pragma unroll
+    for (int dy = 0; dy < SS; ++dy) {
+      const int iy = iy0 + dy;
+#pragma unroll
+      for (int dx = 0; dx < SS; ++dx) {
+        const int ix = X * SS + dx - p;
+        const bool ok = iy >= 0 && iy < H && ix >= 0 && ix < W;
+#pragma unroll
+        for (int c = 0; c < CC; ++c)
+          v[(dy * SS + dx) * CC + c] = ok ? __bfloat162float(lin[c * slot + sh[c] + dy * W + ix]) : 0.f;
+      }
+    }
+    __nv_bfloat16* out = dst + ((long long)blockIdx.x * Ws + X) * CS;
+#pragma unroll
+    for (int q = 0; q < CS / 8; ++q) Vec8<__nv_bfloat16>::store(out + q * 8, v + q * 8);
+  }
+}
+
 __global__ void mask_f32_k(long long n, const uint8_t* __restrict__ keep, float* __restrict__ buf) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     if (!keep[i]) buf[i] = 0.f;
@@ -897,6 +958,15 @@ extern "C" int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int C
   if (n == 0) return PC_OK;
   const int g = grid_for(n, 256);
   auto* d = static_cast<__nv_bfloat16*>(dst);
+  if (src_prec == PC_BF16 && Cs == 64 && s == 4 && C == 3 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const size_t smem = (size_t)C * (((size_t)s * W + 7) / 8 + 1) * 8 * 2;
+    if (smem <= 48 * 1024) {  // AlexNet conv1: row-staged
+      s2d_rows_k<64, 4, 3><<<B * Hs, 64, smem, S(st)>>>(H, W, p, Hs, Ws, (long long)B * C * H * W,
+                                                         static_cast<const __nv_bfloat16*>(src), d);
+      PC_CUDA_CHECK_LAUNCH("space_to_depth");
+      return PC_OK;
+    }
+  }
   DISPATCH_PREC(src_prec, TS, {
     const TS* x = static_cast<const TS*>(src);
     if (Cs == 64 && s == 4 && C == 3)        // AlexNet conv1 (11x11/s4)

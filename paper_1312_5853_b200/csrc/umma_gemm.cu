@@ -1644,18 +1644,32 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   return launch_kb<A_GATHER_FWD, EPI_BF16>(p, t, 1, st);
 }
 
-__global__ void transpose_w_k(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt, int N, int KK,
-                              int C, int flip) {
-  // wt[c][ij][n] = w[n][ij][c]; flip: wt[c][ij][n] = w[n][KK-1-ij][c] (180-degree filter rotation)
-  long long total = (long long)N * KK * C;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    int n = (int)(t % N);
-    long long r = t / N;
-    int ij = (int)(r % KK);
-    int c = (int)(r / KK);
-    wt[t] = w[((long long)n * KK + (flip ? KK - 1 - ij : ij)) * C + c];
+// wt[c][ij][n] = w[n][ij'][c], ij' = flip ? KK-1-ij : ij (180-degree filter
+// rotation). Per tap a 2-D transpose of [N][C] (row stride KK*C) into [C][N]
+// (row stride KK*N) through a 32x32 SMEM tile: coalesced on both sides.
+__global__ void __launch_bounds__(256) transpose_w_k(const __nv_bfloat16* __restrict__ w,
+                                                     __nv_bfloat16* __restrict__ wt, int N, int KK, int C,
+                                                     int flip) {
+  __shared__ __nv_bfloat16 tile[32][33];
+  const int ij = blockIdx.z, src_ij = flip ? KK - 1 - ij : ij;
+  const int c0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int n = n0 + r, c = c0 + tx;
+    if (n < N && c < C) tile[r][tx] = w[((long long)n * KK + src_ij) * C + c];
   }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int c = c0 + r, n = n0 + tx;
+    if (n < N && c < C) wt[((long long)c * KK + ij) * N + n] = tile[tx][r];
+  }
+}
+
+static void transpose_w(const void* w, __nv_bfloat16* wt, int N, int KK, int C, int flip, cudaStream_t st) {
+  const dim3 grid((C + 31) / 32, (N + 31) / 32, KK);
+  transpose_w_k<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, N, KK, C, flip);
 }
 
 size_t umma_conv_extra_ws(const pc_conv_geom& g, int prec) {
@@ -1674,19 +1688,16 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
   // the transposed weights live at the END of the workspace (wgrad partials use the front)
   __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(
       (reinterpret_cast<uintptr_t>(ws) + ws_bytes - need) & ~uintptr_t(127));
-  long long total = (long long)g.N * KK * g.C;
-  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
   const bool rot = g.stride == 1 && g.H + 2 * g.pad - g.k + 1 == g.Ho;  // dgrad = conv of gy with the rotated filter
   const bool i2c = rot && im2col_ok(g.N, g.N, 0);
   const bool halo_ok = rot && halo_wanted(g.C, g.k);
-  transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C,
-                                        (i2c || halo_ok) ? 1 : 0);
+  transpose_w(w, wt, g.N, KK, g.C, (i2c || halo_ok) ? 1 : 0, st);
   PC_CUDA_CHECK_LAUNCH("transpose_w");
   int M = g.B * g.H * g.W, K = KK * g.N;
   Params p = base_params(M, g.C, K);
   const bool halo = halo_ok && setup_halo(p, gy, g.B, g.Ho, g.Wo, g.N, g.k, g.pad - (g.k - 1), g.H, g.W);
   if (halo_ok && !halo && !i2c) {  // rotated weights were written for a path that does not apply
-    transpose_w_k<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), wt, g.N, KK, g.C, 0);
+    transpose_w(w, wt, g.N, KK, g.C, 0, st);
     PC_CUDA_CHECK_LAUNCH("transpose_w");
   }
   const Tile t = pick_k(p.M, g.C, i2c || halo);

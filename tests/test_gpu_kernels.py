@@ -280,3 +280,33 @@ def test_maxpool_k3s2_vectorised_backward(shape, prec):
     gx = K.maxpool_backward(x, 3, 2, gy, arg)
     rgx = O.maxpool_backward(x.shape, 3, 2, gy, rarg)
     assert rel(gx, rgx) < (1e-6 if prec == "fp32" else BF16_OUT_TOL)
+
+
+@pytest.mark.parametrize("case", [(3, 3, 227, 227, 4, 0), (2, 3, 227, 227, 4, 2), (2, 3, 35, 29, 4, 1),
+                                  (2, 3, 64, 64, 2, 1)])
+@pytest.mark.parametrize("src", ["bf16", "fp32"])
+def test_space_to_depth_bit_exact(case, src):
+    """pc_space_to_depth (input layer regrouping, SURVEY §8 a): dst[b][Y][X][(dy*s+dx)*C+c] =
+    x[b][c][Y*s+dy-p][X*s+dx-p], zero outside the image and in the padding channels;
+    bit-exact for both source precisions (the bf16 AlexNet case takes the row-staged kernel)."""
+    import ctypes
+    import torch
+    from paper_1312_5853_b200._lib import lib, PC_BF16, PC_FP32
+    b, c, h, w, s, p = case
+    rs = np.random.RandomState(5)
+    x = torch.as_tensor(rs.randn(b, c, h, w).astype(np.float32))
+    if src == "bf16":
+        x = x.bfloat16()
+    hs, ws = (h + 2 * p + s - 1) // s, (w + 2 * p + s - 1) // s
+    xd = x.cuda()
+    out = torch.full((b, hs, ws, 64), 7.0, dtype=torch.bfloat16, device="cuda")
+    lib().call("pc_space_to_depth", b, c, h, w, s, p, 64, xd.data_ptr(), PC_BF16 if src == "bf16" else PC_FP32,
+               out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    got = out.float().cpu().numpy()
+    xp = np.zeros((b, c, hs * s, ws * s), np.float32)
+    xf = x.float().numpy()
+    xp[:, :, p:p + h, p:p + w] = xf[:, :, : hs * s - p, : ws * s - p]
+    want = np.zeros((b, hs, ws, 64), np.float32)
+    blk = xp.reshape(b, c, hs, s, ws, s).transpose(0, 2, 4, 3, 5, 1).reshape(b, hs, ws, s * s * c)
+    want[..., : s * s * c] = torch.as_tensor(blk).bfloat16().float().numpy()
+    assert np.array_equal(got, want)
