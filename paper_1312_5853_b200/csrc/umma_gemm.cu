@@ -44,7 +44,12 @@ enum AMode {
   // weight gradient with M <= 640 and N <= 128 (the input layer: 9 taps x 64
   // channels x 96 filters): one CTA holds MACC = 5 accumulators (all of M) x N in
   // TMEM, so each split-K slice streams the upstream gradient (B) exactly once
-  A_IM2COL_MN5 = 8
+  A_IM2COL_MN5 = 8,
+  // halo A with the whole B operand resident in shared memory (loaded once per
+  // CTA): a narrow layer whose filters fit (the space-to-depth input layer: 9 taps
+  // x 64 channels x 96 filters = 54 KB per SM of a CTA pair); stages carry only
+  // the input window
+  A_HALO_KR = 9
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
@@ -320,6 +325,8 @@ constexpr int tmem_cols() {
 // Halo stage: the input window for (channel chunk, filter column j) (<= 256 rows of
 // 64 channels) plus the B tiles of that column's k filter rows (k <= HALO_KMAX).
 constexpr int HALO_SLOT_BYTES = 256 * 128, HALO_KMAX = 5;
+// A_HALO_KR: window slots of <= 224 rows and <= 56 KB of resident B tiles
+constexpr int HALO_R_SLOT_BYTES = 224 * 128, RES_B_BYTES = 56 * 1024;
 template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM <= A_GATHER_WGRAD; }
 // cp.async gather producers (warps 6..): 8 warps, each thread 16 B per row for
 // 1024 / GATHER_THREADS rows of the 128 x 64 stage.
@@ -375,6 +382,20 @@ __device__ __forceinline__ TileCoord tile_coord(const Params& p, int t, int bn) 
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Accumulator-empty arrivals: relaxed — the MMA warp needs only the TMEM reads
+// ordered (tcgen05.fence::before_thread_sync), not this thread's outstanding
+// global stores, which a release arrive would wait for.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
 }
 
 // Epilogue: drain one accumulator (this CTA's 128 rows x BN fp32 in TMEM) per
@@ -485,9 +506,9 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
     if (lane == 0) {
       if constexpr (CG == 1) {
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_relaxed(&tempty[acc]);
       } else {
-        mbar_arrive_cluster(&tempty[acc], 0);
+        mbar_arrive_cluster_relaxed(&tempty[acc], 0);
       }
     }
   }
@@ -503,7 +524,8 @@ constexpr int F32_BOX_BYTES = 32 * 128;
 constexpr int F32_STAGE_BYTES = 8 * F32_BOX_BYTES;  // one box per epilogue warp
 template <int EPI, int BN, int STAGES, int CG, int AM>
 constexpr bool f32_tma_epi() {
-  return EPI == EPI_F32 && !a_is_gather<AM>() && macc_of<AM>() == 1 && AM != A_HALO_K && BN % 32 == 0 &&
+  return EPI == EPI_F32 && !a_is_gather<AM>() && macc_of<AM>() == 1 && AM != A_HALO_K && AM != A_HALO_KR &&
+         BN % 32 == 0 &&
          smem_bytes<BN, STAGES, CG, false, 1>() + 1024 + F32_STAGE_BYTES <= 227 * 1024;
 }
 // EPI_SGD boxes per epilogue warp: p (fp32 32x32, 128B swizzle), v (same), bf16
@@ -512,6 +534,8 @@ constexpr int SGD_WARP_BYTES = 4096 + 4096 + 2048;
 constexpr int SGD_STAGE_BYTES = 8 * SGD_WARP_BYTES + 8 * 8;
 template <int EPI, int BN, int STAGES, int CG, int AM>
 constexpr int kernel_smem() {
+  if constexpr (AM == A_HALO_KR)
+    return 1024 + STAGES * HALO_R_SLOT_BYTES + RES_B_BYTES + (2 * STAGES + 5) * 8 + 16 + 1024 + 4 * 64 * BN;
   return smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>()>() +
          (f32_tma_epi<EPI, BN, STAGES, CG, AM>() ? 1024 + F32_STAGE_BYTES : 0) +
          (EPI == EPI_SGD ? 1024 + SGD_STAGE_BYTES : 0);
@@ -630,9 +654,9 @@ __device__ __forceinline__ void epilogue_sgd_tma(const Params& p, uint32_t tmem,
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
     if (lane == 0) {
       if constexpr (CG == 1) {
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_relaxed(&tempty[acc]);
       } else {
-        mbar_arrive_cluster(&tempty[acc], 0);
+        mbar_arrive_cluster_relaxed(&tempty[acc], 0);
       }
     }
   }
@@ -690,14 +714,108 @@ __device__ __forceinline__ void epilogue_f32_tma(const Params& p, uint32_t tmem,
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
     if (lane == 0) {
       if constexpr (CG == 1) {
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_relaxed(&tempty[acc]);
       } else {
-        mbar_arrive_cluster(&tempty[acc], 0);
+        mbar_arrive_cluster_relaxed(&tempty[acc], 0);
       }
     }
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncwarp();
+}
+
+// bf16 epilogue for A_HALO_KR with coalesced stores: the two warps of a TMEM lane
+// quadrant each drain one half of the BN columns of their 32 rows (bias, ReLU)
+// into a shared [32][BN] bf16 box (16-byte writes); after a
+// 64-thread named barrier each warp stores two 8-row groups, lanes covering
+// consecutive 16-byte chunks, so every warp store is 512 contiguous bytes. An
+// 8-row group never straddles an output row (Wv % 8 == 0) and is contiguous in
+// the NHWC output; virtual columns x >= Wo are skipped. The accumulator is
+// released as soon as it is read. (Each lane storing its own 192-byte row kept
+// this 96-column layer epilogue-bound.)
+template <int BN, int CG>
+__device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
+                                                   int unit, int units, uint32_t rank, int quad, int grp, int lane,
+                                                   uint8_t* box) {
+  constexpr int TCOLS = tmem_cols<BN>();
+  constexpr int ACC = acc_count<BN>();
+  constexpr int HALF = BN / 2, ROWB = BN * 2, CH = HALF * 2 / 16, RCH = ROWB / 16;
+  static_assert(HALF % 16 == 0, "16-column TMEM loads");
+  const uint32_t sbox = smem_u32(box);
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+  int lt = 0;
+  for (int t = unit; t < p.tiles; t += units, ++lt) {
+    const TileCoord tc = tile_coord<CG>(p, t, BN);
+    const int acc = lt % ACC;
+    mbar_wait(&tfull[acc], (lt / ACC) & 1);
+    tc_fence_after();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
+    const uint32_t tbase = tmem + acc * TCOLS + grp * HALF + ((uint32_t)(quad * 32) << 16);
+    float v[HALF];
+#pragma unroll
+    for (int c = 0; c < HALF / 16; ++c) tmem_ld16(tbase + 16 * c, v + 16 * c);
+    tc_fence_before();
+    __syncwarp();
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
+    if (lane == 0) {
+      if constexpr (CG == 1) {
+        mbar_arrive_relaxed(&tempty[acc]);
+      } else {
+        mbar_arrive_cluster_relaxed(&tempty[acc], 0);
+      }
+    }
+    const int n0 = tc.n0 + grp * HALF;
+#pragma unroll
+    for (int q = 0; q < HALF; ++q) {
+      float val = v[q];
+      if (p.bias) val += __ldg(p.bias + n0 + q);
+      if (p.relu) val = val > 0.f ? val : 0.f;
+      v[q] = val;
+    }
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 12);
+    // the previous tile's stores have read the box (64 threads: this quadrant's two warps)
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 13);
+    #pragma unroll
+    for (int s = 0; s < CH; ++s) {
+      const int j = s;  // (a lane-rotated order would index v[] dynamically: local memory)
+      uint32_t w[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * j + 2 * h], v[8 * j + 2 * h + 1]);
+        w[h] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sbox + lane * ROWB + grp * HALF * 2 + 16 * j),
+                   "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                   : "memory");
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 14);
+    const int tile = (tc.m0 + (int)rank * BM) / BM;
+    const int hb = tile / p.halo_tpi, y0 = (tile - hb * p.halo_tpi) * p.halo_R;
+#pragma unroll
+    for (int g8 = 0; g8 < 2; ++g8) {
+      const int r0 = 16 * grp + 8 * g8;  // first of this group's 8 rows within the quadrant
+      const int row = quad * 32 + r0, yy = row / p.halo_Wv, xx = row - yy * p.halo_Wv, y = y0 + yy;
+      if (yy >= p.halo_R || y >= p.i2c_Ho) continue;
+      const int nrow = min(8, p.i2c_Wo - xx);
+      __nv_bfloat16* dst = out + (((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx) * BN;
+#pragma unroll
+      for (int i = 0; i < (8 * RCH + 31) / 32; ++i) {
+        const int c = i * 32 + lane, r = c / RCH, part = c - r * RCH;
+        if (r < nrow) {
+          uint4 u;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                       : "r"(sbox + (r0 + r) * ROWB + 16 * part)
+                       : "memory");
+          *reinterpret_cast<uint4*>(dst + r * BN + part * 8) = u;
+        }
+      }
+    }
+    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 15);
+    
+  }
 }
 
 // Stage count for a (BN, CG) ring: one stage fewer for an fp32 output when that
@@ -734,19 +852,23 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr bool HALO = AM == A_HALO_K;
+  constexpr bool BRES = AM == A_HALO_KR;
+  constexpr bool HALO = AM == A_HALO_K || BRES;
   // stage s: A at sA + s * A_STRIDE, B at sB + s * B_STRIDE (a halo stage holds its
-  // window and its k B tiles contiguously)
-  constexpr int A_STRIDE = HALO ? halo_stage_bytes<BN, CG>() : A_STAGE;
-  constexpr int B_STRIDE = HALO ? halo_stage_bytes<BN, CG>() : B_STAGE_BYTES;
+  // window and its k B tiles contiguously; BRES: stages hold windows only, the B
+  // tiles of every (k-block, filter row) sit after the ring)
+  constexpr int A_STRIDE = BRES ? HALO_R_SLOT_BYTES : HALO ? halo_stage_bytes<BN, CG>() : A_STAGE;
+  constexpr int B_STRIDE = BRES ? 0 : HALO ? halo_stage_bytes<BN, CG>() : B_STAGE_BYTES;
   uint8_t* sA = smem;
-  uint8_t* sB = HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (HALO ? halo_stage_bytes<BN, CG>()
-                                                                       : A_STAGE + B_STAGE_BYTES));
+  uint8_t* sB = BRES ? smem + STAGES * HALO_R_SLOT_BYTES : HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(BRES ? sB + RES_B_BYTES
+                                                    : smem + STAGES * (HALO ? halo_stage_bytes<BN, CG>()
+                                                                            : A_STAGE + B_STAGE_BYTES));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [ACC]
   uint64_t* tempty = tfull + 2;      // [ACC]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres = tempty + 2;       // BRES: resident B loaded
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2 + (BRES ? 1 : 0));
   constexpr bool F32TMA = f32_tma_epi<EPI, BN, STAGES, CG, AM>();
   uint8_t* f32_boxes = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot) + 4 + 1023) & ~uintptr_t(1023));
   uint64_t* sgd_bars = reinterpret_cast<uint64_t*>(f32_boxes + 8 * SGD_WARP_BYTES);  // EPI_SGD
@@ -771,6 +893,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
 
       if constexpr (EPI == EPI_SGD)
         for (int w = 0; w < 8; ++w) mbar_init(&sgd_bars[w], 1);
+      if constexpr (BRES) mbar_init(bres, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -808,6 +931,21 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
     // lane issues. im2col coordinates advance incrementally: the divisions run
     // once per tile, not once per k-block.
     int git = 0, plt = 0;
+    if constexpr (BRES) {
+      // resident B: tile r = kb * k + i (k-block kb = (chunk, filter column j), filter
+      // row i) holds this CTA's BNC filters at K offset ((i k + j) C + 64 chunk)
+      if (elect_one()) {
+        const int nt = p.num_kb * p.i2c_k;
+        if (leader) mbar_arrive_expect_tx(bres, CG * nt * B_STAGE_BYTES);
+        for (int r = 0; r < nt; ++r) {
+          const int kb = r / p.i2c_k, i = r - kb * p.i2c_k;
+          const int ch = kb / p.i2c_k, j = kb - ch * p.i2c_k;
+          tma_load_3d<CG>(&p.tma_b, bres, smem_u32(sB + r * B_STAGE_BYTES), (i * p.i2c_k + j) * p.i2c_C + ch * BK,
+                          (int)rank * BNC, 0);
+        }
+      }
+      __syncwarp();
+    }
     for (int t = unit; t < total; t += units, ++plt) {
       if (lane == 0) trace_stamp(p, plt, 0);
       long long tr_wait = 0, tr_issue = 0;
@@ -867,12 +1005,13 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         const int kb = tc.kb_begin + it;
         if (HALO && elect_one()) {
           // the window for (chunk, column j) and the B tiles of taps (0..k-1, j)
-          if (leader) mbar_arrive_expect_tx(&full[s], CG * (p.halo_bytes + p.i2c_k * B_STAGE_BYTES));
+          if (leader) mbar_arrive_expect_tx(&full[s], CG * (p.halo_bytes + (BRES ? 0 : p.i2c_k * B_STAGE_BYTES)));
           const uint32_t st0 = smem_u32(sA + s * A_STRIDE);
           tma_load_4d<CG>(&p.tma_a, &full[s], st0, kc, p.halo_lo + kj, hy0 + p.halo_lo, hb);
-          for (int i = 0; i < p.i2c_k; ++i)
-            tma_load_3d<CG>(&p.tma_b, &full[s], st0 + HALO_SLOT_BYTES + i * B_STAGE_BYTES,
-                            (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
+          if constexpr (!BRES)
+            for (int i = 0; i < p.i2c_k; ++i)
+              tma_load_3d<CG>(&p.tma_b, &full[s], st0 + HALO_SLOT_BYTES + i * B_STAGE_BYTES,
+                              (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
         } else if (!HALO && elect_one()) {
           if (leader)
             mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + (GATHER ? 0 : MACC > 1 ? p.macc_chunks * 64 * BK * 2
@@ -1088,6 +1227,10 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       const uint64_t b0 = B_MN ? make_desc(smem_u32(sB), 64 * BK * 2, 1024) : make_desc(smem_u32(sB), 16, 1024);
       constexpr uint32_t A_KSTEP = (A_MN ? 2048 : 32) >> 4, B_KSTEP = (B_MN ? 2048 : 32) >> 4;
       int git = 0, lt = 0;
+      if constexpr (BRES) {
+        mbar_wait(bres, 0);
+        tc_fence_after();
+      }
       for (int t = unit; t < total; t += units, ++lt) {
         const TileCoord tc = tile_coord<CG>(p, t, BN);
         const int acc = lt % ACC;
@@ -1124,7 +1267,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (elect_one()) {
             const uint64_t ad = a0 + (uint64_t)((s * A_STRIDE) >> 4);
-            const uint64_t bd = b0 + (uint64_t)((s * B_STRIDE) >> 4);
+            const uint64_t bd = BRES ? b0 + (uint64_t)(((tc.kb_begin + it) * p.i2c_k * B_STAGE_BYTES) >> 4)
+                                     : b0 + (uint64_t)((s * B_STRIDE) >> 4);
             if constexpr (HALO) {
               // filter row i: the window shifted by i * Wv rows (multiple of 8), B tile i
               const int k = p.i2c_k;
@@ -1189,7 +1333,10 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
     }
   } else {
     const int quad = warp & 3, grp = warp >= 6 ? 1 : 0;
-    if constexpr (EPI == EPI_SGD) {
+    if constexpr (BRES && EPI == EPI_BF16) {
+      epilogue_bf16_halo<BN, CG>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
+                                 f32_boxes + quad * (64 * BN));
+    } else if constexpr (EPI == EPI_SGD) {
       static_assert(EPW == 2 && BN % 32 == 0, "fused SGD epilogue: 8 epilogue warps, 32-column groups");
       epilogue_sgd_tma<BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
                                     f32_boxes + (grp * 4 + quad) * SGD_WARP_BYTES, &sgd_bars[grp * 4 + quad]);
@@ -1443,7 +1590,10 @@ static Tile pick_mn(int M, int N, bool pair_ok, int splits = 1) {
 
 template <int AM, int EPI>
 static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
-  if constexpr (AM == A_HALO_K) {  // stages of (window + k B tiles); N <= 128
+  if constexpr (AM == A_HALO_KR) {  // window stages + resident B (CTA pair, N <= 96)
+    if (t.cg == 2 && t.bn <= 96) return launch<AM, B_TMA_K, EPI, 96, 5, 2>(p, splits, st);
+    PC_REQUIRE(false, PC_ESHAPE, "resident-B halo: CTA pair with N <= 96 only");
+  } else if constexpr (AM == A_HALO_K) {  // stages of (window + k B tiles); N <= 128
     if (t.cg == 2) {
       if (t.bn <= 64) return launch<AM, B_TMA_K, EPI, 64, 4, 2>(p, splits, st);
       if (t.bn <= 96) return launch<AM, B_TMA_K, EPI, 96, 3, 2>(p, splits, st);
@@ -1611,6 +1761,21 @@ static bool setup_halo(Params& p, const void* in, int B, int Hi, int Wi, int Ci,
   return true;
 }
 
+// Resident-B halo (A_HALO_KR): a CTA pair with N <= 96 whose filters fit in
+// RES_B_BYTES per SM and whose windows fit a HALO_R_SLOT_BYTES slot — the
+// space-to-depth input layer (9 taps x 64 channels x 96 filters). PC_HALO_RES=0 off.
+static bool halo_res_fits(const Params& p, int N) {
+  static const int on = [] {
+    const char* e = getenv("PC_HALO_RES");
+    return e ? atoi(e) : 1;
+  }();
+  if (!on || !cg2_enabled() || N != 96) return false;
+  const long long res = (long long)p.num_kb * p.i2c_k * 48 * BK * 2;
+  const long long pair_tiles = (p.M + 2 * BM - 1) / (2 * BM);
+  return res <= RES_B_BYTES && (long long)(p.halo_R + p.i2c_k - 1) * p.halo_Wv * 128 <= HALO_R_SLOT_BYTES &&
+         pair_tiles >= 74;
+}
+
 int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const float* bias, void* y,
                       int flags, cudaStream_t st) {
   if (!conv_tc_shape(g)) {
@@ -1619,10 +1784,18 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   }
   int M = g.B * g.Ho * g.Wo, K = g.k * g.k * g.C;
   Params p = base_params(M, g.N, K);
-  const bool halo = g.stride == 1 && g.C == g.cs && halo_wanted(g.N, g.k) &&
-                    setup_halo(p, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo);
+  bool halo = g.stride == 1 && g.C == g.cs && halo_wanted(g.N, g.k) &&
+             setup_halo(p, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo);
+  bool res = false;
+  if (!halo && g.stride == 1 && g.C == g.cs && g.N <= 96) {
+    Params q = p;
+    if (setup_halo(q, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo) && halo_res_fits(q, g.N)) {
+      p = q;
+      halo = res = true;
+    }
+  }
   const bool i2c = !halo && im2col_k_ok(g.cs, g.C, g.cstride);
-  const Tile t = pick_k(p.M, g.N, i2c || halo);
+  const Tile t = res ? Tile{96, 2} : pick_k(p.M, g.N, i2c || halo);
   int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, t.bn / t.cg);
   if (rc) return rc;
   p.b_cb = 0;
@@ -1632,6 +1805,19 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   p.o_ld = g.N;
   p.bias = bias;
   p.relu = (flags & PC_RELU) != 0;
+  if (res) {
+    // output view {N, Wo, B*Ho}, box {N/2, 8 rows, 1} (epilogue_bf16_halo_tma)
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.Wo, (cuuint64_t)g.B * g.Ho};
+    cuuint64_t strides[2] = {(cuuint64_t)g.N * 2, (cuuint64_t)g.Wo * g.N * 2};
+    cuuint32_t box[3] = {(cuuint32_t)(t.bn / 2), 8u, 1u}, estr[3] = {1u, 1u, 1u};
+    PC_REQUIRE(g.N == t.bn && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+                   g_encode(&p.tma_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, y, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS,
+               PC_ECUDA, "resident-B halo: output tensor map");
+    p.out_tma = 1;
+    return launch_kb<A_HALO_KR, EPI_BF16>(p, t, 1, st);
+  }
   if (halo) return launch_kb<A_HALO_K, EPI_BF16>(p, t, 1, st);
   if (i2c) {
     rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, BM, -g.pad, -g.pad,

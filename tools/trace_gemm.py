@@ -63,3 +63,7 @@ print("median per tile: producer empty-wait %.0f tma-issue %.0f | mma full-wait 
     med(allr[:, 8] + base_fix(allr)), med(allr[:, 9]), med(allr[:, 10]), med(allr[:, 11])))
 tot = [r[-1, 6] for r in rows]
 print("CTA span cycles: median %.0f max %.0f; tiles per CTA %s" % (np.median(tot), np.max(tot), sorted(set(len(r) for r in rows))))
+ext = allr[:, 12:16]
+if (ext > 0).any():
+    d = [med(allr[:, 12] - allr[:, 6])] + [med(allr[:, 12 + i] - allr[:, 11 + i]) for i in range(1, 4)]
+    print("epilogue tail (slots 12-15, deltas from the release): %s" % " | ".join("%.0f" % x for x in d))
