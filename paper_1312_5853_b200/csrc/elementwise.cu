@@ -98,21 +98,18 @@ __global__ void maxpool_fwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int 
   const int ox = (int)(pix - row * Wo);
   const int b = (int)(row / (unsigned)Ho);
   const int oy = (int)(row - (unsigned)b * Ho);
-  uint4 r[9];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const __nv_bfloat16* xr = x + (((long long)b * H + oy * 2 + i) * W + ox * 2) * C + c0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) r[i * 3 + j] = __ldg(reinterpret_cast<const uint4*>(xr + (long long)j * C));
-  }
   // keys: (bf16 bits << 16) | (15 - window index): one 32-bit max per channel and
-  // element gives the largest value and, among equal values, the first index
+  // element gives the largest value and, among equal values, the first index.
+  // The 9 loads are consumed as they arrive (no window kept in registers: the
+  // rare fallback reloads it), so the kernel runs at high occupancy.
   uint32_t sign = 0, mk[8];
 #pragma unroll
   for (int v = 0; v < 8; ++v) mk[v] = 0u;
+  const __nv_bfloat16* x0 = x + (((long long)b * H + oy * 2) * W + ox * 2) * C + c0;
 #pragma unroll
   for (int e = 0; e < 9; ++e) {
-    const uint32_t w[4] = {r[e].x, r[e].y, r[e].z, r[e].w};
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(x0 + ((long long)(e / 3) * W + (e % 3)) * C));
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       sign |= w[q];
@@ -139,6 +136,9 @@ __global__ void maxpool_fwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int 
     *reinterpret_cast<uint2*>(arg + o) = packed;
     return;
   }
+  uint4 r[9];
+#pragma unroll 1
+  for (int e = 0; e < 9; ++e) r[e] = __ldg(reinterpret_cast<const uint4*>(x0 + ((long long)(e / 3) * W + (e % 3)) * C));
   float best[8];
   int bi[8];
   unsigned short bits[8];  // the winner's original bits (NaN payload kept)

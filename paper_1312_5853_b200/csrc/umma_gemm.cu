@@ -340,10 +340,14 @@ template <int AM> constexpr int macc_of() { return AM == A_IM2COL_MN5 ? 5 : 1; }
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
 template <int BN, int CG>
 constexpr int halo_stage_bytes() { return HALO_SLOT_BYTES + HALO_KMAX * (BN / CG) * BK * 2; }
-template <int BN, int STAGES, int CG, bool HALO = false, int MACC = 1>
+// B rows a CTA stages per k-block: an MN-major B is loaded in whole 64-column
+// chunks (a pair tile of N = 192 stages 128 columns per CTA and the MMA reads 96)
+template <int BN, int CG, bool BMN>
+constexpr int b_rows() { return BMN ? (BN / CG + 63) / 64 * 64 : BN / CG; }
+template <int BN, int STAGES, int CG, bool HALO = false, int MACC = 1, bool BMN = false>
 constexpr int smem_bytes() {
   return 1024 /*align slack*/ + (HALO ? STAGES * halo_stage_bytes<BN, CG>()
-                                      : STAGES * (MACC * A_STAGE_BYTES + (BN / CG) * BK * 2)) +
+                                      : STAGES * (MACC * A_STAGE_BYTES + b_rows<BN, CG, BMN>() * BK * 2)) +
          (2 * STAGES + 4) * 8 + 16;
 }
 
@@ -522,22 +526,22 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
 // reaches ~2 TB/s on the 151 MB fc6 weight gradient.
 constexpr int F32_BOX_BYTES = 32 * 128;
 constexpr int F32_STAGE_BYTES = 8 * F32_BOX_BYTES;  // one box per epilogue warp
-template <int EPI, int BN, int STAGES, int CG, int AM>
+template <int EPI, int BN, int STAGES, int CG, int AM, bool BMN = false>
 constexpr bool f32_tma_epi() {
   return EPI == EPI_F32 && !a_is_gather<AM>() && macc_of<AM>() == 1 && AM != A_HALO_K && AM != A_HALO_KR &&
          BN % 32 == 0 &&
-         smem_bytes<BN, STAGES, CG, false, 1>() + 1024 + F32_STAGE_BYTES <= 227 * 1024;
+         smem_bytes<BN, STAGES, CG, false, 1, BMN>() + 1024 + F32_STAGE_BYTES <= 227 * 1024;
 }
 // EPI_SGD boxes per epilogue warp: p (fp32 32x32, 128B swizzle), v (same), bf16
 // shadow (32x32, 64B swizzle); then one transaction barrier per warp.
 constexpr int SGD_WARP_BYTES = 4096 + 4096 + 2048;
 constexpr int SGD_STAGE_BYTES = 8 * SGD_WARP_BYTES + 8 * 8;
-template <int EPI, int BN, int STAGES, int CG, int AM>
+template <int EPI, int BN, int STAGES, int CG, int AM, bool BMN = false>
 constexpr int kernel_smem() {
   if constexpr (AM == A_HALO_KR)
     return 1024 + STAGES * HALO_R_SLOT_BYTES + RES_B_BYTES + (2 * STAGES + 5) * 8 + 16 + 1024 + 4 * 64 * BN;
-  return smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>()>() +
-         (f32_tma_epi<EPI, BN, STAGES, CG, AM>() ? 1024 + F32_STAGE_BYTES : 0) +
+  return smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>(), BMN>() +
+         (f32_tma_epi<EPI, BN, STAGES, CG, AM, BMN>() ? 1024 + F32_STAGE_BYTES : 0) +
          (EPI == EPI_SGD ? 1024 + SGD_STAGE_BYTES : 0);
 }
 
@@ -820,11 +824,12 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
 
 // Stage count for a (BN, CG) ring: one stage fewer for an fp32 output when that
 // makes room for the TMA-store boxes.
-template <int EPI, int BN, int S, int CG>
+template <int EPI, int BN, int S, int CG, bool BMN = false>
 constexpr int fst() {
   const int extra = EPI == EPI_SGD ? 1024 + SGD_STAGE_BYTES : EPI == EPI_F32 && BN % 32 == 0 ? 1024 + F32_STAGE_BYTES : 0;
   int s = S;
-  while (s > 2 && smem_bytes<BN, S, CG, false, 1>() - (S - s) * (BM * BK * 2 + (BN / CG) * BK * 2) + extra > 227 * 1024)
+  while (s > 2 && smem_bytes<BN, S, CG, false, 1, BMN>() - (S - s) * (BM * BK * 2 + b_rows<BN, CG, BMN>() * BK * 2) +
+                         extra > 227 * 1024)
     --s;
   return s;
 }
@@ -840,8 +845,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   constexpr bool A_MN = a_is_mn<AM>();
   constexpr bool B_MN = BMODE == B_TMA_MN;
   constexpr int BNC = BN / CG;  // B rows (N) this CTA loads
-  static_assert(!B_MN || BNC % 64 == 0, "MN-major B is loaded in 64-column chunks");
-  constexpr int B_STAGE_BYTES = BNC * BK * 2;
+  static_assert(!B_MN || BNC % 32 == 0, "MN-major B is loaded in 64-column chunks");
+  constexpr int B_STAGE_BYTES = b_rows<BN, CG, B_MN>() * BK * 2;
   constexpr int MACC = macc_of<AM>();
   // MACC > 1: MMA N = p.N (<= BN, the B load width), accumulator a at TMEM column a * p.N
   const uint32_t IDESC = MACC > 1 ? ((make_idesc<BN, A_MN, B_MN, CG>() & ~(0x3Fu << 17)) | ((uint32_t)(p.N >> 3) << 17))
@@ -869,7 +874,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   uint64_t* tempty = tfull + 2;      // [ACC]
   uint64_t* bres = tempty + 2;       // BRES: resident B loaded
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2 + (BRES ? 1 : 0));
-  constexpr bool F32TMA = f32_tma_epi<EPI, BN, STAGES, CG, AM>();
+  constexpr bool F32TMA = f32_tma_epi<EPI, BN, STAGES, CG, AM, B_MN>();
   uint8_t* f32_boxes = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot) + 4 + 1023) & ~uintptr_t(1023));
   uint64_t* sgd_bars = reinterpret_cast<uint64_t*>(f32_boxes + 8 * SGD_WARP_BYTES);  // EPI_SGD
 
@@ -1022,7 +1027,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
               tma_load_4d<CG>(&p.tma_b, &full[s], dB, 0, kb * BK, blk_off(n0, p.b_cb) >> 6, blk_idx(n0, p.b_cb));
             } else {
 #pragma unroll
-              for (int c = 0; c < BNC / 64; ++c) {
+              for (int c = 0; c < (BNC + 63) / 64; ++c) {
                 int n = n0 + 64 * c;
                 tma_load_3d<CG>(&p.tma_b, &full[s], dB + c * (64 * BK * 2), blk_off(n, p.b_cb), kb * BK,
                                 blk_idx(n, p.b_cb));
@@ -1486,7 +1491,7 @@ static int f32_out_map(CUtensorMap* map, const Params& p, int splits) {
 template <int AM, int BMODE, int EPI, int BN, int STAGES, int CG>
 static int launch(const Params& p, int splits, cudaStream_t st) {
   auto kern = umma_gemm_k<AM, BMODE, EPI, BN, STAGES, CG>;
-  constexpr int smem = kernel_smem<EPI, BN, STAGES, CG, AM>();
+  constexpr int smem = kernel_smem<EPI, BN, STAGES, CG, AM, BMODE == B_TMA_MN>();
   static_assert(smem <= 227 * 1024, "stage ring exceeds shared memory");
   constexpr int threads = kernel_threads<AM>();
   static int resident = 0;  // persistent CTAs the device holds at once
@@ -1528,7 +1533,7 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
   Params q = p;
   q.trace = g_trace;
   q.mt_rows = BM * CG * macc_of<AM>();
-  if constexpr (f32_tma_epi<EPI, BN, STAGES, CG, AM>()) q.out_tma = f32_out_map(&q.tma_out, q, splits);
+  if constexpr (f32_tma_epi<EPI, BN, STAGES, CG, AM, BMODE == B_TMA_MN>()) q.out_tma = f32_out_map(&q.tma_out, q, splits);
   q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, q.mt_rows) * splits;
   const int units = std::min(q.tiles, resident / CG);
   cfg.gridDim = dim3(units * CG);
@@ -1550,6 +1555,13 @@ struct Tile {
   int bn, cg;
 };
 
+static bool mn192_enabled() {
+  static const int on = [] {
+    const char* e = getenv("PC_MN192");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
 static bool cg2_enabled() {
   static const int on = [] {
     const char* e = getenv("PC_CG2");
@@ -1581,7 +1593,8 @@ static Tile pick_k(int M, int N, bool pair_ok, int splits = 1) {
 }
 static Tile pick_mn(int M, int N, bool pair_ok, int splits = 1) {
   if (pair_ok && cg2_enabled()) {
-    const int bn = N <= 128 ? 128 : 256;
+    // N = 384 (AlexNet conv3 / conv4 filters): two 192-wide tiles instead of 256 + 128
+    const int bn = N <= 128 ? 128 : (N % 192 == 0 && N % 256 != 0 && mn192_enabled()) ? 192 : 256;
     const long long units = (long long)((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn) * splits;
     if (units >= 74) return {bn, 2};
   }
@@ -1632,15 +1645,16 @@ static int launch_mn(const Params& p, Tile t, int splits, cudaStream_t st) {
   }
   if constexpr (!a_is_gather<AM>()) {
     if (t.cg == 2) {
-      if (t.bn == 128) return launch<AM, B_TMA_MN, EPI, 128, fst<EPI, 128, 8, 2>(), 2>(p, splits, st);
-      return launch<AM, B_TMA_MN, EPI, 256, fst<EPI, 256, 6, 2>(), 2>(p, splits, st);
+      if (t.bn == 128) return launch<AM, B_TMA_MN, EPI, 128, fst<EPI, 128, 8, 2, true>(), 2>(p, splits, st);
+      if (t.bn == 192) return launch<AM, B_TMA_MN, EPI, 192, fst<EPI, 192, 6, 2, true>(), 2>(p, splits, st);
+      return launch<AM, B_TMA_MN, EPI, 256, fst<EPI, 256, 6, 2, true>(), 2>(p, splits, st);
     }
   }
   switch (t.bn) {
-    case 64: return launch<AM, B_TMA_MN, EPI, 64, fst<EPI, 64, 8, 1>(), 1>(p, splits, st);
-    case 128: return launch<AM, B_TMA_MN, EPI, 128, fst<EPI, 128, 6, 1>(), 1>(p, splits, st);
-    case 192: return launch<AM, B_TMA_MN, EPI, 192, fst<EPI, 192, 5, 1>(), 1>(p, splits, st);
-    default: return launch<AM, B_TMA_MN, EPI, 256, fst<EPI, 256, 4, 1>(), 1>(p, splits, st);
+    case 64: return launch<AM, B_TMA_MN, EPI, 64, fst<EPI, 64, 8, 1, true>(), 1>(p, splits, st);
+    case 128: return launch<AM, B_TMA_MN, EPI, 128, fst<EPI, 128, 6, 1, true>(), 1>(p, splits, st);
+    case 192: return launch<AM, B_TMA_MN, EPI, 192, fst<EPI, 192, 5, 1, true>(), 1>(p, splits, st);
+    default: return launch<AM, B_TMA_MN, EPI, 256, fst<EPI, 256, 4, 1, true>(), 1>(p, splits, st);
   }
 }
 
@@ -1649,7 +1663,7 @@ static int launch_mn(const Params& p, Tile t, int splits, cudaStream_t st) {
 static int setup_mn_b(Params& p, const void* ptr, long long cb, long long rows, long long blocks, long long ld,
                       long long bstride, Tile t) {
   const int bnc = t.bn / t.cg;
-  p.b_chunked = (blocks == 1 || cb % bnc == 0) &&
+  p.b_chunked = bnc % 64 == 0 && (blocks == 1 || cb % bnc == 0) &&
                 make_mn_chunked_map(&p.tma_b, ptr, cb, rows, blocks, ld, bstride, bnc / 64);
   if (p.b_chunked) return PC_OK;
   return make_map(&p.tma_b, ptr, cb, rows, blocks, ld, bstride, 64);
@@ -1959,7 +1973,9 @@ static WgradPlan wgrad_plan(const pc_conv_geom& g) {
     return e ? atoi(e) : 1;
   }();
   const bool pair = cg2_enabled() && (i2c || (gather_cg2 && g.N % 128 == 0));
-  const Tile t = pair ? Tile{g.N <= 128 ? 128 : 256, 2} : Tile{bn_for_mn(g.N), 1};
+  // N = 384 (conv3 / conv4 filters): two 192-wide pair tiles instead of 256 + 128
+  const int pbn = g.N <= 128 ? 128 : (i2c && g.N % 192 == 0 && g.N % 256 != 0 && mn192_enabled()) ? 192 : 256;
+  const Tile t = pair ? Tile{pbn, 2} : Tile{bn_for_mn(g.N), 1};
   const long long tiles = ((Kc + BM * t.cg - 1) / (BM * t.cg)) * ((g.N + t.bn - 1) / t.bn);
   const long long kbs = (P + BK - 1) / BK;
   long long sp = choose_splits(tiles, kbs, t.bn, t.cg);

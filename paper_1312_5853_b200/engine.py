@@ -22,6 +22,7 @@ host.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -217,6 +218,17 @@ class ColumnEngine:
         for i in range(1, n):
             st, prv = self.layers[i], self.layers[i - 1]
             st.mask_dx = st.kind in ("conv", "fc", "pool") and prv.kind == "relu" and prv.skip_bwd
+        # ReLU -> max-pool -> conv/FC: the ReLU mask at a pixel that receives pool
+        # gradient is (its value > 0) = (the window maximum > 0), so the consumer's
+        # data-gradient epilogue masks by its own input (the pooled maximum) and the
+        # pool backward routes without reading the full-resolution activation —
+        # exact (masks are 0/1 and every contribution to a pixel shares its value).
+        if os.environ.get("PC_POOL_MASK_FOLD", "1") != "0":
+            for i in range(1, n - 1):
+                st, nxt = self.layers[i], self.layers[i + 1]
+                if st.kind == "pool" and st.mask_dx and nxt.kind in ("conv", "fc") and not nxt.mask_dx \
+                        and not (nxt.kind == "conv" and nxt.col):
+                    st.mask_dx, nxt.mask_dx = False, True
 
     def param_region(self, i: int) -> tuple:
         """[lo, hi) of layer position i's weights + bias in the flat buffers (up to the
