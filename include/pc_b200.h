@@ -216,6 +216,16 @@ PC_API int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, co
  * tensor-core implicit GEMM with 128-byte channel rows. */
 PC_API int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
                              void* dst, pc_stream_t stream);
+/* As pc_space_to_depth, with padding channel `ones` (s*s*C <= ones < Cs; -1 =
+ * none) set to 1.0 in every block: the input layer's weight gradient at that
+ * channel and tap (0, 0) is then its bias gradient (pc_s2d_wgrad_finish), so the
+ * bias needs no separate reduction over the upstream gradient. */
+PC_API int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
+                                int ones, void* dst, pc_stream_t stream);
+/* gb[n] = gw[n * K + ones] for n < N, then gw[i] = 0 where keep[i] == 0 (the
+ * structural zeros of the regrouped input-layer weights, including `ones`). */
+PC_API int pc_s2d_wgrad_finish(int N, int K, int ones, const uint8_t* keep, float* gw, float* gb,
+                               pc_stream_t stream);
 /* buf[i] = 0 where keep[i] == 0 (fp32): pins the regrouped conv's structural-zero
  * weights by zeroing their gradients before the SGD update. */
 PC_API int pc_mask_f32(long long n, const uint8_t* keep, float* buf, pc_stream_t stream);

@@ -309,11 +309,13 @@ extern "C" int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const
     float* ws = static_cast<float*>(workspace);
     if (g->B == 0) {
       cudaMemsetAsync(gw, 0, sizeof(float) * g->N * g->k * g->k * g->C, S(st));
-      cudaMemsetAsync(gb, 0, sizeof(float) * g->N, S(st));
+      if (gb) cudaMemsetAsync(gb, 0, sizeof(float) * g->N, S(st));
       return PC_OK;
     }
-    rc = colsum(gy, P, g->N, prec, gb, ws, S(st));
-    if (rc) return rc;
+    if (gb) {  // null: the caller derives the bias gradient otherwise (pc_s2d_wgrad_finish)
+      rc = colsum(gy, P, g->N, prec, gb, ws, S(st));
+      if (rc) return rc;
+    }
     float* part = ws + colsum_ws(P, g->N);
     if (prec == PC_BF16) {
       rc = umma_conv_wgrad(*g, x, gy, gw, part, S(st), upd);

@@ -611,7 +611,7 @@ __device__ __forceinline__ float ldg_ro(const __nv_bfloat16* p) { return __bfloa
 
 template <typename TS, int CS, int SS, int CC>  // SS, CC > 0: compile-time stride / channels
 __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_, int p, int Hs, int Ws,
-                                             const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst) {
+                                             const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst, int ones) {
   const int s = SS > 0 ? SS : s_, C = CC > 0 ? CC : C_;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)B * Hs * Ws) return;
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_
   const int Y = (int)(r % Hs), b = (int)(r / Hs);
   float v[CS];
 #pragma unroll
-  for (int i = 0; i < CS; ++i) v[i] = 0.f;
+  for (int i = 0; i < CS; ++i) v[i] = i == ones ? 1.f : 0.f;
   if constexpr (SS > 0 && CC > 0) {
 #pragma unroll
     for (int dy = 0; dy < SS; ++dy) {
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_
 template <int CS, int SS, int CC>
 __global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, int Ws, long long total,
                                                  const __nv_bfloat16* __restrict__ x,
-                                                 __nv_bfloat16* __restrict__ dst) {
+                                                 __nv_bfloat16* __restrict__ dst, int ones) {
   extern __shared__ __align__(16) uint8_t s2d_sm[];
   const int span = SS * W;                    // elements of SS consecutive rows
   const int slot = ((span + 7) / 8 + 1) * 8;  // per-channel staging (aligned-down start)
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, in
   for (int X = threadIdx.x; X < Ws; X += blockDim.x) {
     float v[CS];
 #pragma unroll
-    for (int i = 0; i < CS; ++i) v[i] = 0.f;
+    for (int i = 0; i < CS; ++i) v[i] = i == ones ? 1.f : 0.f;
 #pragma unroll
     for (int dy = 0; dy < SS; ++dy) {
       const int iy = iy0 + dy;
@@ -951,8 +951,15 @@ extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp
 
 extern "C" int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
                                  void* dst, pc_stream_t st) {
+  return pc_space_to_depth_ex(B, C, H, W, s, p, Cs, src, src_prec, -1, dst, st);
+}
+
+extern "C" int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, int Cs, const void* src,
+                                    int src_prec, int ones, void* dst, pc_stream_t st) {
   PC_REQUIRE(B >= 0 && C > 0 && H > 0 && W > 0 && s > 0 && p >= 0 && Cs >= s * s * C && (Cs == 64 || Cs == 32),
              PC_EVALUE, "space_to_depth: bad arguments (Cs must be 32 or 64 and >= s*s*C)");
+  PC_REQUIRE(ones < 0 || (ones >= s * s * C && ones < Cs), PC_EVALUE,
+             "space_to_depth: the ones channel must be a padding channel");
   const int Hs = (H + 2 * p + s - 1) / s, Ws = (W + 2 * p + s - 1) / s;
   const long long n = (long long)B * Hs * Ws;
   if (n == 0) return PC_OK;
@@ -962,7 +969,7 @@ extern "C" int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int C
     const size_t smem = (size_t)C * (((size_t)s * W + 7) / 8 + 1) * 8 * 2;
     if (smem <= 48 * 1024) {  // AlexNet conv1: row-staged
       s2d_rows_k<64, 4, 3><<<B * Hs, 64, smem, S(st)>>>(H, W, p, Hs, Ws, (long long)B * C * H * W,
-                                                         static_cast<const __nv_bfloat16*>(src), d);
+                                                         static_cast<const __nv_bfloat16*>(src), d, ones);
       PC_CUDA_CHECK_LAUNCH("space_to_depth");
       return PC_OK;
     }
@@ -970,15 +977,38 @@ extern "C" int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int C
   DISPATCH_PREC(src_prec, TS, {
     const TS* x = static_cast<const TS*>(src);
     if (Cs == 64 && s == 4 && C == 3)        // AlexNet conv1 (11x11/s4)
-      s2d_k<TS, 64, 4, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
+      s2d_k<TS, 64, 4, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d, ones);
     else if (Cs == 64 && s == 2 && C == 3)   // small64 conv1 (6x6/s2)
-      s2d_k<TS, 64, 2, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
+      s2d_k<TS, 64, 2, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d, ones);
     else if (Cs == 64)
-      s2d_k<TS, 64, 0, 0><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
+      s2d_k<TS, 64, 0, 0><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d, ones);
     else
-      s2d_k<TS, 32, 0, 0><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d);
+      s2d_k<TS, 32, 0, 0><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d, ones);
   });
   PC_CUDA_CHECK_LAUNCH("space_to_depth");
+  return PC_OK;
+}
+
+// Input-layer weight gradient finish: gb[n] = gw[n][ones] (the weight gradient
+// of the all-ones padding channel at tap (0, 0) IS the bias gradient: sum over
+// pixels of gy * 1), then the structural zeros are pinned (keep mask).
+__global__ void s2d_wgrad_finish_k(int N, int K, int ones, const uint8_t* __restrict__ keep,
+                                   float* __restrict__ gw, float* __restrict__ gb) {
+  const long long n = (long long)N * K;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / K), c = (int)(i - (long long)r * K);
+    if (c == ones) gb[r] = gw[i];
+    if (!keep[i]) gw[i] = 0.f;
+  }
+}
+
+extern "C" int pc_s2d_wgrad_finish(int N, int K, int ones, const uint8_t* keep, float* gw, float* gb,
+                                   pc_stream_t st) {
+  PC_REQUIRE(N > 0 && K > 0 && ones >= 0 && ones < K && keep && gw && gb, PC_EVALUE, "s2d_wgrad_finish: bad arguments");
+  int g = grid_for((long long)N * K, 256);
+  if (g > 148 * 8) g = 148 * 8;
+  s2d_wgrad_finish_k<<<g, 256, 0, S(st)>>>(N, K, ones, keep, gw, gb);
+  PC_CUDA_CHECK_LAUNCH("s2d_wgrad_finish");
   return PC_OK;
 }
 

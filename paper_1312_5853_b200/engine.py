@@ -115,6 +115,7 @@ class ColumnEngine:
         # pixels; col_kp = padded K (reference (c, i, j) order).
         self.col_kp = 0
         self.s2d = 0
+        self.s2d_ones = -1
         lay0 = first.layer if isinstance(first.layer, Conv) else None
         if self.prec == L.PC_BF16 and lay0 is not None and c % 64 and lay0.stride > 1 and \
                 c * lay0.stride ** 2 <= 64:
@@ -123,6 +124,10 @@ class ColumnEngine:
                            layout.s2d_extent(w, lay0.kernel, lay0.stride, lay0.pad)[0])
             self.in_cp = 64
             self.x = self._new(B * self.s2d_hw[0] * self.s2d_hw[1] * 64)
+            # padding channel held at 1.0: its weight gradient at tap (0, 0) is the
+            # layer's bias gradient (pc_s2d_wgrad_finish); its weights stay 0
+            self.s2d_ones = c * lay0.stride ** 2 if c * lay0.stride ** 2 < 64 and \
+                os.environ.get("PC_S2D_ONES", "1") != "0" else -1
         elif self.prec == L.PC_BF16 and lay0 is not None and c % 64:
             k0 = lay0.kernel
             self.col_kp = (c * k0 * k0 + 7) // 8 * 8
@@ -492,8 +497,8 @@ class ColumnEngine:
         src_prec = L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32
         if self.s2d:
             lay = self.cs.col_layers[0].layer
-            self.lib.call("pc_space_to_depth", self.B, c, h, w, lay.stride, lay.pad, 64, x_nchw.data_ptr(),
-                          src_prec, self.x.data_ptr(), self.stream)
+            self.lib.call("pc_space_to_depth_ex", self.B, c, h, w, lay.stride, lay.pad, 64, x_nchw.data_ptr(),
+                          src_prec, self.s2d_ones, self.x.data_ptr(), self.stream)
         elif self.col_kp:
             lay = self.cs.col_layers[0].layer
             self.lib.call("pc_im2col", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
@@ -576,7 +581,8 @@ class ColumnEngine:
                 st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
                 st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
                 st.inp.data_ptr() if st.mask_dx else None,
-                self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, f,
+                self.g32[st.w_off:].data_ptr(),
+                None if (st.s2d and self.s2d_ones >= 0) else self.g32[st.b_off:].data_ptr(), self.prec, f,
                 self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s, tag=tag))
         elif st.kind == "fc":
             d = math.prod(st.in_nhwc)
@@ -609,7 +615,10 @@ class ColumnEngine:
                 self._call(st, "pc_maxpool_backward", self.B, hh, ww, cc, st.cl.layer.kernel, st.cl.layer.stride,
                          st.gout.data_ptr(), st.argmax.data_ptr(),
                          st.inp.data_ptr() if st.mask_dx else None, st.gin.data_ptr(), self.prec, s)
-        if st.keep is not None:
+        if st.keep is not None and self.s2d_ones >= 0:
+            self.lib.call("pc_s2d_wgrad_finish", st.w_shape[0], st.keep.numel() // st.w_shape[0], self.s2d_ones,
+                          st.keep.data_ptr(), self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), s)
+        elif st.keep is not None:
             self.lib.call("pc_mask_f32", st.keep.numel(), st.keep.data_ptr(), self.g32[st.w_off:].data_ptr(),
                           s)
         if st.cl.cross and st.cl.shared and want_dx and self.m > 1:
