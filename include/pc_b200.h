@@ -216,6 +216,14 @@ PC_API int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, co
  * tensor-core implicit GEMM with 128-byte channel rows. */
 PC_API int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
                              void* dst, pc_stream_t stream);
+/* Bias gradient gb[n] = sum_p gy[p][n] (gy [P][N] in prec, N % 8 == 0) by a
+ * fixed grid of `ctas` CTAs using no shared memory, so it can run on a side
+ * stream beside the persistent tensor-core kernels; deterministic order.
+ * Workspace: pc_bias_grad_workspace(P, N, ctas) bytes. (The data/weight gradient
+ * entry points skip their own bias reduction when gb is NULL.) */
+PC_API size_t pc_bias_grad_workspace(long long P, int N, int ctas);
+PC_API int pc_bias_grad(long long P, int N, const void* gy, int prec, float* gb, float* ws, size_t ws_bytes,
+                        int ctas, pc_stream_t stream);
 /* As pc_space_to_depth, with padding channel `ones` (s*s*C <= ones < Cs; -1 =
  * none) set to 1.0 in every block: the input layer's weight gradient at that
  * channel and tap (0, 0) is then its bias gradient (pc_s2d_wgrad_finish), so the

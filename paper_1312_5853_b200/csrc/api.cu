@@ -235,6 +235,76 @@ int colsum(const void* g, long long P, int N, int prec, float* out, float* ws, c
   return PC_OK;
 }
 
+static int check_prec(int prec);
+
+// Background bias gradient (side stream, beside the data/weight-gradient GEMMs,
+// whose persistent CTAs hold nearly all shared memory): no shared memory, a
+// fixed grid of `ctas` CTAs. Pass 1: thread t owns 8-column group t % G and row
+// lane t / G of L = threads / G lanes, summing rows lane, lane + L, ... into
+// part[lane][.]; pass 2: a warp per 8-column group, lane l summing partial rows
+// l, l + 32, ... then a fixed xor-shuffle tree. Fixed order => deterministic.
+template <typename T>
+__global__ void __launch_bounds__(256) bias_bg1_k(const T* __restrict__ g, long long P, int N, int L,
+                                                  float* __restrict__ part) {
+  const int groups = N / 8;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int grp = t % groups, lane = t / groups;
+  if (lane >= L) return;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const T* col = g + (long long)grp * 8;
+#pragma unroll 4
+  for (long long r = lane; r < P; r += L) V8<T>::add(col + r * N, a);
+  float4* o = reinterpret_cast<float4*>(part + (long long)lane * N + grp * 8);
+  o[0] = make_float4(a[0], a[1], a[2], a[3]);
+  o[1] = make_float4(a[4], a[5], a[6], a[7]);
+}
+
+__global__ void __launch_bounds__(128) bias_bg2_k(const float* __restrict__ part, int L, int N,
+                                                  float* __restrict__ out) {
+  const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (grp >= N / 8) return;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int r = lane; r < L; r += 32) V8<float>::add(part + (long long)r * N + grp * 8, a);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] += __shfl_xor_sync(0xffffffffu, a[i], o);
+  if (lane < 8) {
+    float v = a[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) v = lane == i ? a[i] : v;
+    out[grp * 8 + lane] = v;
+  }
+}
+
+static int bias_bg_lanes(int N, int ctas) { return (ctas * 256) / (N / 8); }
+
+extern "C" PC_API size_t pc_bias_grad_workspace(long long P, int N, int ctas) {
+  if (N <= 0 || N % 8 || ctas <= 0) return 0;
+  return (size_t)bias_bg_lanes(N, ctas) * N * sizeof(float);
+}
+
+extern "C" PC_API int pc_bias_grad(long long P, int N, const void* gy, int prec, float* gb, float* ws, size_t ws_bytes,
+                            int ctas, pc_stream_t st) {
+  PC_REQUIRE(N > 0 && N % 8 == 0 && P >= 0 && ctas > 0 && (reinterpret_cast<uintptr_t>(gy) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(ws) & 15) == 0,
+             PC_EVALUE, "bias_grad: N %% 8 == 0, 16-byte aligned buffers required");
+  PC_REQUIRE(ws_bytes >= pc_bias_grad_workspace(P, N, ctas), PC_EVALUE, "bias_grad: workspace too small");
+  int rc = check_prec(prec);
+  if (rc) return rc;
+  const int L = bias_bg_lanes(N, ctas);
+  PC_REQUIRE(L >= 1, PC_EVALUE, "bias_grad: too few CTAs for %d columns", N);
+  const int blocks = (int)(((long long)L * (N / 8) + 255) / 256);
+  if (prec == PC_FP32)
+    bias_bg1_k<float><<<blocks, 256, 0, S(st)>>>(static_cast<const float*>(gy), P, N, L, ws);
+  else
+    bias_bg1_k<__nv_bfloat16><<<blocks, 256, 0, S(st)>>>(static_cast<const __nv_bfloat16*>(gy), P, N, L, ws);
+  bias_bg2_k<<<(N / 8 + 3) / 4, 128, 0, S(st)>>>(ws, L, N, gb);
+  count_launches(1);
+  PC_CUDA_CHECK_LAUNCH("bias_grad");
+  return PC_OK;
+}
+
 static int check_geom(const pc_conv_geom* g) {
   PC_REQUIRE(g != nullptr, PC_EVALUE, "null conv geometry");
   PC_REQUIRE(g->B >= 0 && g->H > 0 && g->W > 0 && g->C > 0 && g->N > 0 && g->k > 0 && g->stride > 0 &&
@@ -386,12 +456,14 @@ extern "C" int pc_fc_backward_ex(int B, int D, int U, const pc_mat* x, const voi
     if ((rc = check_mat(x, "fc_backward x"))) return rc;
     if (B == 0) {
       cudaMemsetAsync(gw, 0, sizeof(float) * (size_t)U * D, S(st));
-      cudaMemsetAsync(gb, 0, sizeof(float) * U, S(st));
+      if (gb) cudaMemsetAsync(gb, 0, sizeof(float) * U, S(st));
       return PC_OK;
     }
     float* ws = static_cast<float*>(workspace);
-    rc = colsum(gy, B, U, prec, gb, ws, S(st));
-    if (rc) return rc;
+    if (gb) {  // null: the caller derives the bias gradient otherwise (pc_bias_grad)
+      rc = colsum(gy, B, U, prec, gb, ws, S(st));
+      if (rc) return rc;
+    }
     PC_REQUIRE(upd == nullptr || prec == PC_BF16, PC_EVALUE, "fused SGD update: bf16 tensor-core path only");
     rc = prec == PC_BF16 ? umma_fc_wgrad(B, D, U, *x, gy, gw, ws + colsum_ws(B, U), S(st), upd)
                          : simt_fc_wgrad(B, D, U, *x, gy, gw, S(st), prec);

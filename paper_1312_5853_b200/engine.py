@@ -96,6 +96,7 @@ class ColumnEngine:
         self.has_dropout = any(st.kind == "dropout" for st in self.layers)
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=device)
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+        self.bias_side = None                # enable_bias_side
 
     # ------------------------------------------------------------------ setup
     def _new(self, n, dtype=None):
@@ -342,6 +343,40 @@ class ColumnEngine:
         self.lib.call("pc_sgd_step_ex", n, dev.data_ptr(), mx, self.lr, self.mom, self.wd, ctas_per_sm,
                       self.stream if stream is None else stream)
 
+    def enable_bias_side(self, stream, ctas: int):
+        """Single-replica plans: bias gradients of conv / FC layers run on ``stream``
+        (pc_bias_grad: no shared memory, ``ctas`` CTAs) beside the data/weight-gradient
+        GEMMs; the step program joins the stream before the update."""
+        self.bias_side, self.bias_ctas = stream, int(ctas)
+        ws = 16
+        for st in self.layers:
+            if st.kind in ("conv", "fc") and not st.col and not st.s2d:
+                n = st.cl.out_shape[0]
+                if n % 8 == 0:
+                    ws = max(ws, self.lib.raw("pc_bias_grad_workspace")(self._bias_rows(st), n, self.bias_ctas))
+        self.bias_ws = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
+
+    def _bias_rows(self, st) -> int:
+        return self.B * st.geom.Ho * st.geom.Wo if st.kind == "conv" else self.B
+
+    def _bias_fork(self, st) -> bool:
+        """Launch layer st's bias gradient on the side stream (True) or leave it to
+        the gradient kernels (False)."""
+        side = getattr(self, "bias_side", None)
+        n = st.cl.out_shape[0]
+        if side is None or n % 8 or st.col or st.s2d:
+            return False
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        self.lib.call("pc_bias_grad", self._bias_rows(st), n, st.gout.data_ptr(), self.prec,
+                      self.g32[st.b_off:].data_ptr(), self.bias_ws.data_ptr(), self.bias_ws.numel(), self.bias_ctas,
+                      side.cuda_stream)
+        return True
+
+    def join_side(self):
+        side = getattr(self, "bias_side", None)
+        if side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(side)
+
     def configure_fused_sgd(self, on: bool):
         """Single-replica plans (no gradient reduction between backward and update):
         the bf16 weight-gradient kernels of conv/FC layers apply the momentum-SGD
@@ -577,12 +612,12 @@ class ColumnEngine:
         elif st.kind == "conv":
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
+            no_gb = (st.s2d and self.s2d_ones >= 0) or self._bias_fork(st)
             self._split_backward(st, "pc_conv2d_backward_ex", flags, lambda f, tag: self._call(
                 st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
                 st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
                 st.inp.data_ptr() if st.mask_dx else None,
-                self.g32[st.w_off:].data_ptr(),
-                None if (st.s2d and self.s2d_ones >= 0) else self.g32[st.b_off:].data_ptr(), self.prec, f,
+                self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(), self.prec, f,
                 self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s, tag=tag))
         elif st.kind == "fc":
             d = math.prod(st.in_nhwc)
@@ -591,10 +626,11 @@ class ColumnEngine:
             gm = L.Mat(st.gin.data_ptr() if want_dx else st.inp.data_ptr(), xm.ld, xm.cb, xm.bstride)
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
+            no_gb = self._bias_fork(st)
             self._split_backward(st, "pc_fc_backward_ex", flags, lambda f, tag: self._call(
                 st, "pc_fc_backward_ex", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
                 C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
-                self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), self.prec, f,
+                self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(), self.prec, f,
                 self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s, tag=tag))
         elif st.kind == "relu":
             if not st.skip_bwd and want_dx:

@@ -133,6 +133,17 @@ class _Runner:
                     if tabs is not None:
                         self.split_sgd[wid] = tabs
         self.side = torch.cuda.Stream(device=dev) if self.split_sgd else None
+        # opt-in (PC_BIAS_SIDE=1), single replica: bias gradients on their own side
+        # stream beside the GEMMs (with d > 1 the bucketed all-reduce needs each
+        # layer's bias at once). Measured on AlexNet b256: no gain — the reduction
+        # competes with the operand-bound GEMMs for L2 bandwidth — so off by default.
+        self.bias_side = None
+        if d == 1 and os.environ.get("PC_BIAS_SIDE", "0") != "0":
+            self.bias_side = torch.cuda.Stream(device=dev)
+            ctas = torch.cuda.get_device_properties(dev).multi_processor_count * \
+                int(os.environ.get("PC_BIAS_CTAS_PER_SM", "2"))
+            for eng in self.engines.values():
+                eng.enable_bias_side(self.bias_side, ctas)
         # background CTAs per SM for the side-stream update: few enough that each
         # backward GEMM still finds room for its one persistent CTA per SM
         self.sgd_bg_ctas = int(os.environ.get("PC_SGD_BG_CTAS", "2"))
@@ -232,12 +243,16 @@ class _Runner:
                         self.reducer.layer_done(e, *e.param_region(i))
                     if i == self.head_pos and e.wid in self.split_sgd:   # fork: head update on the side stream
                         self.side.wait_stream(torch.cuda.current_stream())
+                        if e.bias_side is not None:   # the head's bias gradients
+                            self.side.wait_stream(e.bias_side)
                         with torch.cuda.stream(self.side):
                             e.sgd_table(self.split_sgd[e.wid][0], ctas_per_sm=self.sgd_bg_ctas)
                 if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
                     self.exchange.reduce_scatter(i, engines)
         if self.reducer is not None:
             self.reducer.reduce(self.columns)
+        for eng in self.engines.values():
+            eng.join_side()
         for eng in self.engines.values():
             if eng.wid in self.split_sgd:
                 eng.sgd_table(self.split_sgd[eng.wid][1])
