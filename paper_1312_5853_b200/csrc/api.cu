@@ -44,8 +44,47 @@ __global__ void reduce_partials_k(const float* __restrict__ ws, int splits, long
   }
 }
 
+// Many slices of a short output (the input layer: 148 slices of 55 K weights):
+// 8 lanes per float4, lane l summing slices l, l + 8, ... (unrolled, loads in
+// flight), then a fixed xor-shuffle tree — deterministic, and 8x the parallelism
+// of one thread walking all slices.
+__global__ void __launch_bounds__(256) reduce_partials_wide_k(const float* __restrict__ ws, int splits, long long n,
+                                                              float* __restrict__ out, pc_sgd_fuse upd, int fused) {
+  const long long i = ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3) * 4;
+  const int lane = threadIdx.x & 7;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n) {
+#pragma unroll 4
+    for (int z = lane; z < splits; z += 8) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(ws + z * n + i));
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+    a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+    a.z += __shfl_xor_sync(0xffffffffu, a.z, o);
+    a.w += __shfl_xor_sync(0xffffffffu, a.w, o);
+  }
+  if (lane == 0 && i < n) {
+    if (fused) sgd_apply4(upd, i, a);
+    else *reinterpret_cast<float4*>(out + i) = a;
+  }
+}
+
 int reduce_partials(const float* ws, int splits, long long n, float* out, cudaStream_t st, const pc_sgd_fuse* upd) {
   if (n == 0) return PC_OK;
+  if (splits >= 32 && (n & 3) == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 &&
+      (upd || (reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+    pc_sgd_fuse u;
+    memset(&u, 0, sizeof(u));
+    if (upd) u = *upd;
+    const long long threads = (n / 4) * 8;
+    reduce_partials_wide_k<<<(int)((threads + 255) / 256), 256, 0, st>>>(ws, splits, n, out, u, upd != nullptr);
+    PC_CUDA_CHECK_LAUNCH("reduce_partials");
+    return PC_OK;
+  }
   long long g = (n / 4 + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
   if (g < 1) g = 1;

@@ -456,11 +456,67 @@ __global__ void __launch_bounds__(NT) softmax_xent_k(int K, const T* __restrict_
   }
 }
 
-__global__ void sum_f64_k(int n, const double* __restrict__ v, double* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double acc = 0.0;
-    for (int i = 0; i < n; ++i) acc += v[i];
-    out[0] = acc;
+// Warp per row (K <= 32 * KPL): the row stays in registers (lane l holds classes
+// l, l + 32, ...), max and sum-of-exp are warp-shuffle reductions, one pass of
+// loads and one of stores; 8 rows per 256-thread CTA. Same arithmetic as
+// softmax_xent_k (fp32 exp / sums, fp64 log-probability of the label).
+template <typename T, int KPL>
+__global__ void __launch_bounds__(256) softmax_xent_warp_k(int B, int K, const T* __restrict__ logits,
+                                                          const int32_t* __restrict__ labels, double scale,
+                                                          T* __restrict__ grad, double* __restrict__ row_loss,
+                                                          int* __restrict__ bad) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= B) return;
+  const T* z = logits + (long long)row * K;
+  float x[KPL];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const int i = lane + 32 * j;
+    x[j] = i < K ? ld(z + i) : -INFINITY;
+    mx = fmaxf(mx, x[j]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    x[j] = lane + 32 * j < K ? expf(x[j] - mx) : 0.f;
+    sum += x[j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const int lab = labels[row];
+  const bool ok = lab >= 0 && lab < K;
+  const float inv = 1.f / sum, sc = (float)scale;
+  T* g = grad + (long long)row * K;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const int i = lane + 32 * j;
+    if (i < K) g[i] = cvt<T>((x[j] * inv - (i == lab ? 1.f : 0.f)) * sc);
+  }
+  if (lane == 0) {
+    if (!ok) { *bad = 1; row_loss[row] = 0.0; return; }
+    const double logp = (double)(ld(z + lab) - mx) - log((double)sum);
+    row_loss[row] = -logp * scale;
+  }
+}
+
+// Step loss: 256 threads, thread t summing v[t], v[t + 256], ... in order, then a
+// fixed tree (warp xor-shuffles, then the 8 warp sums in order): deterministic,
+// and the row losses load in parallel instead of one dependent chain.
+__global__ void __launch_bounds__(256) sum_f64_k(int n, const double* __restrict__ v, double* __restrict__ out) {
+  __shared__ double sh[8];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) acc += v[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = sh[0];
+    for (int w = 1; w < 8; ++w) t += sh[w];
+    out[0] = t;
   }
 }
 
@@ -668,6 +724,7 @@ __global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, in
   const int span = SS * W;                    // elements of SS consecutive rows
   const int slot = ((span + 7) / 8 + 1) * 8;  // per-channel staging (aligned-down start)
   __nv_bfloat16* lin = reinterpret_cast<__nv_bfloat16*>(s2d_sm);
+  __nv_bfloat16* lout = lin + CC * slot;  // [Ws][CS] staged output row (16-byte aligned: slot % 8 == 0)
   const int b = blockIdx.x / Hs, Y = blockIdx.x - b * Hs;
   const int iy0 = Y * SS - p;
   int sh[CC];
@@ -710,9 +767,25 @@ __global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, in
           v[(dy * SS + dx) * CC + c] = ok ? __bfloat162float(lin[c * slot + sh[c] + dy * W + ix]) : 0.f;
       }
     }
-    __nv_bfloat16* out = dst + ((long long)blockIdx.x * Ws + X) * CS;
+    // stage the block row in SMEM; 16-byte chunk q of block X at slot q ^ (X % 8)
+    // (XOR swizzle: conflict-free writes, static register indices)
 #pragma unroll
-    for (int q = 0; q < CS / 8; ++q) Vec8<__nv_bfloat16>::store(out + q * 8, v + q * 8);
+    for (int q = 0; q < CS / 8; ++q) {
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(lout + (X * CS + ((q ^ (X & 7)) % (CS / 8)) * 8)) = u;
+    }
+  }
+  __syncthreads();
+  // the (b, Y) block row is contiguous in dst: coalesced 16-byte stores
+  static_assert(CS / 8 == 8 || CS / 8 == 4, "swizzle over 8 (or 4) chunks per block");
+  uint4* out = reinterpret_cast<uint4*>(dst + (long long)blockIdx.x * Ws * CS);
+  const uint4* src = reinterpret_cast<const uint4*>(lout);
+  for (int c = threadIdx.x; c < Ws * CS / 8; c += blockDim.x) {
+    const int X = c / (CS / 8), q = c % (CS / 8);
+    out[c] = src[X * (CS / 8) + ((q ^ (X & 7)) % (CS / 8))];
   }
 }
 
@@ -870,14 +943,19 @@ extern "C" int pc_softmax_xent(int B, int K, const void* logits, const int32_t* 
                                void* grad, double* row_loss, int* bad_label, int prec, pc_stream_t st) {
   PC_REQUIRE(B >= 0 && K >= 2, PC_ESHAPE, "softmax_xent: bad extents B=%d K=%d", B, K);
   if (B == 0) return PC_OK;
-  DISPATCH_PREC(prec, T, softmax_xent_k<T, 256><<<B, 256, 0, S(st)>>>(
-      K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label));
+  if (K <= 32 * 32) {
+    DISPATCH_PREC(prec, T, softmax_xent_warp_k<T, 32><<<(B + 7) / 8, 256, 0, S(st)>>>(
+        B, K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label));
+  } else {
+    DISPATCH_PREC(prec, T, softmax_xent_k<T, 256><<<B, 256, 0, S(st)>>>(
+        K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label));
+  }
   PC_CUDA_CHECK_LAUNCH("softmax_xent");
   return PC_OK;
 }
 
 extern "C" int pc_sum_f64(int n, const double* v, double* out, pc_stream_t st) {
-  sum_f64_k<<<1, 32, 0, S(st)>>>(n, v, out);
+  sum_f64_k<<<1, 256, 0, S(st)>>>(n, v, out);
   PC_CUDA_CHECK_LAUNCH("sum_f64");
   return PC_OK;
 }
@@ -966,7 +1044,7 @@ extern "C" int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, in
   const int g = grid_for(n, 256);
   auto* d = static_cast<__nv_bfloat16*>(dst);
   if (src_prec == PC_BF16 && Cs == 64 && s == 4 && C == 3 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-    const size_t smem = (size_t)C * (((size_t)s * W + 7) / 8 + 1) * 8 * 2;
+    const size_t smem = (size_t)C * (((size_t)s * W + 7) / 8 + 1) * 8 * 2 + (size_t)Ws * 64 * 2;
     if (smem <= 48 * 1024) {  // AlexNet conv1: row-staged
       s2d_rows_k<64, 4, 3><<<B * Hs, 64, smem, S(st)>>>(H, W, p, Hs, Ws, (long long)B * C * H * W,
                                                          static_cast<const __nv_bfloat16*>(src), d, ones);
