@@ -44,7 +44,7 @@ typedef void* pc_stream_t; /* cudaStream_t */
 
 enum pc_prec { PC_FP32 = 0, PC_BF16 = 1 };
 enum pc_status { PC_OK = 0, PC_ESHAPE = 1, PC_EVALUE = 2, PC_ECUDA = 3, PC_ENCCL = 4 };
-enum pc_conv_flags { PC_RELU = 1, PC_WANT_DX = 2, PC_WANT_DW = 4, PC_MASK_DX = 8 };
+enum pc_conv_flags { PC_RELU = 1, PC_WANT_DX = 2, PC_WANT_DW = 4, PC_MASK_DX = 8, PC_WT_PRESET = 16 };
 
 /* Conv geometry (reference ConvParams + input shape, kernels.py:37-83). */
 typedef struct {
@@ -224,6 +224,13 @@ PC_API int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, c
 PC_API size_t pc_bias_grad_workspace(long long P, int N, int ctas);
 PC_API int pc_bias_grad(long long P, int N, const void* gy, int prec, float* gb, float* ws, size_t ws_bytes,
                         int ctas, pc_stream_t stream);
+/* bf16 conv data gradient, prepared filters: wt = the filters in the layout
+ * (transposed, rotated as the data-gradient path needs) that pc_conv2d_backward
+ * otherwise rebuilds in its workspace on every call. With PC_WT_PRESET in the
+ * backward flags, `w` is taken to be this wt for the data gradient — so a step
+ * can prepare every layer's wt off the critical path (a side stream at the
+ * start of the step). wt holds N*k*k*C bf16. */
+PC_API int pc_conv2d_dgrad_weights(const pc_conv_geom* g, const void* w, void* wt, int prec, pc_stream_t stream);
 /* As pc_space_to_depth, with padding channel `ones` (s*s*C <= ones < Cs; -1 =
  * none) set to 1.0 in every block: the input layer's weight gradient at that
  * channel and tap (0, 0) is then its bias gradient (pc_s2d_wgrad_finish), so the

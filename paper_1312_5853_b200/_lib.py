@@ -17,7 +17,7 @@ from .errors import status_error
 LIB_PATH = Path(__file__).resolve().parent / "libpcb200.so"
 
 PC_FP32, PC_BF16 = 0, 1
-PC_RELU, PC_WANT_DX, PC_WANT_DW, PC_MASK_DX = 1, 2, 4, 8
+PC_RELU, PC_WANT_DX, PC_WANT_DW, PC_MASK_DX, PC_WT_PRESET = 1, 2, 4, 8, 16
 
 _vp, _i, _ll, _sz, _f, _d = C.c_void_p, C.c_int, C.c_longlong, C.c_size_t, C.c_float, C.c_double
 
@@ -69,6 +69,7 @@ SIGNATURES = {
     "pc_sgd_step_ex": (_i, [_i, _vp, _ll, _f, _f, _f, _i, _vp]),
     "pc_space_to_depth": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "pc_mask_f32": (_i, [_ll, _vp, _vp, _vp]),
+    "pc_conv2d_dgrad_weights": (_i, [_P(ConvGeom), _vp, _vp, _i, _vp]),
     "pc_bias_grad_workspace": (_sz, [_ll, _i, _i]),
     "pc_bias_grad": (_i, [_ll, _i, _vp, _i, _vp, _vp, _sz, _i, _vp]),
     "pc_space_to_depth_ex": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp]),

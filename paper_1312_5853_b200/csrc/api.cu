@@ -410,7 +410,8 @@ extern "C" int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const
   if (flags & PC_WANT_DX) {
     if (g->B == 0) return PC_OK;
     const void* mk = (flags & PC_MASK_DX) ? mask : nullptr;
-    rc = prec == PC_BF16 ? umma_conv_dgrad(*g, w, gy, gx, mk, S(st), workspace, ws_bytes)
+    PC_REQUIRE(!(flags & PC_WT_PRESET) || prec == PC_BF16, PC_EVALUE, "PC_WT_PRESET: bf16 path only");
+    rc = prec == PC_BF16 ? umma_conv_dgrad(*g, w, gy, gx, mk, S(st), workspace, ws_bytes, (flags & PC_WT_PRESET) != 0)
                          : simt_conv_dgrad(*g, w, gy, gx, mk, S(st), prec);
     if (rc) return rc;
   }
@@ -435,6 +436,13 @@ extern "C" int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const
     if (rc) return rc;
   }
   return PC_OK;
+}
+
+extern "C" PC_API int pc_conv2d_dgrad_weights(const pc_conv_geom* g, const void* w, void* wt, int prec, pc_stream_t st) {
+  int rc = check_geom(g);
+  if (rc || (rc = check_prec(prec))) return rc;
+  PC_REQUIRE(prec == PC_BF16 && w && wt, PC_EVALUE, "conv2d_dgrad_weights: bf16 weights required");
+  return umma_conv_dgrad_weights(*g, w, wt, S(st));
 }
 
 static int check_mat(const pc_mat* m, const char* what) {

@@ -8,7 +8,8 @@ bool umma_available();
 int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const float* bias, void* y,
                       int flags, cudaStream_t st);
 int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* gx, const void* mask,
-                    cudaStream_t st, void* ws, size_t ws_bytes);
+                    cudaStream_t st, void* ws, size_t ws_bytes, bool w_preset = false);
+int umma_conv_dgrad_weights(const pc_conv_geom& g, const void* w, void* wt, cudaStream_t st);
 int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float* gw, float* part,
                     cudaStream_t st, const pc_sgd_fuse* upd = nullptr);
 long long umma_wgrad_splits(const pc_conv_geom& g);

@@ -1876,29 +1876,56 @@ size_t umma_conv_extra_ws(const pc_conv_geom& g, int prec) {
   return prec == PC_BF16 ? (size_t)g.N * g.k * g.k * g.C * 2 + 256 : 0;
 }
 
+// The data gradient reads its filters as wt[c][ij][n] (N contiguous), rotated by
+// 180 degrees (flip) when it runs as a forward conv of gy (TMA im2col or halo
+// paths). dgrad_flip() is that choice, made from the geometry alone, so the
+// caller can prepare wt ahead of time (pc_conv2d_dgrad_weights).
+static bool halo_geom_ok(int Ci, int k, int Wo) {
+  const int Wv = (Wo + 7) / 8 * 8;
+  if (Wv > 128 || Ci % 8 || Ci < 64 || k > HALO_KMAX) return false;
+  const int R = BM / Wv;
+  return BM + (k - 1) * Wv <= HALO_SLOT_BYTES / 128 && R + k - 1 <= 256;
+}
+static int dgrad_flip(const pc_conv_geom& g) {
+  const bool rot = g.stride == 1 && g.H + 2 * g.pad - g.k + 1 == g.Ho;  // dgrad = conv of gy with the rotated filter
+  const bool i2c = rot && im2col_ok(g.N, g.N, 0);
+  const bool halo = rot && halo_wanted(g.C, g.k) && halo_geom_ok(g.N, g.k, g.W);
+  return (i2c || halo) ? 1 : 0;
+}
+
+int umma_conv_dgrad_weights(const pc_conv_geom& g, const void* w, void* wt, cudaStream_t st) {
+  transpose_w(w, static_cast<__nv_bfloat16*>(wt), g.N, g.k * g.k, g.C, dgrad_flip(g), st);
+  PC_CUDA_CHECK_LAUNCH("transpose_w");
+  return PC_OK;
+}
+
 int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* gx, const void* mask,
-                    cudaStream_t st, void* ws, size_t ws_bytes) {
+                    cudaStream_t st, void* ws, size_t ws_bytes, bool w_preset) {
   if (!conv_tc_shape(g)) {
+    PC_REQUIRE(!w_preset, PC_EVALUE, "conv dgrad: prepared weights need the tensor-core path");
     g_simt_launches++;
     return simt_conv_dgrad(g, w, gy, gx, mask, st, PC_BF16);
   }
   const int KK = g.k * g.k;
   size_t need = (size_t)g.N * KK * g.C * 2;
-  PC_REQUIRE(ws != nullptr && ws_bytes >= need, PC_EVALUE, "conv dgrad: workspace too small");
-  // the transposed weights live at the END of the workspace (wgrad partials use the front)
-  __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(
-      (reinterpret_cast<uintptr_t>(ws) + ws_bytes - need) & ~uintptr_t(127));
-  const bool rot = g.stride == 1 && g.H + 2 * g.pad - g.k + 1 == g.Ho;  // dgrad = conv of gy with the rotated filter
+  const int flip = dgrad_flip(g);
+  const bool rot = g.stride == 1 && g.H + 2 * g.pad - g.k + 1 == g.Ho;
   const bool i2c = rot && im2col_ok(g.N, g.N, 0);
   const bool halo_ok = rot && halo_wanted(g.C, g.k);
-  transpose_w(w, wt, g.N, KK, g.C, (i2c || halo_ok) ? 1 : 0, st);
-  PC_CUDA_CHECK_LAUNCH("transpose_w");
   int M = g.B * g.H * g.W, K = KK * g.N;
   Params p = base_params(M, g.C, K);
   const bool halo = halo_ok && setup_halo(p, gy, g.B, g.Ho, g.Wo, g.N, g.k, g.pad - (g.k - 1), g.H, g.W);
-  if (halo_ok && !halo && !i2c) {  // rotated weights were written for a path that does not apply
-    transpose_w(w, wt, g.N, KK, g.C, 0, st);
+  PC_REQUIRE(!w_preset || (i2c || halo) == (flip != 0), PC_EVALUE,
+             "conv dgrad: prepared weights do not match the data-gradient path");
+  const void* wt = w;
+  if (!w_preset) {
+    PC_REQUIRE(ws != nullptr && ws_bytes >= need, PC_EVALUE, "conv dgrad: workspace too small");
+    // the transposed weights live at the END of the workspace (wgrad partials use the front)
+    __nv_bfloat16* wt_ws = reinterpret_cast<__nv_bfloat16*>(
+        (reinterpret_cast<uintptr_t>(ws) + ws_bytes - need) & ~uintptr_t(127));
+    transpose_w(w, wt_ws, g.N, KK, g.C, (i2c || halo) ? 1 : 0, st);
     PC_CUDA_CHECK_LAUNCH("transpose_w");
+    wt = wt_ws;
   }
   const Tile t = pick_k(p.M, g.C, i2c || halo);
   int rc = make_map(&p.tma_b, wt, K, g.C, 1, K, 0, t.bn / t.cg);

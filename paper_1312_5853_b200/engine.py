@@ -71,6 +71,7 @@ class LayerState:
     s2d: int = 0                         # space-to-depth input conv: block size (= reference stride)
     drop: tuple = ()                     # dropout: (H, W, C, C_dense, c_off, threshold) of this column's slice
     keep: torch.Tensor | None = None     # s2d: uint8 mask of real filter taps in the device weights
+    wt: torch.Tensor | None = None       # conv: filters prepared for the data gradient (pc_conv2d_dgrad_weights)
 
 
 class ColumnEngine:
@@ -97,6 +98,7 @@ class ColumnEngine:
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=device)
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
         self.bias_side = None                # enable_bias_side
+        self.wt_ready = False                # the step program prepared st.wt this step
 
     # ------------------------------------------------------------------ setup
     def _new(self, n, dtype=None):
@@ -372,6 +374,26 @@ class ColumnEngine:
                       side.cuda_stream)
         return True
 
+    def enable_dgrad_weights(self):
+        """bf16: per conv layer with a data gradient, a buffer for its filters in the
+        data-gradient layout, filled by prepare_dgrad_weights (on a side stream at the
+        start of the step) instead of by a transpose inside every backward call."""
+        if self.prec != L.PC_BF16:
+            return False
+        for i, st in enumerate(self.layers):
+            g = st.geom
+            tc = g is not None and g.C % 8 == 0 and g.cs % 8 == 0 and g.N % 8 == 0 and \
+                (g.C == g.cs or g.cstride % 8 == 0)   # the tensor-core data gradient (conv_tc_shape)
+            if st.kind == "conv" and i > 0 and not st.col and not st.s2d and tc:
+                st.wt = torch.empty(layout.numel(st.w_shape), dtype=torch.bfloat16, device=self.device)
+        return any(st.wt is not None for st in self.layers)
+
+    def prepare_dgrad_weights(self, stream):
+        for st in self.layers:
+            if st.wt is not None:
+                self.lib.call("pc_conv2d_dgrad_weights", C.byref(st.geom), self._w_lowp(st), st.wt.data_ptr(),
+                              self.prec, stream)
+
     def join_side(self):
         side = getattr(self, "bias_side", None)
         if side is not None:
@@ -613,8 +635,12 @@ class ColumnEngine:
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
             no_gb = (st.s2d and self.s2d_ones >= 0) or self._bias_fork(st)
+            w_ptr = self._w_lowp(st)
+            if want_dx and st.wt is not None and self.wt_ready:
+                flags |= L.PC_WT_PRESET
+                w_ptr = st.wt.data_ptr()
             self._split_backward(st, "pc_conv2d_backward_ex", flags, lambda f, tag: self._call(
-                st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
+                st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
                 st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
                 st.inp.data_ptr() if st.mask_dx else None,
                 self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(), self.prec, f,

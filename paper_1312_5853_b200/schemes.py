@@ -137,6 +137,12 @@ class _Runner:
         # stream beside the GEMMs (with d > 1 the bucketed all-reduce needs each
         # layer's bias at once). Measured on AlexNet b256: no gain — the reduction
         # competes with the operand-bound GEMMs for L2 bandwidth — so off by default.
+        # conv filters in the data-gradient layout, prepared on a side stream at the
+        # start of every step (beside the forward) instead of inside each backward
+        self.wt_side = None
+        if os.environ.get("PC_WT_PREP", "1") != "0":
+            if any([eng.enable_dgrad_weights() for eng in self.engines.values()]):
+                self.wt_side = torch.cuda.Stream(device=dev)
         self.bias_side = None
         if d == 1 and os.environ.get("PC_BIAS_SIDE", "0") != "0":
             self.bias_side = torch.cuda.Stream(device=dev)
@@ -230,12 +236,19 @@ class _Runner:
             eng.load_batch(self.x_dev[lo:lo + shard], self.y_dev[lo:lo + shard])
         n = len(self.cs.col_layers)
         overlap = self.reducer is not None and hasattr(self.reducer, "layer_done")
+        if self.wt_side is not None:   # fork: data-gradient filters, joined before the backward
+            self.wt_side.wait_stream(torch.cuda.current_stream())
+            for eng in self.engines.values():
+                eng.prepare_dgrad_weights(self.wt_side.cuda_stream)
+                eng.wt_ready = True
         for engines in self.replicas.values():
             for i in range(n):
                 if self.cs.col_layers[i].cross and self.exchange is not None:
                     self.exchange.all_gather(i, engines)
                 for e in engines:
                     e.forward(i, loss_scale)
+            if self.wt_side is not None:
+                torch.cuda.current_stream().wait_stream(self.wt_side)
             for i in range(n - 1, -1, -1):
                 for e in engines:
                     e.backward(i)
