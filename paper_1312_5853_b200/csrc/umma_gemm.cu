@@ -1535,7 +1535,11 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
   q.mt_rows = BM * CG * macc_of<AM>();
   if constexpr (f32_tma_epi<EPI, BN, STAGES, CG, AM, BMODE == B_TMA_MN>()) q.out_tma = f32_out_map(&q.tma_out, q, splits);
   q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, q.mt_rows) * splits;
-  const int units = std::min(q.tiles, resident / CG);
+  static const int max_ctas = [] {  // debug: cap the persistent grid (PC_MAX_CTAS)
+    const char* e = getenv("PC_MAX_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  const int units = std::min(q.tiles, (max_ctas > 0 ? std::min(resident, max_ctas) : resident) / CG);
   cfg.gridDim = dim3(units * CG);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, q);
   PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "umma_gemm launch: %s", cudaGetErrorString(e));
@@ -2119,6 +2123,11 @@ static FcPlan fc_split_plan(int M, int N, int K) {
   const int cap = 148 / cg, kbs = (K + BK - 1) / BK;
   if (tiles * 2 > cap || kbs < 8) return {t, 1};
   int sp = (int)std::min<long long>(cap / tiles, kbs / 4);
+  static const int sp_cap = [] {  // tuning knob: PC_FC_SPLIT_CAP
+    const char* e = getenv("PC_FC_SPLIT_CAP");
+    return e ? atoi(e) : 0;
+  }();
+  if (sp_cap > 0) sp = std::min(sp, sp_cap);
   if (sp < 2) return {t, 1};
   const int per = (kbs + sp - 1) / sp;
   return {t, (kbs + per - 1) / per};
