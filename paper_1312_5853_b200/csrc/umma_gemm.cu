@@ -973,8 +973,12 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         kj = tc.kb_begin - (tc.kb_begin / p.i2c_k) * p.i2c_k;
       }
       if constexpr (AM == A_IM2COL_K) {
-        t_ox = m0 % p.i2c_Wo;
-        const int q = m0 / p.i2c_Wo;
+        // a CTA whose rows all lie past M (second half of a partial pair tile) loads
+        // the first pixels instead (its rows are discarded by the epilogue): an
+        // im2col start pixel outside the tensor faults the TMA unit
+        const int mv = m0 < p.M ? m0 : 0;
+        t_ox = mv % p.i2c_Wo;
+        const int q = mv / p.i2c_Wo;
         t_oy = q % p.i2c_Ho;
         t_b = q / p.i2c_Ho;
         ktap = tc.kb_begin / p.i2c_cpt;
@@ -2027,7 +2031,9 @@ static bool macc_wgrad_ok(const pc_conv_geom& g) {
     return e ? atoi(e) : 1;
   }();
   const int Kc = g.k * g.k * g.C;
-  return on && Kc > 2 * BM && Kc <= 5 * BM && g.N <= 128 && g.N % 16 == 0 && im2col_ok(g.cs, g.C, g.cstride);
+  // one TMEM accumulator of N fp32 columns per 128 rows of M: all of them within 512 columns
+  return on && Kc > 2 * BM && Kc <= 5 * BM && g.N <= 128 && g.N % 16 == 0 &&
+         (long long)((Kc + BM - 1) / BM) * g.N <= 512 && im2col_ok(g.cs, g.C, g.cstride);
 }
 static int macc_splits(const pc_conv_geom& g) {
   const long long kbs = ((long long)g.B * g.Ho * g.Wo + BK - 1) / BK;
