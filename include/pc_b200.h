@@ -231,6 +231,11 @@ PC_API int pc_bias_grad(long long P, int N, const void* gy, int prec, float* gb,
  * can prepare every layer's wt off the critical path (a side stream at the
  * start of the step). wt holds N*k*k*C bf16. */
 PC_API int pc_conv2d_dgrad_weights(const pc_conv_geom* g, const void* w, void* wt, int prec, pc_stream_t stream);
+/* Cap (0 = none) on the number of CTAs of the persistent tensor-core kernels
+ * launched next by the calling thread; a step program uses it to run the FC
+ * weight-gradient + update chain on a side stream beside the convolution
+ * backward on disjoint SM sets. */
+PC_API int pc_set_grid_cap(int ctas);
 /* As pc_space_to_depth, with padding channel `ones` (s*s*C <= ones < Cs; -1 =
  * none) set to 1.0 in every block: the input layer's weight gradient at that
  * channel and tap (0, 0) is then its bias gradient (pc_s2d_wgrad_finish), so the

@@ -116,10 +116,21 @@ int apply_sgd(const float* g, long long n, const pc_sgd_fuse* upd, cudaStream_t 
 // each column a warp (fixed-order strided sums, then a fixed shuffle tree).
 // Rows per pass-1 block: each of the CTA's row lanes (256 threads / 8-column groups)
 // sums ~24 rows, so pass 1 has many CTAs with many 16-byte loads in flight.
+// Rows per pass-1 block: enough blocks for ~8 resident CTAs on each of 148 SMs
+// (the conv3-5 upstream gradients, 22-33 MB, ran at ~3 TB/s with 2.4 CTAs per SM),
+// at least 4 rows per lane.
 static long long cs_rb(long long P, int N) {
   const int groups = N % 8 == 0 ? N / 8 : 0;
-  const int lanes = groups ? 256 / (groups < 256 ? groups : 256) : 1;
-  return groups ? (long long)lanes * 24 : 512;
+  if (!groups) return 512;
+  const long long lanes = 256 / (groups < 256 ? groups : 256);
+  static const int occ = [] {  // target pass-1 CTAs per SM (PC_CS_OCC; 0 = 24 rows per lane)
+    const char* e = getenv("PC_CS_OCC");
+    return e ? atoi(e) : 8;
+  }();
+  if (occ <= 0) return lanes * 24;
+  const long long want = (P + 148LL * occ - 1) / (148LL * occ);
+  const long long rb = (want + lanes - 1) / lanes * lanes;
+  return rb > lanes * 4 ? rb : lanes * 4;
 }
 long long colsum_ws(long long P, int N) { return ((P + cs_rb(P, N) - 1) / cs_rb(P, N)) * (long long)N; }
 
@@ -371,6 +382,11 @@ using namespace pc;
 
 extern "C" const char* pc_last_error(void) { return g_err.c_str(); }
 extern "C" int pc_version(void) { return 1; }
+extern "C" PC_API int pc_set_grid_cap(int ctas) {
+  PC_REQUIRE(ctas >= 0, PC_EVALUE, "grid cap must be >= 0");
+  set_grid_cap(ctas);
+  return PC_OK;
+}
 extern "C" unsigned long long pc_launch_count(void) { return g_launches.load(); }
 extern "C" int pc_has_tcgen05(void) { return umma_available() ? 1 : 0; }
 

@@ -5,6 +5,7 @@
 namespace pc {
 
 bool umma_available();
+void set_grid_cap(int ctas);
 int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const float* bias, void* y,
                       int flags, cudaStream_t st);
 int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* gx, const void* mask,

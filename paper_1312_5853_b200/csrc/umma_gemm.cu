@@ -1458,6 +1458,10 @@ static int make_im2col_map(CUtensorMap* map, const void* ptr, int cs, int W, int
 }
 
 static std::atomic<unsigned long long> g_tc_launches{0}, g_simt_launches{0};
+// Per-thread cap on the persistent grid of the next tensor-core launches
+// (pc_set_grid_cap): lets a step program run two GEMM chains side by side on
+// disjoint SM sets (the CUDA graph records the grid of each launch).
+static thread_local int t_grid_cap = 0;
 
 // Programmatic dependent launch for the GEMM kernels (PC_PDL=0 disables): a
 // GEMM's prologue overlaps the tail of the kernel before it on the stream.
@@ -1543,7 +1547,10 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
     const char* e = getenv("PC_MAX_CTAS");
     return e ? atoi(e) : 0;
   }();
-  const int units = std::min(q.tiles, (max_ctas > 0 ? std::min(resident, max_ctas) : resident) / CG);
+  int cap = resident;
+  if (max_ctas > 0) cap = std::min(cap, max_ctas);
+  if (t_grid_cap > 0) cap = std::min(cap, std::max(t_grid_cap, CG));
+  const int units = std::min(q.tiles, cap / CG);
   cfg.gridDim = dim3(units * CG);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, q);
   PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "umma_gemm launch: %s", cudaGetErrorString(e));
@@ -1693,6 +1700,8 @@ static Params base_params(int M, int N, int K) {
 }  // namespace umma
 
 using namespace umma;
+
+void set_grid_cap(int ctas) { umma::t_grid_cap = ctas; }
 
 bool umma_available() {
   int dev = 0, major = 0, minor = 0;

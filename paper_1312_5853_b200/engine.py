@@ -394,10 +394,33 @@ class ColumnEngine:
                 self.lib.call("pc_conv2d_dgrad_weights", C.byref(st.geom), self._w_lowp(st), st.wt.data_ptr(),
                               self.prec, stream)
 
+    def enable_fc_side(self, stream, side_ctas: int, main_ctas: int, span: int):
+        """Single replica, fused update: every FC layer's weight gradient + momentum
+        update (HBM-bound: the FC6 update alone moves 680 MB) runs on ``stream`` with
+        its GEMM grid capped at ``side_ctas`` CTAs, while the data-gradient chain keeps
+        the main stream; the main-stream GEMMs are capped at ``main_ctas`` from the
+        first fork through the next ``span`` conv layers, so the two chains run on
+        disjoint SM sets instead of queueing behind each other's persistent grids."""
+        self.fc_side, self.fc_side_ctas, self.fc_main_ctas, self.fc_span = stream, side_ctas, main_ctas, span
+        self.ws_side = torch.empty(max(self.ws_bytes, 16), dtype=torch.uint8, device=self.device)
+        self._main_cap_left = 0
+
+    def _main_cap(self, st):
+        """Grid cap of this main-stream layer's GEMMs while the FC side chain runs."""
+        if getattr(self, "_main_cap_left", 0) <= 0 or st.kind not in ("conv", "fc"):
+            return False
+        self.lib.call("pc_set_grid_cap", self.fc_main_ctas)
+        if st.kind == "conv":
+            self._main_cap_left -= 1
+        return True
+
     def join_side(self):
-        side = getattr(self, "bias_side", None)
-        if side is not None:
-            torch.cuda.current_stream(self.device).wait_stream(side)
+        for side in (getattr(self, "bias_side", None), getattr(self, "fc_side", None)):
+            if side is not None:
+                torch.cuda.current_stream(self.device).wait_stream(side)
+        if getattr(self, "fc_side", None) is not None:
+            self._main_cap_left = 0
+            self.lib.call("pc_set_grid_cap", 0)
 
     def configure_fused_sgd(self, on: bool):
         """Single-replica plans (no gradient reduction between backward and update):
@@ -622,6 +645,14 @@ class ColumnEngine:
         return L.Mat(st.inp.data_ptr(), ds, ds, self.B * ds)
 
     def backward(self, i: int):
+        capped = self._main_cap(self.layers[i])
+        try:
+            self._backward(i)
+        finally:
+            if capped:
+                self.lib.call("pc_set_grid_cap", 0)
+
+    def _backward(self, i: int):
         st, lib, s = self.layers[i], self.lib, self.stream
         want_dx = i > 0
         if st.kind == "conv" and st.col:      # input layer: weight / bias gradients only
@@ -653,11 +684,29 @@ class ColumnEngine:
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
             no_gb = self._bias_fork(st)
-            self._split_backward(st, "pc_fc_backward_ex", flags, lambda f, tag: self._call(
-                st, "pc_fc_backward_ex", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
-                C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
-                self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(), self.prec, f,
-                self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s, tag=tag))
+
+            def fc_call(f, tag, stream=s, ws=self.ws):
+                self._call(st, "pc_fc_backward_ex", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
+                           C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
+                           self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(),
+                           self.prec, f, ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None,
+                           stream, tag=tag)
+
+            side = getattr(self, "fc_side", None)
+            if side is not None and upd is not None and PROFILE is None:
+                # data gradient here; weight gradient + fused update on the side chain, forked
+                # after the data gradient (which reads the pre-update weights)
+                if want_dx:
+                    fc_call(flags & ~L.PC_WANT_DW, "")
+                side.wait_stream(torch.cuda.current_stream(self.device))
+                self.lib.call("pc_set_grid_cap", self.fc_side_ctas)
+                try:
+                    fc_call(flags & ~(L.PC_WANT_DX | L.PC_MASK_DX), "", stream=side.cuda_stream, ws=self.ws_side)
+                finally:
+                    self.lib.call("pc_set_grid_cap", 0)
+                self._main_cap_left = self.fc_span
+            else:
+                self._split_backward(st, "pc_fc_backward_ex", flags, fc_call)
         elif st.kind == "relu":
             if not st.skip_bwd and want_dx:
                 self._call(st, "pc_relu_backward", self.B * math.prod(st.in_nhwc), st.inp.data_ptr(),

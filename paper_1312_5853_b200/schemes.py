@@ -137,6 +137,18 @@ class _Runner:
         # stream beside the GEMMs (with d > 1 the bucketed all-reduce needs each
         # layer's bias at once). Measured on AlexNet b256: no gain — the reduction
         # competes with the operand-bound GEMMs for L2 bandwidth — so off by default.
+        # FC weight gradients + fused updates on a side stream, on a separate SM set
+        # (PC_FC_SIDE_CTAS CTAs; 0 = off) beside the data-gradient chain
+        self.fc_side = None
+        side_ctas = int(os.environ.get("PC_FC_SIDE_CTAS", "0"))
+        if fuse and side_ctas > 0:
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            side_ctas = min(side_ctas, sms - 2) & ~1
+            self.fc_side = torch.cuda.Stream(device=dev)
+            for eng in self.engines.values():
+                if getattr(eng, "fuse_sgd", False):
+                    eng.enable_fc_side(self.fc_side, side_ctas, (sms - side_ctas) & ~1,
+                                       int(os.environ.get("PC_FC_SIDE_SPAN", "2")))
         # conv filters in the data-gradient layout, prepared on a side stream at the
         # start of every step (beside the forward) instead of inside each backward
         self.wt_side = None
