@@ -105,6 +105,12 @@ struct alignas(64) Params {
   // the bf16 shadow of p, updated in place (v = mom v - lr (g + wd p); p += v)
   CUtensorMap tma_p, tma_v, tma_pl;
   float lr, mom, wd;
+  // A_IM2COL_K with a last channel chunk of <= 32 channels (conv2: 96 = 64 + 32):
+  // that k-block loads 32-channel boxes (64-byte rows, 64B swizzle) of A and B
+  // instead of zero-filled / unused 64-channel ones — a quarter fewer operand
+  // bytes for the layer, whose GEMMs are limited by operand delivery
+  int half_chunk;
+  CUtensorMap tma_a32, tma_b32;
 };
 
 // Debug timeline: slot s of tile lt of CTA b (first TRACE_TILES tiles).
@@ -306,6 +312,11 @@ __device__ __forceinline__ int blk_idx(int idx, int cb) { return cb ? (int)((uns
 __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// Same with 64B swizzle (layout type 4): K-major rows of 32 bf16, 8-row atoms of 512 B.
+__device__ __forceinline__ uint64_t make_desc_sw64(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (4ull << 61);
 }
 
 // Instruction descriptor: D f32, A/B bf16, majorness, N (pair tile width), M = 128 * CG.
@@ -1022,8 +1033,11 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
               tma_load_3d<CG>(&p.tma_b, &full[s], st0 + HALO_SLOT_BYTES + i * B_STAGE_BYTES,
                               (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
         } else if (!HALO && elect_one()) {
+          // A_IM2COL_K: the k-block of a last chunk with <= 32 channels moves 32-channel boxes
+          const bool half = AM == A_IM2COL_K && p.half_chunk && kc + 32 >= p.i2c_C;
           if (leader)
-            mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + (GATHER ? 0 : MACC > 1 ? p.macc_chunks * 64 * BK * 2
+            mbar_arrive_expect_tx(&full[s], half ? CG * (B_STAGE_BYTES + A_STAGE_BYTES) / 2
+                                                 : CG * (B_STAGE_BYTES + (GATHER ? 0 : MACC > 1 ? p.macc_chunks * 64 * BK * 2
                                                                                        : A_STAGE_BYTES)));
           const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
           if constexpr (B_MN) {
@@ -1039,11 +1053,11 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             }
           } else {
             const int k = AM == A_IM2COL_K ? ktap * p.i2c_C + kc : kb * BK;
-            tma_load_3d<CG>(&p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
+            tma_load_3d<CG>(half ? &p.tma_b32 : &p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
           }
           if constexpr (AM == A_IM2COL_K) {
-            // 128 output pixels from the tile's first pixel; K block = 64 channels of tap (i, j)
-            tma_im2col_5d<CG>(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
+            // 128 output pixels from the tile's first pixel; K block = 64 (or 32) channels of tap (i, j)
+            tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
                               t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
                               (uint16_t)ki);
           } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5) {
@@ -1234,6 +1248,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
     if (leader) {
       const uint64_t a0 = A_MN ? make_desc(smem_u32(sA), 64 * BK * 2, 1024) : make_desc(smem_u32(sA), 16, 1024);
       const uint64_t b0 = B_MN ? make_desc(smem_u32(sB), 64 * BK * 2, 1024) : make_desc(smem_u32(sB), 16, 1024);
+      const uint64_t a0h = make_desc_sw64(smem_u32(sA), 16, 512), b0h = make_desc_sw64(smem_u32(sB), 16, 512);
       constexpr uint32_t A_KSTEP = (A_MN ? 2048 : 32) >> 4, B_KSTEP = (B_MN ? 2048 : 32) >> 4;
       int git = 0, lt = 0;
       if constexpr (BRES) {
@@ -1257,9 +1272,11 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         int hj = HALO ? tc.kb_begin % p.i2c_k : 0, hch = HALO ? tc.kb_begin / p.i2c_k : 0;
         for (int it = 0; it < tc.nkb; ++it, ++git) {
           int nk16 = BK / 16;
+          bool half = false;
           if (partial) {
             const int left = p.i2c_C - mchunk * BK;
             if (left < BK) nk16 = (left + 15) / 16;
+            half = p.half_chunk && left <= 32;
             if (++mchunk == p.i2c_cpt) mchunk = 0;
           }
           if constexpr (HALO) {
@@ -1275,9 +1292,9 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           if (it == 0 && lane == 0) trace_stamp(p, lt, 7);
           if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (elect_one()) {
-            const uint64_t ad = a0 + (uint64_t)((s * A_STRIDE) >> 4);
+            const uint64_t ad = (half ? a0h : a0) + (uint64_t)((s * A_STRIDE) >> 4);
             const uint64_t bd = BRES ? b0 + (uint64_t)(((tc.kb_begin + it) * p.i2c_k * B_STAGE_BYTES) >> 4)
-                                     : b0 + (uint64_t)((s * B_STRIDE) >> 4);
+                                     : (half ? b0h : b0) + (uint64_t)((s * B_STRIDE) >> 4);
             if constexpr (HALO) {
               // filter row i: the window shifted by i * Wv rows (multiple of 8), B tile i
               const int k = p.i2c_k;
@@ -1394,16 +1411,17 @@ static bool get_encode() {
 
 // 3-D bf16 view {inner, rows, blocks} with strides (ld, bstride) elements; box {64, box_rows, 1}.
 static int make_map(CUtensorMap* map, const void* ptr, long long inner, long long rows, long long blocks,
-                    long long ld, long long bstride, int box_rows) {
+                    long long ld, long long bstride, int box_rows, int box_inner = 64) {
   PC_REQUIRE(get_encode(), PC_ECUDA, "cuTensorMapEncodeTiled unavailable");
   PC_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && ld % 8 == 0 && (blocks == 1 || bstride % 8 == 0),
              PC_EVALUE, "TMA view not 16-byte aligned (ld=%lld bstride=%lld)", ld, bstride);
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)blocks};
   cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)(blocks > 1 ? bstride : ld * rows) * 2};
-  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, 1u};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        box_inner == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   PC_REQUIRE(r == CUDA_SUCCESS, PC_ECUDA, "cuTensorMapEncodeTiled failed (%d): inner=%lld rows=%lld blocks=%lld",
              (int)r, inner, rows, blocks);
@@ -1433,7 +1451,8 @@ static std::once_flag g_encode_i2c_once;
 // im2col view of a channel-blocked NHWC activation: dims {cs, W, H, B, nblk};
 // each load = `pixels` walked output positions x 64 channels (128 B rows, 128B swizzle).
 static int make_im2col_map(CUtensorMap* map, const void* ptr, int cs, int W, int H, int B, int nblk,
-                           long long cstride, int pixels, int lw, int lh, int uw, int uh, int stride) {
+                           long long cstride, int pixels, int lw, int lh, int uw, int uh, int stride,
+                           int chans = 64) {
   std::call_once(g_encode_i2c_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1450,8 +1469,9 @@ static int make_im2col_map(CUtensorMap* map, const void* ptr, int cs, int W, int
   int lower[3] = {lw, lh, 0}, upper[3] = {uw, uh, 0};
   cuuint32_t estr[5] = {1u, (cuuint32_t)stride, (cuuint32_t)stride, 1u, 1u};
   CUresult r = g_encode_i2c(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, lower,
-                            upper, 64u, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            upper, (cuuint32_t)chans, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            chans == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   PC_REQUIRE(r == CUDA_SUCCESS, PC_ECUDA, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
   return PC_OK;
@@ -1712,6 +1732,13 @@ bool umma_available() {
 }
 
 // TMA im2col needs 64-channel (128 B) pixel rows within one channel block.
+static bool half_chunk_enabled() {  // PC_HALF_CHUNK=0: zero-filled 64-channel boxes instead
+  static const int on = [] {
+    const char* e = getenv("PC_HALF_CHUNK");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
 static bool im2col_enabled() {
   static const int enabled = [] {
     const char* e = getenv("PC_IM2COL");
@@ -1856,6 +1883,13 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
     if (rc) return rc;
     set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
     set_i2c_kloop(p, g.C, g.k);
+    if (g.C == g.cs && g.C % BK != 0 && g.C % BK <= 32 && half_chunk_enabled()) {
+      rc = make_im2col_map(&p.tma_a32, x, g.cs, g.W, g.H, g.B, 1, g.cstride, BM, -g.pad, -g.pad,
+                           g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride, 32);
+      if (!rc) rc = make_map(&p.tma_b32, w, K, g.N, 1, K, 0, t.bn / t.cg, 32);
+      if (rc) return rc;
+      p.half_chunk = 1;
+    }
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
   return launch_kb<A_GATHER_FWD, EPI_BF16>(p, t, 1, st);
