@@ -128,6 +128,16 @@ PC_API int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, const vo
 PC_API int pc_maxpool_backward(int B, int H, int W, int C, int k, int s, const void* gy,
                         const uint8_t* argmax, const void* mask, void* gx, int prec,
                         pc_stream_t stream);
+/* pc_maxpool_backward (bf16, 3x3 / stride 2, 256 % (C/8) == 0) that also writes
+ * gb[c] = sum over (b, y, x) of the stored gx: the bias gradient of the conv whose
+ * ReLU output this pool reads (gx is that conv's upstream gradient), reduced in a
+ * fixed order while gx is written instead of by a second pass over it.
+ * gb == NULL: plain pc_maxpool_backward. Workspace:
+ * pc_maxpool_backward_bias_workspace(C) bytes. */
+PC_API size_t pc_maxpool_backward_bias_workspace(int C);
+PC_API int pc_maxpool_backward_bias(int B, int H, int W, int C, int k, int s, const void* gy, const uint8_t* argmax,
+                                    const void* mask, void* gx, int prec, float* gb, void* ws, size_t ws_bytes,
+                                    pc_stream_t stream);
 
 /* --- softmax cross-entropy: kernels.softmax_xent_scaled (kernels.py:252-276) */
 /* grad[b][k] = (softmax - onehot) * scale (stored in prec); row_loss[b] =

@@ -69,6 +69,8 @@ SIGNATURES = {
     "pc_sgd_step_ex": (_i, [_i, _vp, _ll, _f, _f, _f, _i, _vp]),
     "pc_space_to_depth": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _vp]),
     "pc_mask_f32": (_i, [_ll, _vp, _vp, _vp]),
+    "pc_maxpool_backward_bias_workspace": (_sz, [_i]),
+    "pc_maxpool_backward_bias": (_i, [_i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _sz, _vp]),
     "pc_set_grid_cap": (_i, [_i]),
     "pc_conv2d_dgrad_weights": (_i, [_P(ConvGeom), _vp, _vp, _i, _vp]),
     "pc_bias_grad_workspace": (_sz, [_ll, _i, _i]),

@@ -350,6 +350,130 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
   }
 }
 
+// bf16 3x3/s2 backward that also reduces the bias gradient of the layer whose
+// upstream gradient it writes (conv -> ReLU -> pool: gx IS that conv's gy): a
+// fixed grid walks the 2x2 blocks grid-stride (the thread's 8-channel group is
+// constant because 256 % (C / 8) == 0), each thread sums the bf16 values it
+// stores, the CTA combines its row lanes in a fixed order into part[block][C],
+// and pool_bias_rows_k sums the CTA rows (warp per 8 channels, fixed xor tree).
+// Deterministic; saves the separate two-pass reduction that re-read gx.
+__global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H, int W, int C, int Ho, int Wo,
+                                                                    const __nv_bfloat16* __restrict__ gy,
+                                                                    const uint8_t* __restrict__ arg,
+                                                                    const __nv_bfloat16* __restrict__ mask,
+                                                                    __nv_bfloat16* __restrict__ gx,
+                                                                    float* __restrict__ part) {
+  __shared__ float red[256][9];
+  const int H2 = (H + 1) >> 1, W2 = (W + 1) >> 1;
+  const unsigned cg = (unsigned)(C >> 3);
+  const unsigned total = (unsigned)B * H2 * W2 * cg;
+  float bsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const unsigned blk = t / cg;
+    const int c0 = (int)(t - blk * cg) * 8;
+    const unsigned r = blk / (unsigned)W2;
+    const int X = (int)(blk - r * W2);
+    const int b = (int)(r / (unsigned)H2);
+    const int Y = (int)(r - (unsigned)b * H2);
+    float acc[4][8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[q][v] = 0.f;
+#pragma unroll
+    for (int dy = -1; dy <= 0; ++dy) {
+      const int oy = Y + dy;
+      if (oy < 0 || oy >= Ho) continue;
+#pragma unroll
+      for (int dx = -1; dx <= 0; ++dx) {
+        const int ox = X + dx;
+        if (ox < 0 || ox >= Wo) continue;
+        const long long o = (((long long)b * Ho + oy) * Wo + ox) * C + c0;
+        const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + o));
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(gy + o));
+#pragma unroll
+        for (int qy = 0; qy < 2; ++qy) {
+          const int li = qy - 2 * dy;
+          if (li > 2) continue;
+#pragma unroll
+          for (int qx = 0; qx < 2; ++qx) {
+            const int lj = qx - 2 * dx;
+            if (lj > 2) continue;
+            const unsigned want = 0x01010101u * (unsigned)(li * 3 + lj);
+            const unsigned m0 = __vcmpeq4(a.x, want), m1 = __vcmpeq4(a.y, want);
+            const unsigned s0 = g.x & __byte_perm(m0, 0, 0x1100), s1 = g.y & __byte_perm(m0, 0, 0x3322);
+            const unsigned s2 = g.z & __byte_perm(m1, 0, 0x1100), s3 = g.w & __byte_perm(m1, 0, 0x3322);
+            float* ac = acc[qy * 2 + qx];
+            ac[0] += __uint_as_float(s0 << 16);
+            ac[1] += __uint_as_float(s0 & 0xFFFF0000u);
+            ac[2] += __uint_as_float(s1 << 16);
+            ac[3] += __uint_as_float(s1 & 0xFFFF0000u);
+            ac[4] += __uint_as_float(s2 << 16);
+            ac[5] += __uint_as_float(s2 & 0xFFFF0000u);
+            ac[6] += __uint_as_float(s3 << 16);
+            ac[7] += __uint_as_float(s3 & 0xFFFF0000u);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int y = 2 * Y + (q >> 1), x = 2 * X + (q & 1);
+      if (y >= H || x >= W) continue;
+      const long long o = (((long long)b * H + y) * W + x) * C + c0;
+      if (mask) {
+        float mk[8];
+        Vec8<__nv_bfloat16>::load(mask + o, mk);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[q][v] = mk[v] > 0.f ? acc[q][v] : 0.f;
+      }
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        h[e] = __floats2bfloat162_rn(acc[q][2 * e], acc[q][2 * e + 1]);
+        const float2 f = __bfloat1622float2(h[e]);  // the stored values: what a reduction of gx would read
+        bsum[2 * e] += f.x;
+        bsum[2 * e + 1] += f.y;
+      }
+      *reinterpret_cast<uint4*>(gx + o) = u;
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 8; ++v) red[threadIdx.x][v] = bsum[v];
+  __syncthreads();
+  // thread -> (channel group q = tid % cg, lane = tid / cg); lanes combine in order
+  const int lanes = 256 / (int)cg;
+  if (threadIdx.x < cg * 8) {
+    const int q = threadIdx.x >> 3, v = threadIdx.x & 7;
+    float sum = 0.f;
+    for (int l = 0; l < lanes; ++l) sum += red[l * cg + q][v];
+    part[(long long)blockIdx.x * C + q * 8 + v] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(128) pool_bias_rows_k(const float* __restrict__ part, int R, int N,
+                                                        float* __restrict__ out) {
+  const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (grp >= N / 8) return;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int r = lane; r < R; r += 32) {
+    const float4* p = reinterpret_cast<const float4*>(part + (long long)r * N + grp * 8);
+    const float4 x = p[0], y = p[1];
+    a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w; a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] += __shfl_xor_sync(0xffffffffu, a[i], o);
+  if (lane < 8) {
+    float v = a[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) v = lane == i ? a[i] : v;
+    out[grp * 8 + lane] = v;
+  }
+}
+
 // k=3, s=2 (every AlexNet pool): one thread per 2x2 input block (Y, X) and 8
 // channels. The block is covered exactly by windows {Y-1, Y} x {X-1, X}, so the
 // thread reads those <= 4 windows' gradient + argmax once and writes 4 pixels
@@ -903,6 +1027,34 @@ extern "C" int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, cons
           B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(x), static_cast<T*>(y), argmax);
   });
   PC_CUDA_CHECK_LAUNCH("maxpool_forward");
+  return PC_OK;
+}
+
+static constexpr int POOL_BIAS_CTAS = 148 * 8;
+
+extern "C" size_t pc_maxpool_backward_bias_workspace(int C) { return (size_t)POOL_BIAS_CTAS * C * sizeof(float); }
+
+extern "C" int pc_maxpool_backward_bias(int B, int H, int W, int C, int k, int s, const void* gy,
+                                        const uint8_t* argmax, const void* mask, void* gx, int prec, float* gb,
+                                        void* ws, size_t ws_bytes, pc_stream_t st) {
+  if (!gb) return pc_maxpool_backward(B, H, W, C, k, s, gy, argmax, mask, gx, prec, st);
+  int Ho, Wo, rc = pool_geom(H, W, k, s, &Ho, &Wo);
+  if (rc) return rc;
+  PC_REQUIRE(prec == PC_BF16 && k == 3 && s == 2 && C % 8 == 0 && 256 % (C / 8) == 0 && aligned(gy, 32) &&
+                 aligned(gx, 32) && aligned(argmax, 8) && (!mask || aligned(mask, 32)) && aligned(ws, 16),
+             PC_EVALUE, "maxpool_backward_bias: bf16 3x3/s2, C/8 dividing 256, aligned buffers");
+  PC_REQUIRE(ws_bytes >= pc_maxpool_backward_bias_workspace(C), PC_EVALUE, "maxpool_backward_bias: workspace");
+  if ((long long)B * C == 0) {
+    cudaMemsetAsync(gb, 0, sizeof(float) * C, S(st));
+    return PC_OK;
+  }
+  float* part = static_cast<float*>(ws);
+  maxpool_bwd_bf16_k3s2_bias_k<<<POOL_BIAS_CTAS, 256, 0, S(st)>>>(
+      B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(gy), argmax, static_cast<const __nv_bfloat16*>(mask),
+      static_cast<__nv_bfloat16*>(gx), part);
+  pool_bias_rows_k<<<(C / 8 + 3) / 4, 128, 0, S(st)>>>(part, POOL_BIAS_CTAS, C, gb);
+  count_launches(1);
+  PC_CUDA_CHECK_LAUNCH("maxpool_backward_bias");
   return PC_OK;
 }
 

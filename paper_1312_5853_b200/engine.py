@@ -72,6 +72,8 @@ class LayerState:
     drop: tuple = ()                     # dropout: (H, W, C, C_dense, c_off, threshold) of this column's slice
     keep: torch.Tensor | None = None     # s2d: uint8 mask of real filter taps in the device weights
     wt: torch.Tensor | None = None       # conv: filters prepared for the data gradient (pc_conv2d_dgrad_weights)
+    bias_by_pool: bool = False           # conv: bias gradient reduced by the pool backward that writes its gy
+    pool_bias: int = -1                  # pool: position of the conv whose bias gradient it reduces
 
 
 class ColumnEngine:
@@ -231,6 +233,20 @@ class ColumnEngine:
         # data-gradient epilogue masks by its own input (the pooled maximum) and the
         # pool backward routes without reading the full-resolution activation —
         # exact (masks are 0/1 and every contribution to a pixel shares its value).
+        # conv -> ReLU -> 3x3/s2 max-pool (bf16): the pool backward writes the conv's
+        # upstream gradient and reduces its bias gradient on the way (pc_maxpool_backward_bias)
+        if self.prec == L.PC_BF16 and os.environ.get("PC_POOL_BIAS", "1") != "0":
+            for i in range(2, n):
+                st, rl, cv = self.layers[i], self.layers[i - 1], self.layers[i - 2]
+                if st.kind == "pool" and rl.kind == "relu" and rl.skip_bwd and cv.kind == "conv" and \
+                        not cv.col and not cv.s2d and st.cl.layer.kernel == 3 and st.cl.layer.stride == 2:
+                    c = st.in_nhwc[2]
+                    if c % 8 == 0 and 256 % (c // 8) == 0:
+                        st.pool_bias, cv.bias_by_pool = i - 2, True
+        if any(st.pool_bias >= 0 for st in self.layers):
+            cmax = max(st.in_nhwc[2] for st in self.layers if st.pool_bias >= 0)
+            self.pool_ws = torch.empty(self.lib.raw("pc_maxpool_backward_bias_workspace")(cmax), dtype=torch.uint8,
+                                       device=self.device)
         if os.environ.get("PC_POOL_MASK_FOLD", "1") != "0":
             for i in range(1, n - 1):
                 st, nxt = self.layers[i], self.layers[i + 1]
@@ -665,7 +681,7 @@ class ColumnEngine:
         elif st.kind == "conv":
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
             upd = self._fuse.get(id(st)) if getattr(self, "_fuse", None) else None
-            no_gb = (st.s2d and self.s2d_ones >= 0) or self._bias_fork(st)
+            no_gb = (st.s2d and self.s2d_ones >= 0) or st.bias_by_pool or self._bias_fork(st)
             w_ptr = self._w_lowp(st)
             if want_dx and st.wt is not None and self.wt_ready:
                 flags |= L.PC_WT_PRESET
@@ -723,9 +739,16 @@ class ColumnEngine:
         elif st.kind == "pool":
             if want_dx:
                 hh, ww, cc = st.in_nhwc
-                self._call(st, "pc_maxpool_backward", self.B, hh, ww, cc, st.cl.layer.kernel, st.cl.layer.stride,
-                         st.gout.data_ptr(), st.argmax.data_ptr(),
-                         st.inp.data_ptr() if st.mask_dx else None, st.gin.data_ptr(), self.prec, s)
+                if st.pool_bias >= 0:
+                    cv = self.layers[st.pool_bias]
+                    self._call(st, "pc_maxpool_backward_bias", self.B, hh, ww, cc, st.cl.layer.kernel,
+                               st.cl.layer.stride, st.gout.data_ptr(), st.argmax.data_ptr(),
+                               st.inp.data_ptr() if st.mask_dx else None, st.gin.data_ptr(), self.prec,
+                               self.g32[cv.b_off:].data_ptr(), self.pool_ws.data_ptr(), self.pool_ws.numel(), s)
+                else:
+                    self._call(st, "pc_maxpool_backward", self.B, hh, ww, cc, st.cl.layer.kernel,
+                               st.cl.layer.stride, st.gout.data_ptr(), st.argmax.data_ptr(),
+                               st.inp.data_ptr() if st.mask_dx else None, st.gin.data_ptr(), self.prec, s)
         if st.keep is not None and self.s2d_ones >= 0:
             self.lib.call("pc_s2d_wgrad_finish", st.w_shape[0], st.keep.numel() // st.w_shape[0], self.s2d_ones,
                           st.keep.data_ptr(), self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), s)

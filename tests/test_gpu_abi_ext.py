@@ -117,3 +117,27 @@ def test_grid_cap_keeps_results_bit_identical():
             lib.call("pc_set_grid_cap", 0)
         outs.append(y)
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("shape", [(8, 27, 27, 256), (4, 13, 13, 128), (3, 55, 55, 64)])
+def test_pool_backward_bias_matches_plain_backward_and_column_sums(shape):
+    import torch
+    L, lib = _lib()
+    B, H, W, Cc = shape
+    Ho, Wo = (H - 3) // 2 + 1, (W - 3) // 2 + 1
+    st = torch.cuda.current_stream().cuda_stream
+    x = torch.randn(B * H * W * Cc, device="cuda").relu().bfloat16()
+    y = torch.empty(B * Ho * Wo * Cc, device="cuda", dtype=torch.bfloat16)
+    arg = torch.empty(B * Ho * Wo * Cc, device="cuda", dtype=torch.uint8)
+    lib.call("pc_maxpool_forward", B, H, W, Cc, 3, 2, x.data_ptr(), y.data_ptr(), arg.data_ptr(), L.PC_BF16, st)
+    gy = torch.randn(B * Ho * Wo * Cc, device="cuda").bfloat16()
+    gx0, gx1 = torch.empty_like(x), torch.empty_like(x)
+    lib.call("pc_maxpool_backward", B, H, W, Cc, 3, 2, gy.data_ptr(), arg.data_ptr(), None, gx0.data_ptr(),
+             L.PC_BF16, st)
+    ws = torch.empty(lib.raw("pc_maxpool_backward_bias_workspace")(Cc), dtype=torch.uint8, device="cuda")
+    gb = torch.empty(Cc, device="cuda")
+    lib.call("pc_maxpool_backward_bias", B, H, W, Cc, 3, 2, gy.data_ptr(), arg.data_ptr(), None, gx1.data_ptr(),
+             L.PC_BF16, gb.data_ptr(), ws.data_ptr(), ws.numel(), st)
+    assert torch.equal(gx0, gx1)
+    want = gx0.view(-1, Cc).double().sum(0)
+    assert float((gb.double() - want).abs().max() / want.abs().max()) < 1e-5
