@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
 // fixed grid walks the 2x2 blocks grid-stride (the thread's 8-channel group is
 // constant because 256 % (C / 8) == 0), each thread sums the bf16 values it
 // stores, the CTA combines its row lanes in a fixed order into part[block][C],
-// and pool_bias_rows_k sums the CTA rows (warp per 8 channels, fixed xor tree).
+// and pool_bias_rows_k sums the CTA rows (a CTA per 8 channels, fixed tree).
 // Deterministic; saves the separate two-pass reduction that re-read gx.
 __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H, int W, int C, int Ho, int Wo,
                                                                     const __nv_bfloat16* __restrict__ gy,
@@ -452,26 +452,29 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H
   }
 }
 
-__global__ void __launch_bounds__(128) pool_bias_rows_k(const float* __restrict__ part, int R, int N,
+// Column sums of the per-CTA partial rows: a CTA per 8 columns, thread r summing
+// rows r, r + 256, ... (float4 pairs), then a fixed shared-memory tree over the 256
+// threads. Deterministic.
+__global__ void __launch_bounds__(256) pool_bias_rows_k(const float* __restrict__ part, int R, int N,
                                                         float* __restrict__ out) {
-  const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (grp >= N / 8) return;
+  __shared__ float sh[256][9];
+  const int grp = blockIdx.x;
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int r = lane; r < R; r += 32) {
+  for (int r = threadIdx.x; r < R; r += 256) {
     const float4* p = reinterpret_cast<const float4*>(part + (long long)r * N + grp * 8);
-    const float4 x = p[0], y = p[1];
+    const float4 x = __ldg(p), y = __ldg(p + 1);
     a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w; a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
+  for (int i = 0; i < 8; ++i) sh[threadIdx.x][i] = a[i];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] += __shfl_xor_sync(0xffffffffu, a[i], o);
-  if (lane < 8) {
-    float v = a[0];
-#pragma unroll
-    for (int i = 1; i < 8; ++i) v = lane == i ? a[i] : v;
-    out[grp * 8 + lane] = v;
+      for (int i = 0; i < 8; ++i) sh[threadIdx.x][i] += sh[threadIdx.x + w][i];
+    __syncthreads();
   }
+  if (threadIdx.x < 8) out[grp * 8 + threadIdx.x] = sh[0][threadIdx.x];
 }
 
 // k=3, s=2 (every AlexNet pool): one thread per 2x2 input block (Y, X) and 8
@@ -1052,7 +1055,7 @@ extern "C" int pc_maxpool_backward_bias(int B, int H, int W, int C, int k, int s
   maxpool_bwd_bf16_k3s2_bias_k<<<POOL_BIAS_CTAS, 256, 0, S(st)>>>(
       B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(gy), argmax, static_cast<const __nv_bfloat16*>(mask),
       static_cast<__nv_bfloat16*>(gx), part);
-  pool_bias_rows_k<<<(C / 8 + 3) / 4, 128, 0, S(st)>>>(part, POOL_BIAS_CTAS, C, gb);
+  pool_bias_rows_k<<<C / 8, 256, 0, S(st)>>>(part, POOL_BIAS_CTAS, C, gb);
   count_launches(1);
   PC_CUDA_CHECK_LAUNCH("maxpool_backward_bias");
   return PC_OK;
