@@ -49,7 +49,13 @@ enum AMode {
   // CTA): a narrow layer whose filters fit (the space-to-depth input layer: 9 taps
   // x 64 channels x 96 filters = 54 KB per SM of a CTA pair); stages carry only
   // the input window
-  A_HALO_KR = 9
+  A_HALO_KR = 9,
+  // weight gradient on a CTA pair with two M accumulators per CTA (M = 512 rows per
+  // pair tile, N = 256 filters, TMEM 2 x 256 columns): the B tile (upstream
+  // gradient) each SM loads feeds twice the MMA work — 25% fewer operand bytes per
+  // FLOP than one 256 x 256 accumulator per pair, for the operand-bound N = 256
+  // weight gradients (conv2, conv5); the epilogue is not overlapped (512 columns)
+  A_IM2COL_MN2 = 10
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
@@ -344,9 +350,9 @@ template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM
 constexpr int GATHER_THREADS = 512;
 constexpr int GR = 1024 / GATHER_THREADS;  // rows (fwd/dgrad) or pixel rows (wgrad) per gather thread
 template <int AM> constexpr bool a_is_mn() {
-  return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN || AM == A_IM2COL_MN5;
+  return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2;
 }
-template <int AM> constexpr int macc_of() { return AM == A_IM2COL_MN5 ? 5 : 1; }
+template <int AM> constexpr int macc_of() { return AM == A_IM2COL_MN5 ? 5 : AM == A_IM2COL_MN2 ? 2 : 1; }
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
 template <int BN, int CG>
@@ -430,7 +436,8 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
     tc_fence_after();
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
     for (int a = 0; a < MACC; ++a) {  // MACC > 1: accumulator a = rows [128 a, 128 a + 128), TMEM column a * N
-    long long m = (long long)tc.m0 + (long long)rank * BM + a * BM + row;
+    // accumulator a of CTA `rank`: rows [a * 128 * CG + rank * 128, ... + 128) of the tile
+    long long m = (long long)tc.m0 + (long long)a * BM * CG + (long long)rank * BM + row;
     bool mrow = m < p.M;
     if (p.m_cp) {
       const long long tap = m / p.m_cp, c = m - tap * p.m_cp;
@@ -998,10 +1005,12 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         kj = ktap - ki * p.i2c_k;
         kblk = kc / p.i2c_cs;
         kcoff = kc - kblk * p.i2c_cs;
-      } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5) {
+      } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2) {
 #pragma unroll
         for (int cch = 0; cch < ACH; ++cch) {
-          int kk = m0 + 64 * cch;
+          // chunk cch = rows of accumulator cch / 2 (CTA pair: interleaved with the peer's)
+          int kk = CG == 2 && MACC > 1 ? tc.m0 + (cch >> 1) * (BM * CG) + (int)rank * BM + (cch & 1) * 64
+                                       : m0 + 64 * cch;
           if (kk >= p.M) kk = 0;  // rows past M are discarded by the epilogue
           const int cpt = p.m_cp ? p.m_cp : p.i2c_C;  // M rows per tap
           const int c = kk % cpt, ij = kk / cpt;
@@ -1060,7 +1069,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
                               t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
                               (uint16_t)ki);
-          } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5) {
+          } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2) {
             // K block = 64 consecutive pixels; M = (i, j, c): 64-channel chunks
 #pragma unroll
             for (int cch = 0; cch < ACH; ++cch)
@@ -1096,7 +1105,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           }
         } else if constexpr (HALO) {
           if (++kj == p.i2c_k) { kj = 0; kc += BK; }
-        } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5) {
+        } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2) {
           pox += BK;
           while (pox >= p.i2c_Wo) {
             pox -= p.i2c_Wo;
@@ -2030,7 +2039,15 @@ static long long choose_splits(long long tiles, long long kbs, int bn, int cg = 
 struct WgradPlan {
   Tile t;
   int splits;
+  bool mn2;  // A_IM2COL_MN2: two M accumulators per CTA of the pair
 };
+static bool mn2_enabled() {
+  static const int on = [] {
+    const char* e = getenv("PC_MN2");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
 // Weight gradient of an unblocked input whose channel count is not a multiple
 // of 64 (conv2: 96) by TMA im2col with zero-filled padding channels: a third more
 // MMA rows than the cp.async gather, but the operand arrives at TMA rate.
@@ -2054,11 +2071,14 @@ static WgradPlan wgrad_plan(const pc_conv_geom& g) {
   // N = 384 (conv3 / conv4 filters): two 192-wide pair tiles instead of 256 + 128
   const int pbn = g.N <= 128 ? 128 : (i2c && g.N % 192 == 0 && g.N % 256 != 0 && mn192_enabled()) ? 192 : 256;
   const Tile t = pair ? Tile{pbn, 2} : Tile{bn_for_mn(g.N), 1};
-  const long long tiles = ((Kc + BM * t.cg - 1) / (BM * t.cg)) * ((g.N + t.bn - 1) / t.bn);
+  // N = 256 on TMA im2col (conv2, conv5): 512-row pair tiles, two accumulators per CTA
+  const bool mn2 = pair && i2c && g.N == 256 && mn2_enabled();
+  const long long rows = BM * t.cg * (mn2 ? 2 : 1);
+  const long long tiles = ((Kc + rows - 1) / rows) * ((g.N + t.bn - 1) / t.bn);
   const long long kbs = (P + BK - 1) / BK;
-  long long sp = choose_splits(tiles, kbs, t.bn, t.cg);
+  long long sp = choose_splits(tiles, kbs, t.bn * (mn2 ? 2 : 1), t.cg);
   const long long per = (kbs + sp - 1) / sp;
-  return {t, (int)((kbs + per - 1) / per)};
+  return {t, (int)((kbs + per - 1) / per), mn2};
 }
 
 static bool macc_wgrad_ok(const pc_conv_geom& g);
@@ -2144,8 +2164,13 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   p.out = splits > 1 ? static_cast<void*>(part) : static_cast<void*>(gw);
   p.split_stride = splits > 1 ? (long long)g.N * Kc : 0;
 
-  rc = i2c ? launch_mn<A_IM2COL_MN, EPI_F32_T>(p, wp.t, splits, st)
-           : launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, wp.t, splits, st);
+  if (wp.mn2) {
+    p.macc_chunks = 4;  // every chunk row exists or is clamped (rows past M are discarded)
+    rc = launch<A_IM2COL_MN2, B_TMA_MN, EPI_F32_T, 256, 4, 2>(p, splits, st);
+  } else {
+    rc = i2c ? launch_mn<A_IM2COL_MN, EPI_F32_T>(p, wp.t, splits, st)
+             : launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, wp.t, splits, st);
+  }
   if (rc) return rc;
   if (splits == 1) return upd ? apply_sgd(gw, (long long)g.N * Kc, upd, st) : PC_OK;
   return reduce_partials(part, splits, (long long)g.N * Kc, gw, st, upd);
