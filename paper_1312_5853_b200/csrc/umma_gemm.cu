@@ -451,7 +451,10 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
       mrow = mrow && yy < p.halo_R && y < p.i2c_Ho && xx < p.i2c_Wo;
       m = ((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx;
     }
-    const uint32_t tbase = tmem + acc * TCOLS + (MACC > 1 ? a * p.N : 0) + ((uint32_t)(quad * 32) << 16);
+    // accumulator stride: A_IM2COL_MN5 packs its 5 accumulators at p.N columns (N <= 96);
+    // A_IM2COL_MN2 (MACC == 2) gives each a BN-wide (tmem_cols) slot
+    const uint32_t tbase = tmem + acc * TCOLS + (MACC == 2 ? a * tmem_cols<BN>() : MACC > 1 ? a * p.N : 0) +
+                           ((uint32_t)(quad * 32) << 16);
     const long long rowoff = m * p.o_ld;
     // (blk, rem) of output column n = n0 + c0 in a channel-blocked view (o_cb % 8 == 0)
     long long n = (long long)tc.n0 + grp * 16;
@@ -867,7 +870,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   constexpr int B_STAGE_BYTES = b_rows<BN, CG, B_MN>() * BK * 2;
   constexpr int MACC = macc_of<AM>();
   // MACC > 1: MMA N = p.N (<= BN, the B load width), accumulator a at TMEM column a * p.N
-  const uint32_t IDESC = MACC > 1 ? ((make_idesc<BN, A_MN, B_MN, CG>() & ~(0x3Fu << 17)) | ((uint32_t)(p.N >> 3) << 17))
+  const uint32_t IDESC = MACC > 2 ? ((make_idesc<BN, A_MN, B_MN, CG>() & ~(0x3Fu << 17)) | ((uint32_t)(p.N >> 3) << 17))
                                   : make_idesc<BN, A_MN, B_MN, CG>();
   constexpr int TCOLS = MACC > 1 ? 512 : tmem_cols<BN>();
   constexpr int ACC = MACC > 1 ? 1 : acc_count<BN>();
@@ -1322,7 +1325,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
                 const uint64_t aa = ad + (uint64_t)((a * A_STAGE_BYTES) >> 4);
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
-                  tc_mma<CG>(tacc + a * p.N, aa + kk * A_KSTEP, bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+                  tc_mma<CG>(tacc + (MACC == 2 ? a * tmem_cols<BN>() : a * p.N), aa + kk * A_KSTEP, bd + kk * B_KSTEP,
+                             IDESC, (it > 0 || kk > 0) ? 1u : 0u);
               }
             } else {
 #pragma unroll
@@ -2072,7 +2076,7 @@ static WgradPlan wgrad_plan(const pc_conv_geom& g) {
   const int pbn = g.N <= 128 ? 128 : (i2c && g.N % 192 == 0 && g.N % 256 != 0 && mn192_enabled()) ? 192 : 256;
   const Tile t = pair ? Tile{pbn, 2} : Tile{bn_for_mn(g.N), 1};
   // N = 256 on TMA im2col (conv2, conv5): 512-row pair tiles, two accumulators per CTA
-  const bool mn2 = pair && i2c && g.N == 256 && mn2_enabled();
+  const bool mn2 = pair && i2c && (g.N == 256 || (g.N % 192 == 0 && g.N % 256 != 0)) && mn2_enabled();
   const long long rows = BM * t.cg * (mn2 ? 2 : 1);
   const long long tiles = ((Kc + rows - 1) / rows) * ((g.N + t.bn - 1) / t.bn);
   const long long kbs = (P + BK - 1) / BK;
@@ -2166,7 +2170,8 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
 
   if (wp.mn2) {
     p.macc_chunks = 4;  // every chunk row exists or is clamped (rows past M are discarded)
-    rc = launch<A_IM2COL_MN2, B_TMA_MN, EPI_F32_T, 256, 4, 2>(p, splits, st);
+    rc = wp.t.bn == 192 ? launch<A_IM2COL_MN2, B_TMA_MN, EPI_F32_T, 192, 4, 2>(p, splits, st)
+                        : launch<A_IM2COL_MN2, B_TMA_MN, EPI_F32_T, 256, 4, 2>(p, splits, st);
   } else {
     rc = i2c ? launch_mn<A_IM2COL_MN, EPI_F32_T>(p, wp.t, splits, st)
              : launch_mn<A_GATHER_WGRAD, EPI_F32_T>(p, wp.t, splits, st);
