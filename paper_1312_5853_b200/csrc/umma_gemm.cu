@@ -55,7 +55,11 @@ enum AMode {
   // gradient) each SM loads feeds twice the MMA work — 25% fewer operand bytes per
   // FLOP than one 256 x 256 accumulator per pair, for the operand-bound N = 256
   // weight gradients (conv2, conv5); the epilogue is not overlapped (512 columns)
-  A_IM2COL_MN2 = 10
+  A_IM2COL_MN2 = 10,
+  // A_IM2COL_MN2 over 32-channel chunks (64B swizzle, MN-major): M rows = (tap,
+  // 32-channel group) units with no padding for a channel count that is a multiple
+  // of 32 but not of 64 (conv2's 96: 2400 rows instead of 25 x 128 = 3200)
+  A_IM2COL_MN2_32 = 11
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
@@ -117,6 +121,8 @@ struct alignas(64) Params {
   // bytes for the layer, whose GEMMs are limited by operand delivery
   int half_chunk;
   CUtensorMap tma_a32, tma_b32;
+  // A_IM2COL_MN2_32: 32-channel groups per tap (M row m -> tap (m/32)/m_grp, group (m/32)%m_grp)
+  int m_grp;
 };
 
 // Debug timeline: slot s of tile lt of CTA b (first TRACE_TILES tiles).
@@ -350,9 +356,12 @@ template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM
 constexpr int GATHER_THREADS = 512;
 constexpr int GR = 1024 / GATHER_THREADS;  // rows (fwd/dgrad) or pixel rows (wgrad) per gather thread
 template <int AM> constexpr bool a_is_mn() {
-  return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2;
+  return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 ||
+         AM == A_IM2COL_MN2_32;
 }
-template <int AM> constexpr int macc_of() { return AM == A_IM2COL_MN5 ? 5 : AM == A_IM2COL_MN2 ? 2 : 1; }
+template <int AM> constexpr int macc_of() {
+  return AM == A_IM2COL_MN5 ? 5 : (AM == A_IM2COL_MN2 || AM == A_IM2COL_MN2_32) ? 2 : 1;
+}
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
 template <int BN, int CG>
@@ -443,6 +452,10 @@ __device__ __forceinline__ void epilogue(const Params& p, uint32_t tmem, uint64_
       const long long tap = m / p.m_cp, c = m - tap * p.m_cp;
       mrow = mrow && c < p.i2c_C;
       m = tap * p.i2c_C + c;
+    }
+    if (p.m_grp) {  // A_IM2COL_MN2_32: row (unit = (tap, 32-channel group), c) -> tap * C + group * 32 + c
+      const long long unit = m >> 5, tap = unit / p.m_grp;
+      m = tap * p.i2c_C + (unit - tap * p.m_grp) * 32 + (m & 31);
     }
     if constexpr (HALO) {  // TMEM row -> (image, output row, column) of this CTA's halo tile
       const int tile = (tc.m0 + (int)rank * BM) / BM;
@@ -981,7 +994,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       // A_IM2COL_K: tile's first output pixel (fixed) and the K position (c, i, j) of kb
       int t_b = 0, t_oy = 0, t_ox = 0, kc = 0, ki = 0, kj = 0, kblk = 0, kcoff = 0, ktap = 0;
       // A_IM2COL_MN: per-chunk (i, j, blk, coff) of the tile's M rows (fixed) and kb's pixel (b, oy, ox)
-      constexpr int ACH = MACC * BM / 64;  // A chunks per stage
+      constexpr bool A32 = AM == A_IM2COL_MN2_32;
+      constexpr int ACH = A32 ? MACC * BM / 32 : MACC * BM / 64;  // A chunks per stage
       int ci[ACH], cj[ACH], cblk[ACH], ccoff[ACH];
       int pb = 0, poy = 0, pox = 0;
       // A_HALO_K: this CTA's tile (image hb, first output row hy0); K walks chunk-major
@@ -1008,15 +1022,24 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         kj = ktap - ki * p.i2c_k;
         kblk = kc / p.i2c_cs;
         kcoff = kc - kblk * p.i2c_cs;
-      } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2) {
+      } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32) {
 #pragma unroll
         for (int cch = 0; cch < ACH; ++cch) {
-          // chunk cch = rows of accumulator cch / 2 (CTA pair: interleaved with the peer's)
-          int kk = CG == 2 && MACC > 1 ? tc.m0 + (cch >> 1) * (BM * CG) + (int)rank * BM + (cch & 1) * 64
-                                       : m0 + 64 * cch;
+          // chunk cch = rows of accumulator cch / 2 (A32: cch / 4) (CTA pair: interleaved with the peer's)
+          int kk = A32 ? tc.m0 + (cch >> 2) * (BM * CG) + (int)rank * BM + (cch & 3) * 32
+                   : CG == 2 && MACC > 1 ? tc.m0 + (cch >> 1) * (BM * CG) + (int)rank * BM + (cch & 1) * 64
+                                         : m0 + 64 * cch;
           if (kk >= p.M) kk = 0;  // rows past M are discarded by the epilogue
-          const int cpt = p.m_cp ? p.m_cp : p.i2c_C;  // M rows per tap
-          const int c = kk % cpt, ij = kk / cpt;
+          int c, ij;
+          if constexpr (A32) {
+            const int unit = kk >> 5;
+            ij = unit / p.m_grp;
+            c = (unit - ij * p.m_grp) * 32;
+          } else {
+            const int cpt = p.m_cp ? p.m_cp : p.i2c_C;  // M rows per tap
+            c = kk % cpt;
+            ij = kk / cpt;
+          }
           ci[cch] = ij / p.i2c_k;
           cj[cch] = ij - ci[cch] * p.i2c_k;
           cblk[cch] = c / p.i2c_cs;
@@ -1072,12 +1095,13 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
                               t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
                               (uint16_t)ki);
-          } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2) {
-            // K block = 64 consecutive pixels; M = (i, j, c): 64-channel chunks
+          } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32) {
+            // K block = 64 consecutive pixels; M = (i, j, c): 64-channel chunks (A32: 32-channel)
 #pragma unroll
             for (int cch = 0; cch < ACH; ++cch)
-              if (MACC == 1 || cch < p.macc_chunks)
-              tma_im2col_5d<CG>(&p.tma_a, &full[s], smem_u32(sA + s * A_STAGE) + cch * (64 * BK * 2),
+              if (MACC == 1 || A32 || cch < p.macc_chunks)
+              tma_im2col_5d<CG>(A32 ? &p.tma_a32 : &p.tma_a, &full[s],
+                                smem_u32(sA + s * A_STAGE) + cch * ((A32 ? 32 : 64) * BK * 2),
                                 ccoff[cch], pox * p.i2c_s + p.i2c_lw, poy * p.i2c_s + p.i2c_lh, pb, cblk[cch],
                                 (uint16_t)cj[cch], (uint16_t)ci[cch]);
           } else if constexpr (!GATHER) {
@@ -1108,7 +1132,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           }
         } else if constexpr (HALO) {
           if (++kj == p.i2c_k) { kj = 0; kc += BK; }
-        } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2) {
+        } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32) {
           pox += BK;
           while (pox >= p.i2c_Wo) {
             pox -= p.i2c_Wo;
@@ -1258,10 +1282,13 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
     // Warp-uniform loop; one elected lane issues the tcgen05.mma / commit.
     // Descriptors: the stage-0 descriptor plus (byte offset >> 4) of stage / k step.
     if (leader) {
-      const uint64_t a0 = A_MN ? make_desc(smem_u32(sA), 64 * BK * 2, 1024) : make_desc(smem_u32(sA), 16, 1024);
+      // A_IM2COL_MN2_32: MN-major 64B swizzle, 32-element MN groups of 64 K rows (4 KB apart)
+      const uint64_t a0 = AM == A_IM2COL_MN2_32 ? make_desc_sw64(smem_u32(sA), 32 * BK * 2, 512)
+                          : A_MN ? make_desc(smem_u32(sA), 64 * BK * 2, 1024) : make_desc(smem_u32(sA), 16, 1024);
       const uint64_t b0 = B_MN ? make_desc(smem_u32(sB), 64 * BK * 2, 1024) : make_desc(smem_u32(sB), 16, 1024);
       const uint64_t a0h = make_desc_sw64(smem_u32(sA), 16, 512), b0h = make_desc_sw64(smem_u32(sB), 16, 512);
-      constexpr uint32_t A_KSTEP = (A_MN ? 2048 : 32) >> 4, B_KSTEP = (B_MN ? 2048 : 32) >> 4;
+      constexpr uint32_t A_KSTEP = (AM == A_IM2COL_MN2_32 ? 1024 : A_MN ? 2048 : 32) >> 4,
+                         B_KSTEP = (B_MN ? 2048 : 32) >> 4;
       int git = 0, lt = 0;
       if constexpr (BRES) {
         mbar_wait(bres, 0);
@@ -2044,7 +2071,17 @@ struct WgradPlan {
   Tile t;
   int splits;
   bool mn2;  // A_IM2COL_MN2: two M accumulators per CTA of the pair
+  bool g32;  // ... over 32-channel groups (A_IM2COL_MN2_32)
 };
+// 32-channel MN-major groups: unblocked input whose channel count is a multiple of
+// 32 but not of 64 (the 64-channel chunks would carry zero padding). PC_GRP32=0 off.
+static bool grp32_ok(const pc_conv_geom& g) {
+  static const int on = [] {
+    const char* e = getenv("PC_GRP32");
+    return e ? atoi(e) : 1;
+  }();
+  return on && g.C == g.cs && g.C % 64 != 0 && g.C % 32 == 0 && g.C >= 32;
+}
 static bool mn2_enabled() {
   static const int on = [] {
     const char* e = getenv("PC_MN2");
@@ -2065,7 +2102,7 @@ static bool wgrad_pad_ok(const pc_conv_geom& g) {
 
 static WgradPlan wgrad_plan(const pc_conv_geom& g) {
   const bool padded = wgrad_pad_ok(g);
-  const long long Kc = (long long)g.k * g.k * (padded ? (g.C + 63) / 64 * 64 : g.C), P = (long long)g.B * g.Ho * g.Wo;
+  const long long Kc0 = (long long)g.k * g.k * (padded ? (g.C + 63) / 64 * 64 : g.C), P = (long long)g.B * g.Ho * g.Wo;
   const bool i2c = im2col_ok(g.cs, g.C, g.cstride) || padded;
   static const int gather_cg2 = [] {
     const char* e = getenv("PC_GATHER_CG2");
@@ -2078,11 +2115,13 @@ static WgradPlan wgrad_plan(const pc_conv_geom& g) {
   // N = 256 on TMA im2col (conv2, conv5): 512-row pair tiles, two accumulators per CTA
   const bool mn2 = pair && i2c && (g.N == 256 || (g.N % 192 == 0 && g.N % 256 != 0)) && mn2_enabled();
   const long long rows = BM * t.cg * (mn2 ? 2 : 1);
+  const bool g32 = mn2 && grp32_ok(g);
+  const long long Kc = g32 ? (long long)g.k * g.k * g.C : Kc0;
   const long long tiles = ((Kc + rows - 1) / rows) * ((g.N + t.bn - 1) / t.bn);
   const long long kbs = (P + BK - 1) / BK;
   long long sp = choose_splits(tiles, kbs, t.bn * (mn2 ? 2 : 1), t.cg);
   const long long per = (kbs + sp - 1) / sp;
-  return {t, (int)((kbs + per - 1) / per), mn2};
+  return {t, (int)((kbs + per - 1) / per), mn2, g32};
 }
 
 static bool macc_wgrad_ok(const pc_conv_geom& g);
@@ -2168,7 +2207,17 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
   p.out = splits > 1 ? static_cast<void*>(part) : static_cast<void*>(gw);
   p.split_stride = splits > 1 ? (long long)g.N * Kc : 0;
 
-  if (wp.mn2) {
+  if (wp.g32) {
+    p.m_cp = 0;
+    p.M = Kc;
+    p.m_grp = g.C / 32;
+    rc = make_im2col_map(&p.tma_a32, x, g.cs, g.W, g.H, g.B, 1, g.cstride, 64, -g.pad, -g.pad,
+                         g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride, 32);
+    if (rc) return rc;
+    set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
+    p.macc_chunks = 4;
+    rc = launch<A_IM2COL_MN2_32, B_TMA_MN, EPI_F32_T, 256, 4, 2>(p, splits, st);
+  } else if (wp.mn2) {
     p.macc_chunks = 4;  // every chunk row exists or is clamped (rows past M are discarded)
     rc = wp.t.bn == 192 ? launch<A_IM2COL_MN2, B_TMA_MN, EPI_F32_T, 192, 4, 2>(p, splits, st)
                         : launch<A_IM2COL_MN2, B_TMA_MN, EPI_F32_T, 256, 4, 2>(p, splits, st);
