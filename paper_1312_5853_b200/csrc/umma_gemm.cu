@@ -59,7 +59,10 @@ enum AMode {
   // A_IM2COL_MN2 over 32-channel chunks (64B swizzle, MN-major): M rows = (tap,
   // 32-channel group) units with no padding for a channel count that is a multiple
   // of 32 but not of 64 (conv2's 96: 2400 rows instead of 25 x 128 = 3200)
-  A_IM2COL_MN2_32 = 11
+  A_IM2COL_MN2_32 = 11,
+  // K-major TMA im2col A (one 16 KB box per stage) with the whole B operand resident
+  // (as A_HALO_KR): deep stage ring, no per-stage filter traffic, coalesced epilogue
+  A_IM2COL_KR = 12
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
@@ -123,6 +126,9 @@ struct alignas(64) Params {
   CUtensorMap tma_a32, tma_b32;
   // A_IM2COL_MN2_32: 32-channel groups per tap (M row m -> tap (m/32)/m_grp, group (m/32)%m_grp)
   int m_grp;
+  int dbg_nostore;  // debug (PC_DEBUG_NOSTORE): the staged bf16 epilogue skips its global stores
+  int dbg_noload;   // debug (PC_DEBUG_NOLOAD): halo producers skip the window loads
+  int epi_direct;   // staged bf16 epilogue: per-row direct stores instead (PC_KR_DIRECT)
 };
 
 // Debug timeline: slot s of tile lt of CTA b (first TRACE_TILES tiles).
@@ -563,6 +569,7 @@ constexpr int F32_STAGE_BYTES = 8 * F32_BOX_BYTES;  // one box per epilogue warp
 template <int EPI, int BN, int STAGES, int CG, int AM, bool BMN = false>
 constexpr bool f32_tma_epi() {
   return EPI == EPI_F32 && !a_is_gather<AM>() && macc_of<AM>() == 1 && AM != A_HALO_K && AM != A_HALO_KR &&
+         AM != A_IM2COL_KR &&
          BN % 32 == 0 &&
          smem_bytes<BN, STAGES, CG, false, 1, BMN>() + 1024 + F32_STAGE_BYTES <= 227 * 1024;
 }
@@ -572,8 +579,10 @@ constexpr int SGD_WARP_BYTES = 4096 + 4096 + 2048;
 constexpr int SGD_STAGE_BYTES = 8 * SGD_WARP_BYTES + 8 * 8;
 template <int EPI, int BN, int STAGES, int CG, int AM, bool BMN = false>
 constexpr int kernel_smem() {
+  if constexpr (AM == A_IM2COL_KR)
+    return 1024 + STAGES * A_STAGE_BYTES + RES_B_BYTES + (2 * STAGES + 5) * 8 + 16 + 1024 + 4 * 64 * BN + 4 * BN;
   if constexpr (AM == A_HALO_KR)
-    return 1024 + STAGES * HALO_R_SLOT_BYTES + RES_B_BYTES + (2 * STAGES + 5) * 8 + 16 + 1024 + 4 * 64 * BN;
+    return 1024 + STAGES * HALO_R_SLOT_BYTES + RES_B_BYTES + (2 * STAGES + 5) * 8 + 16 + 1024 + 4 * 64 * BN + 4 * BN;
   return smem_bytes<BN, STAGES, CG, AM == A_HALO_K, macc_of<AM>(), BMN>() +
          (f32_tma_epi<EPI, BN, STAGES, CG, AM, BMN>() ? 1024 + F32_STAGE_BYTES : 0) +
          (EPI == EPI_SGD ? 1024 + SGD_STAGE_BYTES : 0);
@@ -771,7 +780,7 @@ __device__ __forceinline__ void epilogue_f32_tma(const Params& p, uint32_t tmem,
 // the NHWC output; virtual columns x >= Wo are skipped. The accumulator is
 // released as soon as it is read. (Each lane storing its own 192-byte row kept
 // this 96-column layer epilogue-bound.)
-template <int BN, int CG>
+template <int BN, int CG, bool LINEAR = false>
 __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
                                                    int unit, int units, uint32_t rank, int quad, int grp, int lane,
                                                    uint8_t* box) {
@@ -781,6 +790,14 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
   static_assert(HALF % 16 == 0, "16-column TMEM loads");
   const uint32_t sbox = smem_u32(box);
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+  // bias of the (single) N tile staged in shared memory once: the per-tile loop reads it
+  // with broadcast LDS instead of 48 dependent-latency global loads per thread
+  float* sbias = reinterpret_cast<float*>(box + (4 - quad) * (64 * BN));  // after the 4 quadrant boxes
+  {
+    const int et = (grp * 4 + quad) * 32 + lane;  // 0..255 over the 8 epilogue warps
+    for (int c = et; c < BN; c += 256) sbias[c] = (p.bias && c < p.N) ? __ldg(p.bias + c) : 0.f;
+    asm volatile("bar.sync 5, 256;" ::: "memory");
+  }
   int lt = 0;
   for (int t = unit; t < p.tiles; t += units, ++lt) {
     const TileCoord tc = tile_coord<CG>(p, t, BN);
@@ -805,12 +822,36 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
     const int n0 = tc.n0 + grp * HALF;
 #pragma unroll
     for (int q = 0; q < HALF; ++q) {
-      float val = v[q];
-      if (p.bias) val += __ldg(p.bias + n0 + q);
+      float val = v[q] + sbias[n0 - tc.n0 + q];
       if (p.relu) val = val > 0.f ? val : 0.f;
       v[q] = val;
     }
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 12);
+    if (p.epi_direct) {  // experiment (PC_KR_DIRECT): each lane stores its own row's 16-byte chunks
+      const int row = quad * 32 + lane;
+      long long m = -1;
+      if constexpr (LINEAR) {
+        const long long mm = (long long)tc.m0 + (long long)rank * BM + row;
+        if (mm < p.M) m = mm;
+      } else {
+        const int tile = (tc.m0 + (int)rank * BM) / BM;
+        const int hb = tile / p.halo_tpi, yy = row / p.halo_Wv, xx = row - yy * p.halo_Wv;
+        const int y = (tile - hb * p.halo_tpi) * p.halo_R + yy;
+        if (yy < p.halo_R && y < p.i2c_Ho && xx < p.i2c_Wo) m = ((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx;
+      }
+      if (m >= 0) {
+        __nv_bfloat16* dst = out + m * BN + grp * HALF;
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          uint4 u;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+          *reinterpret_cast<uint4*>(dst + 8 * j) = u;
+        }
+      }
+      continue;
+    }
     // the previous tile's stores have read the box (64 threads: this quadrant's two warps)
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 13);
@@ -830,18 +871,27 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 14);
     const int tile = (tc.m0 + (int)rank * BM) / BM;
-    const int hb = tile / p.halo_tpi, y0 = (tile - hb * p.halo_tpi) * p.halo_R;
+    const int hb = LINEAR ? 0 : tile / p.halo_tpi, y0 = LINEAR ? 0 : (tile - hb * p.halo_tpi) * p.halo_R;
 #pragma unroll
     for (int g8 = 0; g8 < 2; ++g8) {
       const int r0 = 16 * grp + 8 * g8;  // first of this group's 8 rows within the quadrant
-      const int row = quad * 32 + r0, yy = row / p.halo_Wv, xx = row - yy * p.halo_Wv, y = y0 + yy;
-      if (yy >= p.halo_R || y >= p.i2c_Ho) continue;
-      const int nrow = min(8, p.i2c_Wo - xx);
-      __nv_bfloat16* dst = out + (((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx) * BN;
+      int nrow;
+      __nv_bfloat16* dst;
+      if constexpr (LINEAR) {  // rows = consecutive output pixels
+        const long long m = (long long)tc.m0 + (long long)rank * BM + quad * 32 + r0;
+        if (m >= p.M) continue;
+        nrow = (int)min(8LL, (long long)p.M - m);
+        dst = out + m * BN;
+      } else {
+        const int row = quad * 32 + r0, yy = row / p.halo_Wv, xx = row - yy * p.halo_Wv, y = y0 + yy;
+        if (yy >= p.halo_R || y >= p.i2c_Ho) continue;
+        nrow = min(8, p.i2c_Wo - xx);
+        dst = out + (((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx) * BN;
+      }
 #pragma unroll
       for (int i = 0; i < (8 * RCH + 31) / 32; ++i) {
         const int c = i * 32 + lane, r = c / RCH, part = c - r * RCH;
-        if (r < nrow) {
+        if (r < nrow && !p.dbg_nostore) {
           uint4 u;
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
@@ -891,15 +941,17 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr bool BRES = AM == A_HALO_KR;
-  constexpr bool HALO = AM == A_HALO_K || BRES;
+  constexpr bool IKR = AM == A_IM2COL_KR;
+  constexpr bool BRES = AM == A_HALO_KR || IKR;
+  constexpr bool HALO = AM == A_HALO_K || AM == A_HALO_KR;
   // stage s: A at sA + s * A_STRIDE, B at sB + s * B_STRIDE (a halo stage holds its
   // window and its k B tiles contiguously; BRES: stages hold windows only, the B
   // tiles of every (k-block, filter row) sit after the ring)
-  constexpr int A_STRIDE = BRES ? HALO_R_SLOT_BYTES : HALO ? halo_stage_bytes<BN, CG>() : A_STAGE;
+  constexpr int A_STRIDE = IKR ? A_STAGE_BYTES : BRES ? HALO_R_SLOT_BYTES : HALO ? halo_stage_bytes<BN, CG>() : A_STAGE;
   constexpr int B_STRIDE = BRES ? 0 : HALO ? halo_stage_bytes<BN, CG>() : B_STAGE_BYTES;
   uint8_t* sA = smem;
-  uint8_t* sB = BRES ? smem + STAGES * HALO_R_SLOT_BYTES : HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE;
+  uint8_t* sB = IKR ? smem + STAGES * A_STAGE_BYTES
+               : BRES ? smem + STAGES * HALO_R_SLOT_BYTES : HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(BRES ? sB + RES_B_BYTES
                                                     : smem + STAGES * (HALO ? halo_stage_bytes<BN, CG>()
                                                                             : A_STAGE + B_STAGE_BYTES));
@@ -974,13 +1026,19 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       // resident B: tile r = kb * k + i (k-block kb = (chunk, filter column j), filter
       // row i) holds this CTA's BNC filters at K offset ((i k + j) C + 64 chunk)
       if (elect_one()) {
-        const int nt = p.num_kb * p.i2c_k;
+        const int nt = IKR ? p.num_kb : p.num_kb * p.i2c_k;
         if (leader) mbar_arrive_expect_tx(bres, CG * nt * B_STAGE_BYTES);
         for (int r = 0; r < nt; ++r) {
-          const int kb = r / p.i2c_k, i = r - kb * p.i2c_k;
-          const int ch = kb / p.i2c_k, j = kb - ch * p.i2c_k;
-          tma_load_3d<CG>(&p.tma_b, bres, smem_u32(sB + r * B_STAGE_BYTES), (i * p.i2c_k + j) * p.i2c_C + ch * BK,
-                          (int)rank * BNC, 0);
+          int kcoord;
+          if constexpr (IKR) {  // k-block r = (tap, 64-channel chunk)
+            const int tap = r / p.i2c_cpt;
+            kcoord = tap * p.i2c_C + (r - tap * p.i2c_cpt) * BK;
+          } else {              // (k-block (chunk, column j), filter row i)
+            const int kb = r / p.i2c_k, i = r - kb * p.i2c_k;
+            const int ch = kb / p.i2c_k, j = kb - ch * p.i2c_k;
+            kcoord = (i * p.i2c_k + j) * p.i2c_C + ch * BK;
+          }
+          tma_load_3d<CG>(&p.tma_b, bres, smem_u32(sB + r * B_STAGE_BYTES), kcoord, (int)rank * BNC, 0);
         }
       }
       __syncwarp();
@@ -1007,7 +1065,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         kc = (tc.kb_begin / p.i2c_k) * BK;
         kj = tc.kb_begin - (tc.kb_begin / p.i2c_k) * p.i2c_k;
       }
-      if constexpr (AM == A_IM2COL_K) {
+      if constexpr (AM == A_IM2COL_K || IKR) {
         // a CTA whose rows all lie past M (second half of a partial pair tile) loads
         // the first pixels instead (its rows are discarded by the epilogue): an
         // im2col start pixel outside the tensor faults the TMA unit
@@ -1058,7 +1116,9 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         mbar_wait(&empty[s], ph ^ 1);
         const long long c1 = p.trace ? clk() : 0;
         const int kb = tc.kb_begin + it;
-        if (HALO && elect_one()) {
+        if (HALO && p.dbg_noload) {  // debug: MMA + pipeline cost without operand traffic
+          if (leader && elect_one()) mbar_arrive(&full[s]);
+        } else if (HALO && elect_one()) {
           // the window for (chunk, column j) and the B tiles of taps (0..k-1, j)
           if (leader) mbar_arrive_expect_tx(&full[s], CG * (p.halo_bytes + (BRES ? 0 : p.i2c_k * B_STAGE_BYTES)));
           const uint32_t st0 = smem_u32(sA + s * A_STRIDE);
@@ -1071,11 +1131,14 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           // A_IM2COL_K: the k-block of a last chunk with <= 32 channels moves 32-channel boxes
           const bool half = AM == A_IM2COL_K && p.half_chunk && kc + 32 >= p.i2c_C;
           if (leader)
-            mbar_arrive_expect_tx(&full[s], half ? CG * (B_STAGE_BYTES + A_STAGE_BYTES) / 2
+            mbar_arrive_expect_tx(&full[s], IKR ? CG * A_STAGE_BYTES
+                                  : half ? CG * (B_STAGE_BYTES + A_STAGE_BYTES) / 2
                                                  : CG * (B_STAGE_BYTES + (GATHER ? 0 : MACC > 1 ? p.macc_chunks * 64 * BK * 2
                                                                                        : A_STAGE_BYTES)));
           const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
-          if constexpr (B_MN) {
+          if constexpr (IKR) {
+            // B resident
+          } else if constexpr (B_MN) {
             if (p.b_chunked) {  // one op: {64 cols, BK rows, BNC/64 chunks} of the chunked view
               tma_load_4d<CG>(&p.tma_b, &full[s], dB, 0, kb * BK, blk_off(n0, p.b_cb) >> 6, blk_idx(n0, p.b_cb));
             } else {
@@ -1090,7 +1153,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             const int k = AM == A_IM2COL_K ? ktap * p.i2c_C + kc : kb * BK;
             tma_load_3d<CG>(half ? &p.tma_b32 : &p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
           }
-          if constexpr (AM == A_IM2COL_K) {
+          if constexpr (AM == A_IM2COL_K || IKR) {
             // 128 output pixels from the tile's first pixel; K block = 64 (or 32) channels of tap (i, j)
             tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
                               t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
@@ -1121,7 +1184,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         }
         __syncwarp();
         // advance the im2col K position / pixel walk to the next k-block
-        if constexpr (AM == A_IM2COL_K) {
+        if constexpr (AM == A_IM2COL_K || IKR) {
           kc += BK;
           kcoff += BK;
           if (kcoff >= p.i2c_cs) { kcoff = 0; ++kblk; }
@@ -1332,7 +1395,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (elect_one()) {
             const uint64_t ad = (half ? a0h : a0) + (uint64_t)((s * A_STRIDE) >> 4);
-            const uint64_t bd = BRES ? b0 + (uint64_t)(((tc.kb_begin + it) * p.i2c_k * B_STAGE_BYTES) >> 4)
+            const uint64_t bd = BRES ? b0 + (uint64_t)(((tc.kb_begin + it) * (IKR ? 1 : p.i2c_k) * B_STAGE_BYTES) >> 4)
                                      : (half ? b0h : b0) + (uint64_t)((s * B_STRIDE) >> 4);
             if constexpr (HALO) {
               // filter row i: the window shifted by i * Wv rows (multiple of 8), B tile i
@@ -1400,8 +1463,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   } else {
     const int quad = warp & 3, grp = warp >= 6 ? 1 : 0;
     if constexpr (BRES && EPI == EPI_BF16) {
-      epilogue_bf16_halo<BN, CG>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
-                                 f32_boxes + quad * (64 * BN));
+      epilogue_bf16_halo<BN, CG, IKR>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
+                                      f32_boxes + quad * (64 * BN));
     } else if constexpr (EPI == EPI_SGD) {
       static_assert(EPW == 2 && BN % 32 == 0, "fused SGD epilogue: 8 epilogue warps, 32-column groups");
       epilogue_sgd_tma<BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
@@ -1601,6 +1664,21 @@ static int launch(const Params& p, int splits, cudaStream_t st) {
   Params q = p;
   q.trace = g_trace;
   q.mt_rows = BM * CG * macc_of<AM>();
+  static const int nostore = [] {
+    const char* e = getenv("PC_DEBUG_NOSTORE");
+    return e ? atoi(e) : 0;
+  }();
+  q.dbg_nostore = nostore;
+  static const int noload = [] {
+    const char* e = getenv("PC_DEBUG_NOLOAD");
+    return e ? atoi(e) : 0;
+  }();
+  q.dbg_noload = noload;
+  static const int kr_direct = [] {
+    const char* e = getenv("PC_KR_DIRECT");
+    return e ? atoi(e) : 0;
+  }();
+  q.epi_direct = kr_direct;
   if constexpr (f32_tma_epi<EPI, BN, STAGES, CG, AM, BMODE == B_TMA_MN>()) q.out_tma = f32_out_map(&q.tma_out, q, splits);
   q.tiles = ceil_div(p.N, BN) * ceil_div(p.M, q.mt_rows) * splits;
   static const int max_ctas = [] {  // debug: cap the persistent grid (PC_MAX_CTAS)
@@ -1678,7 +1756,15 @@ static Tile pick_mn(int M, int N, bool pair_ok, int splits = 1) {
 
 template <int AM, int EPI>
 static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
-  if constexpr (AM == A_HALO_KR) {  // window stages + resident B (CTA pair, N <= 96)
+  if constexpr (AM == A_IM2COL_KR) {  // 16 KB im2col stages + resident B (CTA pair, N == 96)
+    if (t.cg == 2 && t.bn == 96) return launch<AM, B_TMA_K, EPI, 96, 8, 2>(p, splits, st);
+    PC_REQUIRE(false, PC_ESHAPE, "resident-B im2col: CTA pair with N == 96 only");
+  } else if constexpr (AM == A_HALO_KR) {  // window stages + resident B (CTA pair, N <= 96)
+    static const int kr_stages = [] {  // tuning knob PC_KR_STAGES (4 or 5)
+      const char* e = getenv("PC_KR_STAGES");
+      return e ? atoi(e) : 5;
+    }();
+    if (t.cg == 2 && t.bn <= 96 && kr_stages == 4) return launch<AM, B_TMA_K, EPI, 96, 4, 2>(p, splits, st);
     if (t.cg == 2 && t.bn <= 96) return launch<AM, B_TMA_K, EPI, 96, 5, 2>(p, splits, st);
     PC_REQUIRE(false, PC_ESHAPE, "resident-B halo: CTA pair with N <= 96 only");
   } else if constexpr (AM == A_HALO_K) {  // stages of (window + k B tiles); N <= 128
@@ -1882,6 +1968,31 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   }
   int M = g.B * g.Ho * g.Wo, K = g.k * g.k * g.C;
   Params p = base_params(M, g.N, K);
+  // N = 96 with 64-channel rows whose filters fit in shared memory (the space-to-depth
+  // input layer): TMA im2col A + resident filters (A_IM2COL_KR), opt-in with
+  // PC_I2C_KR=1; by default the resident-filter halo path below (fewer bytes per tile).
+  static const int i2c_kr = [] {  // measured slower than the halo path (141 vs 122 us): opt-in
+    const char* e = getenv("PC_I2C_KR");
+    return e ? atoi(e) : 0;
+  }();
+  if (i2c_kr && g.N == 96 && g.C % BK == 0 && im2col_ok(g.cs, g.C, g.cstride) && cg2_enabled() &&
+      (long long)g.k * g.k * (g.C / BK) * 48 * BK * 2 <= RES_B_BYTES && (M + 2 * BM - 1) / (2 * BM) >= 74) {
+    const Tile t{96, 2};
+    int rc = make_map(&p.tma_b, w, K, g.N, 1, K, 0, t.bn / t.cg);
+    if (!rc) rc = make_im2col_map(&p.tma_a, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, BM, -g.pad, -g.pad,
+                                  g.pad - (g.k - 1), g.pad - (g.k - 1), g.stride);
+    if (rc) return rc;
+    p.b_cb = 0;
+    p.gsrc = static_cast<const __nv_bfloat16*>(x);
+    p.g = g;
+    p.out = y;
+    p.o_ld = g.N;
+    p.bias = bias;
+    p.relu = (flags & PC_RELU) != 0;
+    set_i2c(p, g.C, g.cs, g.k, g.stride, -g.pad, g.Wo, g.Ho);
+    set_i2c_kloop(p, g.C, g.k);
+    return launch_kb<A_IM2COL_KR, EPI_BF16>(p, t, 1, st);
+  }
   bool halo = g.stride == 1 && g.C == g.cs && halo_wanted(g.N, g.k) &&
              setup_halo(p, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo);
   bool res = false;
