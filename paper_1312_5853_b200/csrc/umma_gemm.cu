@@ -62,7 +62,11 @@ enum AMode {
   A_IM2COL_MN2_32 = 11,
   // K-major TMA im2col A (one 16 KB box per stage) with the whole B operand resident
   // (as A_HALO_KR): deep stage ring, no per-stage filter traffic, coalesced epilogue
-  A_IM2COL_KR = 12
+  A_IM2COL_KR = 12,
+  // A_HALO_KR with TWO vertically adjacent halo sub-tiles per CTA (two accumulators of
+  // 128 TMEM columns, still double-buffered): one window per stage covers both, and
+  // every tile boundary (accumulator handoff) is amortised over twice the MMAs
+  A_HALO_KR2 = 13
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
@@ -356,6 +360,7 @@ constexpr int tmem_cols() {
 constexpr int HALO_SLOT_BYTES = 256 * 128, HALO_KMAX = 5;
 // A_HALO_KR: window slots of <= 224 rows and <= 56 KB of resident B tiles
 constexpr int HALO_R_SLOT_BYTES = 224 * 128, RES_B_BYTES = 56 * 1024;
+constexpr int HALO_R2_SLOT_BYTES = 336 * 128;  // A_HALO_KR2: (2 R + k - 1) x Wv <= 336 rows
 template <int AM> constexpr bool a_is_gather() { return AM >= A_GATHER_FWD && AM <= A_GATHER_WGRAD; }
 // cp.async gather producers (warps 6..): 8 warps, each thread 16 B per row for
 // 1024 / GATHER_THREADS rows of the 128 x 64 stage.
@@ -366,7 +371,7 @@ template <int AM> constexpr bool a_is_mn() {
          AM == A_IM2COL_MN2_32;
 }
 template <int AM> constexpr int macc_of() {
-  return AM == A_IM2COL_MN5 ? 5 : (AM == A_IM2COL_MN2 || AM == A_IM2COL_MN2_32) ? 2 : 1;
+  return AM == A_IM2COL_MN5 ? 5 : (AM == A_IM2COL_MN2 || AM == A_IM2COL_MN2_32 || AM == A_HALO_KR2) ? 2 : 1;
 }
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
@@ -569,6 +574,7 @@ constexpr int F32_STAGE_BYTES = 8 * F32_BOX_BYTES;  // one box per epilogue warp
 template <int EPI, int BN, int STAGES, int CG, int AM, bool BMN = false>
 constexpr bool f32_tma_epi() {
   return EPI == EPI_F32 && !a_is_gather<AM>() && macc_of<AM>() == 1 && AM != A_HALO_K && AM != A_HALO_KR &&
+         AM != A_HALO_KR2 &&
          AM != A_IM2COL_KR &&
          BN % 32 == 0 &&
          smem_bytes<BN, STAGES, CG, false, 1, BMN>() + 1024 + F32_STAGE_BYTES <= 227 * 1024;
@@ -579,6 +585,8 @@ constexpr int SGD_WARP_BYTES = 4096 + 4096 + 2048;
 constexpr int SGD_STAGE_BYTES = 8 * SGD_WARP_BYTES + 8 * 8;
 template <int EPI, int BN, int STAGES, int CG, int AM, bool BMN = false>
 constexpr int kernel_smem() {
+  if constexpr (AM == A_HALO_KR2)
+    return 1024 + STAGES * HALO_R2_SLOT_BYTES + RES_B_BYTES + (2 * STAGES + 5) * 8 + 16 + 1024 + 4 * 64 * BN + 4 * BN;
   if constexpr (AM == A_IM2COL_KR)
     return 1024 + STAGES * A_STAGE_BYTES + RES_B_BYTES + (2 * STAGES + 5) * 8 + 16 + 1024 + 4 * 64 * BN + 4 * BN;
   if constexpr (AM == A_HALO_KR)
@@ -780,12 +788,12 @@ __device__ __forceinline__ void epilogue_f32_tma(const Params& p, uint32_t tmem,
 // the NHWC output; virtual columns x >= Wo are skipped. The accumulator is
 // released as soon as it is read. (Each lane storing its own 192-byte row kept
 // this 96-column layer epilogue-bound.)
-template <int BN, int CG, bool LINEAR = false>
+template <int BN, int CG, bool LINEAR = false, int HSUB = 1>
 __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tmem, uint64_t* tfull, uint64_t* tempty,
                                                    int unit, int units, uint32_t rank, int quad, int grp, int lane,
                                                    uint8_t* box) {
-  constexpr int TCOLS = tmem_cols<BN>();
-  constexpr int ACC = acc_count<BN>();
+  constexpr int TCOLS = tmem_cols<BN>() * HSUB;  // one buffer: HSUB sub-tile accumulators
+  constexpr int ACC = HSUB > 1 ? 2 : acc_count<BN>();
   constexpr int HALF = BN / 2, ROWB = BN * 2, CH = HALF * 2 / 16, RCH = ROWB / 16;
   static_assert(HALF % 16 == 0, "16-column TMEM loads");
   const uint32_t sbox = smem_u32(box);
@@ -805,18 +813,22 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
     mbar_wait(&tfull[acc], (lt / ACC) & 1);
     tc_fence_after();
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 5);
-    const uint32_t tbase = tmem + acc * TCOLS + grp * HALF + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+    for (int sub = 0; sub < HSUB; ++sub) {
+    const uint32_t tbase = tmem + acc * TCOLS + sub * tmem_cols<BN>() + grp * HALF + ((uint32_t)(quad * 32) << 16);
     float v[HALF];
 #pragma unroll
     for (int c = 0; c < HALF / 16; ++c) tmem_ld16(tbase + 16 * c, v + 16 * c);
-    tc_fence_before();
-    __syncwarp();
-    if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
-    if (lane == 0) {
-      if constexpr (CG == 1) {
-        mbar_arrive_relaxed(&tempty[acc]);
-      } else {
-        mbar_arrive_cluster_relaxed(&tempty[acc], 0);
+    if (sub == HSUB - 1) {  // every sub-tile read: release the buffer to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 6);
+      if (lane == 0) {
+        if constexpr (CG == 1) {
+          mbar_arrive_relaxed(&tempty[acc]);
+        } else {
+          mbar_arrive_cluster_relaxed(&tempty[acc], 0);
+        }
       }
     }
     const int n0 = tc.n0 + grp * HALF;
@@ -834,9 +846,9 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
         const long long mm = (long long)tc.m0 + (long long)rank * BM + row;
         if (mm < p.M) m = mm;
       } else {
-        const int tile = (tc.m0 + (int)rank * BM) / BM;
+        const int tile = (tc.m0 + (int)rank * HSUB * BM) / (HSUB * BM);
         const int hb = tile / p.halo_tpi, yy = row / p.halo_Wv, xx = row - yy * p.halo_Wv;
-        const int y = (tile - hb * p.halo_tpi) * p.halo_R + yy;
+        const int y = (tile - hb * p.halo_tpi) * p.halo_R * HSUB + sub * p.halo_R + yy;
         if (yy < p.halo_R && y < p.i2c_Ho && xx < p.i2c_Wo) m = ((long long)hb * p.i2c_Ho + y) * p.i2c_Wo + xx;
       }
       if (m >= 0) {
@@ -870,8 +882,9 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
     }
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 14);
-    const int tile = (tc.m0 + (int)rank * BM) / BM;
-    const int hb = LINEAR ? 0 : tile / p.halo_tpi, y0 = LINEAR ? 0 : (tile - hb * p.halo_tpi) * p.halo_R;
+    const int tile = (tc.m0 + (int)rank * HSUB * BM) / (HSUB * BM);
+    const int hb = LINEAR ? 0 : tile / p.halo_tpi;
+    const int y0 = LINEAR ? 0 : (tile - hb * p.halo_tpi) * p.halo_R * HSUB + sub * p.halo_R;
 #pragma unroll
     for (int g8 = 0; g8 < 2; ++g8) {
       const int r0 = 16 * grp + 8 * g8;  // first of this group's 8 rows within the quadrant
@@ -902,7 +915,7 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
       }
     }
     if (quad == 0 && grp == 0 && lane == 0) trace_stamp(p, lt, 15);
-    
+    }  // sub-tiles
   }
 }
 
@@ -935,23 +948,26 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   // MACC > 1: MMA N = p.N (<= BN, the B load width), accumulator a at TMEM column a * p.N
   const uint32_t IDESC = MACC > 2 ? ((make_idesc<BN, A_MN, B_MN, CG>() & ~(0x3Fu << 17)) | ((uint32_t)(p.N >> 3) << 17))
                                   : make_idesc<BN, A_MN, B_MN, CG>();
-  constexpr int TCOLS = MACC > 1 ? 512 : tmem_cols<BN>();
-  constexpr int ACC = MACC > 1 ? 1 : acc_count<BN>();
+  constexpr bool KR2 = AM == A_HALO_KR2;
+  // A_HALO_KR2: per buffer 2 sub-tile accumulators of tmem_cols<BN> columns, double-buffered
+  constexpr int TCOLS = KR2 ? 2 * tmem_cols<BN>() : MACC > 1 ? 512 : tmem_cols<BN>();
+  constexpr int ACC = KR2 ? 2 : MACC > 1 ? 1 : acc_count<BN>();
   constexpr int A_STAGE = MACC * A_STAGE_BYTES;  // this kernel's A bytes per stage (allocated)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr bool IKR = AM == A_IM2COL_KR;
-  constexpr bool BRES = AM == A_HALO_KR || IKR;
-  constexpr bool HALO = AM == A_HALO_K || AM == A_HALO_KR;
+  constexpr bool BRES = AM == A_HALO_KR || IKR || AM == A_HALO_KR2;
+  constexpr bool HALO = AM == A_HALO_K || AM == A_HALO_KR || AM == A_HALO_KR2;
+  constexpr int RSLOT = AM == A_HALO_KR2 ? HALO_R2_SLOT_BYTES : HALO_R_SLOT_BYTES;
   // stage s: A at sA + s * A_STRIDE, B at sB + s * B_STRIDE (a halo stage holds its
   // window and its k B tiles contiguously; BRES: stages hold windows only, the B
   // tiles of every (k-block, filter row) sit after the ring)
-  constexpr int A_STRIDE = IKR ? A_STAGE_BYTES : BRES ? HALO_R_SLOT_BYTES : HALO ? halo_stage_bytes<BN, CG>() : A_STAGE;
+  constexpr int A_STRIDE = IKR ? A_STAGE_BYTES : BRES ? RSLOT : HALO ? halo_stage_bytes<BN, CG>() : A_STAGE;
   constexpr int B_STRIDE = BRES ? 0 : HALO ? halo_stage_bytes<BN, CG>() : B_STAGE_BYTES;
   uint8_t* sA = smem;
   uint8_t* sB = IKR ? smem + STAGES * A_STAGE_BYTES
-               : BRES ? smem + STAGES * HALO_R_SLOT_BYTES : HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE;
+               : BRES ? smem + STAGES * RSLOT : HALO ? smem + HALO_SLOT_BYTES : smem + STAGES * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(BRES ? sB + RES_B_BYTES
                                                     : smem + STAGES * (HALO ? halo_stage_bytes<BN, CG>()
                                                                             : A_STAGE + B_STAGE_BYTES));
@@ -1059,9 +1075,10 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       // A_HALO_K: this CTA's tile (image hb, first output row hy0); K walks chunk-major
       int hb = 0, hy0 = 0;
       if constexpr (HALO) {  // k-block = (channel chunk, filter column j), j fastest
-        const int tile = m0 / BM;
+        // KR2: this CTA's tile = 2 sub-tiles (rows [tc.m0 + rank 256, +256)); halo_tpi counts them
+        const int tile = KR2 ? (tc.m0 + (int)rank * 2 * BM) / (2 * BM) : m0 / BM;
         hb = tile / p.halo_tpi;
-        hy0 = (tile - hb * p.halo_tpi) * p.halo_R;
+        hy0 = (tile - hb * p.halo_tpi) * p.halo_R * (KR2 ? 2 : 1);
         kc = (tc.kb_begin / p.i2c_k) * BK;
         kj = tc.kb_begin - (tc.kb_begin / p.i2c_k) * p.i2c_k;
       }
@@ -1398,15 +1415,19 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             const uint64_t bd = BRES ? b0 + (uint64_t)(((tc.kb_begin + it) * (IKR ? 1 : p.i2c_k) * B_STAGE_BYTES) >> 4)
                                      : (half ? b0h : b0) + (uint64_t)((s * B_STRIDE) >> 4);
             if constexpr (HALO) {
-              // filter row i: the window shifted by i * Wv rows (multiple of 8), B tile i
+              // filter row i: the window shifted by i * Wv rows (multiple of 8), B tile i;
+              // KR2 sub-tile a: further shifted by a * R * Wv rows, accumulator a
               const int k = p.i2c_k;
+#pragma unroll
+              for (int a = 0; a < (KR2 ? 2 : 1); ++a)
               for (int i = 0; i < k; ++i) {
-                const uint64_t ai = ad + (uint64_t)((i * p.halo_Wv * 128) >> 4);
+                const uint64_t ai = ad + (uint64_t)(((a * p.halo_R + i) * p.halo_Wv * 128) >> 4);
                 const uint64_t bi = bd + (uint64_t)((i * B_STAGE_BYTES) >> 4);
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
                   if (kk < nk16)
-                    tc_mma<CG>(tacc, ai + kk * A_KSTEP, bi + kk * B_KSTEP, IDESC, (it > 0 || i > 0 || kk > 0) ? 1u : 0u);
+                    tc_mma<CG>(tacc + a * tmem_cols<BN>(), ai + kk * A_KSTEP, bi + kk * B_KSTEP, IDESC,
+                               (it > 0 || i > 0 || kk > 0) ? 1u : 0u);
               }
             } else if constexpr (MACC > 1) {
               // accumulator a: A rows [128 a, 128 a + 128) of the stage (two 64-row chunks)
@@ -1463,8 +1484,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   } else {
     const int quad = warp & 3, grp = warp >= 6 ? 1 : 0;
     if constexpr (BRES && EPI == EPI_BF16) {
-      epilogue_bf16_halo<BN, CG, IKR>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
-                                      f32_boxes + quad * (64 * BN));
+      epilogue_bf16_halo<BN, CG, IKR, KR2 ? 2 : 1>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
+                                                   f32_boxes + quad * (64 * BN));
     } else if constexpr (EPI == EPI_SGD) {
       static_assert(EPW == 2 && BN % 32 == 0, "fused SGD epilogue: 8 epilogue warps, 32-column groups");
       epilogue_sgd_tma<BN, CG, EPW>(p, tmem, tfull, tempty, unit, units, rank, quad, grp, lane,
@@ -1756,7 +1777,10 @@ static Tile pick_mn(int M, int N, bool pair_ok, int splits = 1) {
 
 template <int AM, int EPI>
 static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
-  if constexpr (AM == A_IM2COL_KR) {  // 16 KB im2col stages + resident B (CTA pair, N == 96)
+  if constexpr (AM == A_HALO_KR2) {  // 42 KB window stages + resident B (CTA pair, N == 96)
+    if (t.cg == 2 && t.bn == 96) return launch<AM, B_TMA_K, EPI, 96, 3, 2>(p, splits, st);
+    PC_REQUIRE(false, PC_ESHAPE, "resident-B halo x2: CTA pair with N == 96 only");
+  } else if constexpr (AM == A_IM2COL_KR) {  // 16 KB im2col stages + resident B (CTA pair, N == 96)
     if (t.cg == 2 && t.bn == 96) return launch<AM, B_TMA_K, EPI, 96, 8, 2>(p, splits, st);
     PC_REQUIRE(false, PC_ESHAPE, "resident-B im2col: CTA pair with N == 96 only");
   } else if constexpr (AM == A_HALO_KR) {  // window stages + resident B (CTA pair, N <= 96)
@@ -1917,25 +1941,29 @@ static bool halo_wanted(int N, int k) {
   }();
   return mode == 2 || (mode == 1 && N <= 128 && k * k >= 16);
 }
-static bool setup_halo(Params& p, const void* in, int B, int Hi, int Wi, int Ci, int k, int lo, int Ho, int Wo) {
+// hsub > 1 (A_HALO_KR2): a CTA tile is hsub vertically adjacent sub-tiles of R rows;
+// the window box spans hsub * R + k - 1 rows and halo_tpi counts CTA tiles.
+static bool setup_halo(Params& p, const void* in, int B, int Hi, int Wi, int Ci, int k, int lo, int Ho, int Wo,
+                       int hsub = 1) {
   const int Wv = (Wo + 7) / 8 * 8;
   if (Wv > 128 || Ci % 8 || Ci < 64 || (reinterpret_cast<uintptr_t>(in) & 15) || !get_encode()) return false;
   const int R = BM / Wv;
   if (BM + (k - 1) * Wv > HALO_SLOT_BYTES / 128 || R + k - 1 > 256 || k > HALO_KMAX) return false;
+  if (hsub > 1 && (hsub * R + k - 1) * Wv * 128 > HALO_R2_SLOT_BYTES) return false;
   cuuint64_t dims[4] = {(cuuint64_t)Ci, (cuuint64_t)Wi, (cuuint64_t)Hi, (cuuint64_t)B};
   cuuint64_t strides[3] = {(cuuint64_t)Ci * 2, (cuuint64_t)Wi * Ci * 2, (cuuint64_t)Hi * Wi * Ci * 2};
-  cuuint32_t box[4] = {64u, (cuuint32_t)Wv, (cuuint32_t)(R + k - 1), 1u};
+  cuuint32_t box[4] = {64u, (cuuint32_t)Wv, (cuuint32_t)(hsub * R + k - 1), 1u};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   if (g_encode(&p.tma_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(in), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   p.halo_R = R;
-  p.halo_tpi = (Ho + R - 1) / R;
+  p.halo_tpi = (Ho + hsub * R - 1) / (hsub * R);
   p.halo_Wv = Wv;
   p.halo_lo = lo;
-  p.halo_bytes = 64 * Wv * (R + k - 1) * 2;
-  p.M = B * p.halo_tpi * BM;  // virtual rows: one 128-row tile per halo tile
+  p.halo_bytes = 64 * Wv * (hsub * R + k - 1) * 2;
+  p.M = B * p.halo_tpi * BM * hsub;  // virtual rows: hsub 128-row sub-tiles per halo tile
   p.i2c_k = k;
   p.i2c_C = Ci;
   p.i2c_Ho = Ho;
@@ -1995,10 +2023,17 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   }
   bool halo = g.stride == 1 && g.C == g.cs && halo_wanted(g.N, g.k) &&
              setup_halo(p, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo);
-  bool res = false;
+  bool res = false, res2 = false;
   if (!halo && g.stride == 1 && g.C == g.cs && g.N <= 96) {
+    static const int kr2 = [] {  // two sub-tiles per CTA (A_HALO_KR2); PC_KR2=0: one
+      const char* e = getenv("PC_KR2");
+      return e ? atoi(e) : 1;
+    }();
     Params q = p;
-    if (setup_halo(q, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo) && halo_res_fits(q, g.N)) {
+    if (kr2 && setup_halo(q, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo, 2) && halo_res_fits(q, g.N)) {
+      p = q;
+      halo = res = res2 = true;
+    } else if (setup_halo(q, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo) && halo_res_fits(q, g.N)) {
       p = q;
       halo = res = true;
     }
@@ -2025,7 +2060,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS,
                PC_ECUDA, "resident-B halo: output tensor map");
     p.out_tma = 1;
-    return launch_kb<A_HALO_KR, EPI_BF16>(p, t, 1, st);
+    return res2 ? launch_kb<A_HALO_KR2, EPI_BF16>(p, t, 1, st) : launch_kb<A_HALO_KR, EPI_BF16>(p, t, 1, st);
   }
   if (halo) return launch_kb<A_HALO_K, EPI_BF16>(p, t, 1, st);
   if (i2c) {

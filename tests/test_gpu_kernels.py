@@ -225,7 +225,10 @@ def _tc_counts():
                                   (2, 128, 31, 31, 96, 5, 1, 2),
                                   # M = 19008 = 74 * 256 + 64: the last CTA pair's second CTA
                                   # has no rows (its im2col start pixel would lie past the batch)
-                                  (297, 64, 8, 8, 128, 3, 1, 1)])
+                                  (297, 64, 8, 8, 128, 3, 1, 1),
+                                  # the space-to-depth input layer at a batch whose pair tiles fill
+                                  # the machine: resident-filter halo forward with two sub-tiles
+                                  (8, 64, 57, 57, 96, 3, 1, 0)])
 def test_conv_bf16_alexnet_shapes_on_tensor_cores(geom):
     from paper_1312_5853_b200 import kernels as K
     b, c, h, w, n, k, s, p = geom
