@@ -66,7 +66,11 @@ enum AMode {
   // A_HALO_KR with TWO vertically adjacent halo sub-tiles per CTA (two accumulators of
   // 128 TMEM columns, still double-buffered): one window per stage covers both, and
   // every tile boundary (accumulator handoff) is amortised over twice the MMAs
-  A_HALO_KR2 = 13
+  A_HALO_KR2 = 13,
+  // A_IM2COL_MN5 on a CTA pair: three M accumulators per CTA (768 rows per pair tile,
+  // N <= 96 packed at p.N columns), the pair sharing the upstream-gradient tile; chunks
+  // of rows past M are not loaded. Input layer weight gradient: 576 x 96.
+  A_IM2COL_MN3P = 14
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
@@ -368,10 +372,11 @@ constexpr int GATHER_THREADS = 512;
 constexpr int GR = 1024 / GATHER_THREADS;  // rows (fwd/dgrad) or pixel rows (wgrad) per gather thread
 template <int AM> constexpr bool a_is_mn() {
   return AM == A_TMA_MN || AM == A_GATHER_WGRAD || AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 ||
-         AM == A_IM2COL_MN2_32;
+         AM == A_IM2COL_MN2_32 || AM == A_IM2COL_MN3P;
 }
 template <int AM> constexpr int macc_of() {
-  return AM == A_IM2COL_MN5 ? 5 : (AM == A_IM2COL_MN2 || AM == A_IM2COL_MN2_32 || AM == A_HALO_KR2) ? 2 : 1;
+  return AM == A_IM2COL_MN5 ? 5 : AM == A_IM2COL_MN3P ? 3
+         : (AM == A_IM2COL_MN2 || AM == A_IM2COL_MN2_32 || AM == A_HALO_KR2) ? 2 : 1;
 }
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
@@ -942,7 +947,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
   constexpr bool A_MN = a_is_mn<AM>();
   constexpr bool B_MN = BMODE == B_TMA_MN;
   constexpr int BNC = BN / CG;  // B rows (N) this CTA loads
-  static_assert(!B_MN || BNC % 32 == 0, "MN-major B is loaded in 64-column chunks");
+  static_assert(!B_MN || BNC % 16 == 0, "MN-major B is loaded in 64-column chunks");
   constexpr int B_STAGE_BYTES = b_rows<BN, CG, B_MN>() * BK * 2;
   constexpr int MACC = macc_of<AM>();
   // MACC > 1: MMA N = p.N (<= BN, the B load width), accumulator a at TMEM column a * p.N
@@ -1064,13 +1069,15 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       long long tr_wait = 0, tr_issue = 0;
       const TileCoord tc = tile_coord<CG>(p, t, BN);
       const int m0 = tc.m0 + (int)rank * BM;     // this CTA's A rows
-      const int n0 = tc.n0 + (int)rank * BNC;    // this CTA's B rows
+      // this CTA's B rows (A_IM2COL_MN3P: the pair MMA has N = p.N <= BN, split in halves)
+      const int n0 = tc.n0 + (int)rank * (AM == A_IM2COL_MN3P ? p.N / 2 : BNC);
       // A_IM2COL_K: tile's first output pixel (fixed) and the K position (c, i, j) of kb
       int t_b = 0, t_oy = 0, t_ox = 0, kc = 0, ki = 0, kj = 0, kblk = 0, kcoff = 0, ktap = 0;
       // A_IM2COL_MN: per-chunk (i, j, blk, coff) of the tile's M rows (fixed) and kb's pixel (b, oy, ox)
       constexpr bool A32 = AM == A_IM2COL_MN2_32;
       constexpr int ACH = A32 ? MACC * BM / 32 : MACC * BM / 64;  // A chunks per stage
       int ci[ACH], cj[ACH], cblk[ACH], ccoff[ACH];
+      bool cvalid[ACH];  // A_IM2COL_MN3P: the chunk holds rows < M (others are not loaded)
       int pb = 0, poy = 0, pox = 0;
       // A_HALO_K: this CTA's tile (image hb, first output row hy0); K walks chunk-major
       int hb = 0, hy0 = 0;
@@ -1097,13 +1104,15 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         kj = ktap - ki * p.i2c_k;
         kblk = kc / p.i2c_cs;
         kcoff = kc - kblk * p.i2c_cs;
-      } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32) {
+      } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32 ||
+                           AM == A_IM2COL_MN3P) {
 #pragma unroll
         for (int cch = 0; cch < ACH; ++cch) {
           // chunk cch = rows of accumulator cch / 2 (A32: cch / 4) (CTA pair: interleaved with the peer's)
           int kk = A32 ? tc.m0 + (cch >> 2) * (BM * CG) + (int)rank * BM + (cch & 3) * 32
                    : CG == 2 && MACC > 1 ? tc.m0 + (cch >> 1) * (BM * CG) + (int)rank * BM + (cch & 1) * 64
                                          : m0 + 64 * cch;
+          cvalid[cch] = kk < p.M;
           if (kk >= p.M) kk = 0;  // rows past M are discarded by the epilogue
           int c, ij;
           if constexpr (A32) {
@@ -1150,6 +1159,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           if (leader)
             mbar_arrive_expect_tx(&full[s], IKR ? CG * A_STAGE_BYTES
                                   : half ? CG * (B_STAGE_BYTES + A_STAGE_BYTES) / 2
+                                  : AM == A_IM2COL_MN3P ? CG * B_STAGE_BYTES + p.macc_chunks * 64 * BK * 2
                                                  : CG * (B_STAGE_BYTES + (GATHER ? 0 : MACC > 1 ? p.macc_chunks * 64 * BK * 2
                                                                                        : A_STAGE_BYTES)));
           const uint32_t dB = smem_u32(sB + s * B_STAGE_BYTES);
@@ -1175,11 +1185,12 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
                               t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
                               (uint16_t)ki);
-          } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32) {
+          } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32 ||
+                               AM == A_IM2COL_MN3P) {
             // K block = 64 consecutive pixels; M = (i, j, c): 64-channel chunks (A32: 32-channel)
 #pragma unroll
             for (int cch = 0; cch < ACH; ++cch)
-              if (MACC == 1 || A32 || cch < p.macc_chunks)
+              if (MACC == 1 || A32 || (AM == A_IM2COL_MN3P ? cvalid[cch] : cch < p.macc_chunks))
               tma_im2col_5d<CG>(A32 ? &p.tma_a32 : &p.tma_a, &full[s],
                                 smem_u32(sA + s * A_STAGE) + cch * ((A32 ? 32 : 64) * BK * 2),
                                 ccoff[cch], pox * p.i2c_s + p.i2c_lw, poy * p.i2c_s + p.i2c_lh, pb, cblk[cch],
@@ -1212,7 +1223,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
           }
         } else if constexpr (HALO) {
           if (++kj == p.i2c_k) { kj = 0; kc += BK; }
-        } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32) {
+        } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32 ||
+                             AM == A_IM2COL_MN3P) {
           pox += BK;
           while (pox >= p.i2c_Wo) {
             pox -= p.i2c_Wo;
@@ -1432,7 +1444,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             } else if constexpr (MACC > 1) {
               // accumulator a: A rows [128 a, 128 a + 128) of the stage (two 64-row chunks)
               for (int a = 0; a < MACC; ++a) {
-                if (2 * a >= p.macc_chunks) break;
+                if (AM == A_IM2COL_MN5 && 2 * a >= p.macc_chunks) break;
                 const uint64_t aa = ad + (uint64_t)((a * A_STAGE_BYTES) >> 4);
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
@@ -2287,9 +2299,19 @@ static bool macc_wgrad_ok(const pc_conv_geom& g) {
   return on && Kc > 2 * BM && Kc <= 5 * BM && g.N <= 128 && g.N % 16 == 0 &&
          (long long)((Kc + BM - 1) / BM) * g.N <= 512 && im2col_ok(g.cs, g.C, g.cstride);
 }
+// The pair variant (A_IM2COL_MN3P): M <= 768 rows in three accumulators per CTA,
+// N <= 96 (3 x N <= 512 TMEM columns; the pair splits B in 64-column halves).
+static bool macc_pair_ok(const pc_conv_geom& g) {
+  static const int on = [] {
+    const char* e = getenv("PC_MACC_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  return on && cg2_enabled() && g.k * g.k * g.C <= 6 * BM && g.N <= 96 && g.N % 16 == 0;
+}
 static int macc_splits(const pc_conv_geom& g) {
   const long long kbs = ((long long)g.B * g.Ho * g.Wo + BK - 1) / BK;
-  long long sp = std::min<long long>(148, std::max<long long>(1, kbs / 16));
+  const int units = macc_pair_ok(g) ? 74 : 148;  // CTA pairs or CTAs
+  long long sp = std::min<long long>(units, std::max<long long>(1, kbs / 16));
   const long long per = (kbs + sp - 1) / sp;
   return (int)((kbs + per - 1) / per);
 }
@@ -2309,7 +2331,9 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
     int splits = macc_splits(g);
     p.kb_per_split = ceil_div(p.num_kb, splits);
     splits = ceil_div(p.num_kb, p.kb_per_split);
-    const Tile t{128, 1};
+    const bool macc_pair = macc_pair_ok(g);
+    // pair: each CTA holds N/2 = 48 of the B columns (one 64-column MN chunk loaded)
+    const Tile t = macc_pair ? Tile{96, 2} : Tile{128, 1};
     int rc = setup_mn_b(p, gy, g.N, P, 1, g.N, 0, t);
     if (rc) return rc;
     p.b_cb = 0;
@@ -2323,7 +2347,12 @@ int umma_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
     p.macc_chunks = (Kc + 63) / 64;
     p.out = splits > 1 ? static_cast<void*>(part) : static_cast<void*>(gw);
     p.split_stride = splits > 1 ? (long long)g.N * Kc : 0;
-    rc = launch<A_IM2COL_MN5, B_TMA_MN, EPI_F32_T, 128, 2, 1>(p, splits, st);
+    if (macc_pair) {
+      p.macc_chunks = (Kc + 63) / 64;  // real 64-row chunks over the whole pair tile
+      rc = launch<A_IM2COL_MN3P, B_TMA_MN, EPI_F32_T, 96, 4, 2>(p, splits, st);
+    } else {
+      rc = launch<A_IM2COL_MN5, B_TMA_MN, EPI_F32_T, 128, 2, 1>(p, splits, st);
+    }
     if (rc) return rc;
     if (splits == 1) return upd ? apply_sgd(gw, (long long)g.N * Kc, upd, st) : PC_OK;
     return reduce_partials(part, splits, (long long)g.N * Kc, gw, st, upd);
