@@ -44,7 +44,11 @@ typedef void* pc_stream_t; /* cudaStream_t */
 
 enum pc_prec { PC_FP32 = 0, PC_BF16 = 1 };
 enum pc_status { PC_OK = 0, PC_ESHAPE = 1, PC_EVALUE = 2, PC_ECUDA = 3, PC_ENCCL = 4 };
-enum pc_conv_flags { PC_RELU = 1, PC_WANT_DX = 2, PC_WANT_DW = 4, PC_MASK_DX = 8, PC_WT_PRESET = 16 };
+enum pc_conv_flags { PC_RELU = 1, PC_WANT_DX = 2, PC_WANT_DW = 4, PC_MASK_DX = 8, PC_WT_PRESET = 16,
+                     /* forward: the last 16 input channels have structural-zero filter
+                      * weights (the space-to-depth input layer: 48 real of 64) — the
+                      * tensor-core path may skip their MMA steps */
+                     PC_ZERO_TAIL16 = 32 };
 
 /* Conv geometry (reference ConvParams + input shape, kernels.py:37-83). */
 typedef struct {

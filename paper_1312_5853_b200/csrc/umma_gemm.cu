@@ -137,6 +137,7 @@ struct alignas(64) Params {
   int dbg_nostore;  // debug (PC_DEBUG_NOSTORE): the staged bf16 epilogue skips its global stores
   int dbg_noload;   // debug (PC_DEBUG_NOLOAD): halo producers skip the window loads
   int epi_direct;   // staged bf16 epilogue: per-row direct stores instead (PC_KR_DIRECT)
+  int zero_tail16;  // halo forward: skip the k16 step of the last 16 channels (PC_ZERO_TAIL16 flag)
 };
 
 // Debug timeline: slot s of tile lt of CTA b (first TRACE_TILES tiles).
@@ -1411,7 +1412,8 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             if (++mchunk == p.i2c_cpt) mchunk = 0;
           }
           if constexpr (HALO) {
-            const int left = p.i2c_C - hch * BK;
+            // zero_tail16: the last 16 input channels carry structural-zero filter weights
+            const int left = p.i2c_C - (p.zero_tail16 ? 16 : 0) - hch * BK;
             if (left < BK) nk16 = (left + 15) / 16;
           }
           const int s = git % STAGES;
@@ -2061,6 +2063,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
   p.o_ld = g.N;
   p.bias = bias;
   p.relu = (flags & PC_RELU) != 0;
+  p.zero_tail16 = (flags & PC_ZERO_TAIL16) && halo && g.C % BK == 0 && g.C == BK;
   if (res) {
     // output view {N, Wo, B*Ho}, box {N/2, 8 rows, 1} (epilogue_bf16_halo_tma)
     cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.Wo, (cuuint64_t)g.B * g.Ho};

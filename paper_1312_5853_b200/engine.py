@@ -615,6 +615,8 @@ class ColumnEngine:
                        L.PC_RELU if st.relu_after else 0, s)
         elif st.kind == "conv":
             flags = L.PC_RELU if st.relu_after else 0
+            if st.s2d and st.cp - self.in_c * st.s2d ** 2 >= 16 and os.environ.get("PC_ZERO_TAIL", "1") != "0":
+                flags |= L.PC_ZERO_TAIL16   # channels >= 48 of the 64 are structural zeros (and the ones channel)
             self._call(st, "pc_conv2d_forward", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
                      self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, s)
         elif st.kind == "fc":
