@@ -1033,9 +1033,17 @@ extern "C" int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, cons
   return PC_OK;
 }
 
-static constexpr int POOL_BIAS_CTAS = 148 * 8;
+// enough CTAs that each thread walks only ~1-2 blocks (the gather's load latency is
+// hidden by parallelism, as in the plain backward), few enough partial rows to sum
+static int pool_bias_ctas() {
+  static const int n = [] {
+    const char* e = getenv("PC_POOL_BIAS_CTAS");
+    return e ? atoi(e) : 148 * 8;
+  }();
+  return n;
+}
 
-extern "C" size_t pc_maxpool_backward_bias_workspace(int C) { return (size_t)POOL_BIAS_CTAS * C * sizeof(float); }
+extern "C" size_t pc_maxpool_backward_bias_workspace(int C) { return (size_t)pool_bias_ctas() * C * sizeof(float); }
 
 extern "C" int pc_maxpool_backward_bias(int B, int H, int W, int C, int k, int s, const void* gy,
                                         const uint8_t* argmax, const void* mask, void* gx, int prec, float* gb,
@@ -1052,10 +1060,10 @@ extern "C" int pc_maxpool_backward_bias(int B, int H, int W, int C, int k, int s
     return PC_OK;
   }
   float* part = static_cast<float*>(ws);
-  maxpool_bwd_bf16_k3s2_bias_k<<<POOL_BIAS_CTAS, 256, 0, S(st)>>>(
+  maxpool_bwd_bf16_k3s2_bias_k<<<pool_bias_ctas(), 256, 0, S(st)>>>(
       B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(gy), argmax, static_cast<const __nv_bfloat16*>(mask),
       static_cast<__nv_bfloat16*>(gx), part);
-  pool_bias_rows_k<<<C / 8, 256, 0, S(st)>>>(part, POOL_BIAS_CTAS, C, gb);
+  pool_bias_rows_k<<<C / 8, 256, 0, S(st)>>>(part, pool_bias_ctas(), C, gb);
   count_launches(1);
   PC_CUDA_CHECK_LAUNCH("maxpool_backward_bias");
   return PC_OK;
