@@ -384,7 +384,7 @@ class ColumnEngine:
         n = st.cl.out_shape[0]
         if side is None or n % 8 or st.col or st.s2d:
             return False
-        side.wait_stream(torch.cuda.current_stream(self.device))
+        self._fork(side)
         self.lib.call("pc_bias_grad", self._bias_rows(st), n, st.gout.data_ptr(), self.prec,
                       self.g32[st.b_off:].data_ptr(), self.bias_ws.data_ptr(), self.bias_ws.numel(), self.bias_ctas,
                       side.cuda_stream)
@@ -410,6 +410,14 @@ class ColumnEngine:
                 self.lib.call("pc_conv2d_dgrad_weights", C.byref(st.geom), self._w_lowp(st), st.wt.data_ptr(),
                               self.prec, stream)
 
+    def enable_wgrad_side(self, stream):
+        """Single replica, fused update: each conv layer's weight gradient (+ bias and
+        fused momentum update) runs on ``stream``, forked after its data gradient, so the
+        persistent weight-gradient kernels fill the SMs the data-gradient chain leaves
+        idle in its last wave (and vice versa); joined before the final update."""
+        self.wg_side = stream
+        self.ws_wg = torch.empty(max(self.ws_bytes, 16), dtype=torch.uint8, device=self.device)
+
     def enable_fc_side(self, stream, side_ctas: int, main_ctas: int, span: int):
         """Single replica, fused update: every FC layer's weight gradient + momentum
         update (HBM-bound: the FC6 update alone moves 680 MB) runs on ``stream`` with
@@ -430,10 +438,19 @@ class ColumnEngine:
             self._main_cap_left -= 1
         return True
 
+    def _fork(self, side):
+        """side waits for the current stream (and is remembered for join_side)."""
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        self._forked = getattr(self, "_forked", [])
+        if all(f is not side for f in self._forked):
+            self._forked.append(side)
+
     def join_side(self):
-        for side in (getattr(self, "bias_side", None), getattr(self, "fc_side", None)):
-            if side is not None:
-                torch.cuda.current_stream(self.device).wait_stream(side)
+        # only streams forked in this step program (joining an unforked stream during a
+        # CUDA-graph capture would depend on work outside the capture)
+        for side in getattr(self, "_forked", []):
+            torch.cuda.current_stream(self.device).wait_stream(side)
+        self._forked = []
         if getattr(self, "fc_side", None) is not None:
             self._main_cap_left = 0
             self.lib.call("pc_set_grid_cap", 0)
@@ -688,6 +705,22 @@ class ColumnEngine:
             if want_dx and st.wt is not None and self.wt_ready:
                 flags |= L.PC_WT_PRESET
                 w_ptr = st.wt.data_ptr()
+            wg = getattr(self, "wg_side", None)
+            if wg is not None and upd is not None and PROFILE is None and (not want_dx or flags & L.PC_WT_PRESET):
+                # data gradient here (it reads the prepared filters, not the ones the fused
+                # update rewrites); weight gradient + bias + update on the side stream
+                gb = None if no_gb else self.g32[st.b_off:].data_ptr()
+                if want_dx:
+                    self.lib.call("pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
+                                  st.gout.data_ptr(), st.gin.data_ptr(), st.inp.data_ptr() if st.mask_dx else None,
+                                  None, None, self.prec, flags & ~L.PC_WANT_DW, None, 0, None, s)
+                self._fork(wg)
+                self.lib.call("pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
+                              st.gout.data_ptr(), None, None, self.g32[st.w_off:].data_ptr(), gb, self.prec,
+                              L.PC_WANT_DW, self.ws_wg.data_ptr(), self.ws_bytes, C.byref(upd), wg.cuda_stream)
+                if st.keep is not None:   # (not reached: the input layer's update is not fused)
+                    raise RuntimeError("weight-gradient side stream: masked layer")
+                return
             self._split_backward(st, "pc_conv2d_backward_ex", flags, lambda f, tag: self._call(
                 st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
                 st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
@@ -716,7 +749,7 @@ class ColumnEngine:
                 # after the data gradient (which reads the pre-update weights)
                 if want_dx:
                     fc_call(flags & ~L.PC_WANT_DW, "")
-                side.wait_stream(torch.cuda.current_stream(self.device))
+                self._fork(side)
                 self.lib.call("pc_set_grid_cap", self.fc_side_ctas)
                 try:
                     fc_call(flags & ~(L.PC_WANT_DX | L.PC_MASK_DX), "", stream=side.cuda_stream, ws=self.ws_side)

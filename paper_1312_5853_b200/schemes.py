@@ -149,6 +149,18 @@ class _Runner:
                 if getattr(eng, "fuse_sgd", False):
                     eng.enable_fc_side(self.fc_side, side_ctas, (sms - side_ctas) & ~1,
                                        int(os.environ.get("PC_FC_SIDE_SPAN", "2")))
+        # conv weight gradients (+ fused updates) on a side stream beside the data-gradient
+        # chain (PC_WGRAD_SIDE=0 off): their persistent kernels fill the SMs the chain's
+        # last waves leave idle; needs the prepared data-gradient filters below
+        self.wg_side = None
+        if fuse and os.environ.get("PC_WGRAD_SIDE", "1") != "0" and os.environ.get("PC_WT_PREP", "1") != "0":
+            self.wg_side = torch.cuda.Stream(device=dev)
+            fc_too = os.environ.get("PC_FC_WG_SIDE", "1") != "0" and self.fc_side is None
+            for eng in self.engines.values():
+                if getattr(eng, "fuse_sgd", False):
+                    eng.enable_wgrad_side(self.wg_side)
+                    if fc_too:   # FC weight gradients + updates on the same stream, no grid caps
+                        eng.enable_fc_side(self.wg_side, 0, 0, 0)
         # conv filters in the data-gradient layout, prepared on a side stream at the
         # start of every step (beside the forward) instead of inside each backward
         self.wt_side = None
