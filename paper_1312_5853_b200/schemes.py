@@ -120,6 +120,12 @@ class _Runner:
             self.columns.setdefault(eng.column, []).append(eng)
         self.x_dev = None
         self.y_dev = None
+        self.fwd_done = None
+        self._fwd_single = True
+        split = len(self.replicas) == 1 and os.environ.get("PC_SPLIT_STEP", "1") != "0" and not fabric.dist
+        self.copy_stream = torch.cuda.Stream(device=dev) if split else None
+        self.loss_stream = torch.cuda.Stream(device=dev) if split else None
+        self.loss_host = torch.zeros(2, dtype=torch.float64).pin_memory() if split else None
         self._graphs, self._seen = {}, set()
         self.graph_launches, self.replays = 0, 0
         # single replica, unfused SGD: the FC head's update runs on a side stream as soon
@@ -205,18 +211,24 @@ class _Runner:
             self.y_host = torch.empty(tuple(y.shape), dtype=torch.int32).pin_memory()
             self.x_dev = torch.empty(shape, dtype=xdt, device=dev)
             self.y_dev = torch.empty(tuple(y.shape), dtype=torch.int32, device=dev)
-        if xs is not None:
-            self.x_dev.copy_(xs)
-        elif x.is_pinned():
-            self.x_dev.copy_(x, non_blocking=True)
-        else:
-            self.x_host.copy_(x)
-            self.x_dev.copy_(self.x_host, non_blocking=True)
-        if y.is_cuda:
-            self.y_dev.copy_(y)
-        else:
-            self.y_host.copy_(y)
-            self.y_dev.copy_(self.y_host, non_blocking=True)
+        # host -> device on a copy stream that waits only until the previous step's
+        # forward has consumed the input buffers: the upload overlaps that step's backward
+        cs = self.copy_stream if self.copy_stream is not None else torch.cuda.current_stream()
+        if self.copy_stream is not None:
+            cs.wait_stream(torch.cuda.current_stream()) if self.fwd_done is None else cs.wait_event(self.fwd_done)
+        with torch.cuda.stream(cs):
+            if xs is not None:
+                self.x_dev.copy_(xs)
+            elif x.is_pinned():
+                self.x_dev.copy_(x, non_blocking=True)
+            else:
+                self.x_host.copy_(x)
+                self.x_dev.copy_(self.x_host, non_blocking=True)
+            if y.is_cuda:
+                self.y_dev.copy_(y)
+            else:
+                self.y_host.copy_(y)
+                self.y_dev.copy_(self.y_host, non_blocking=True)
 
     def program(self, loss_scale: float, eager: bool = False):
         """The device step (no host synchronisation inside).
@@ -227,44 +239,77 @@ class _Runner:
         call from then on replays it, so the ~60 launches of a step cost one
         host call. Under torchrun the NCCL collectives stay eager unless
         ``PC_GRAPH_DIST=1``."""
+        self.fwd_done = None
+        if self.copy_stream is not None:   # this step's batch upload (pipelined, see upload())
+            torch.cuda.current_stream().wait_stream(self.copy_stream)
         if eager or not self._graph_enabled():
-            return self._launch(loss_scale)
+            self._launch(loss_scale, "fwd")
+            self._mark_fwd_done()
+            return self._launch(loss_scale, "bwd")
         key = (float(loss_scale), self.x_dev.data_ptr(), self.x_dev.dtype)
         g = self._graphs.get(key)
         if g is None:
             if key not in self._seen:
                 self._seen.add(key)
-                return self._launch(loss_scale)
+                self._launch(loss_scale, "fwd")
+                self._mark_fwd_done()
+                return self._launch(loss_scale, "bwd")
             # free garbage first: a collection during capture can release blocks that
             # other streams used, and the allocator's event calls would invalidate it
             gc.collect()
             torch.cuda.synchronize(self.fabric.torch_device)
-            g = torch.cuda.CUDAGraph()
             l0 = L.lib().dll.pc_launch_count()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                self._launch(loss_scale)
+            # two graphs (forward + loss, backward + update) when the plan allows it, so the
+            # loss can be read back while the backward runs
+            parts = ("fwd", "bwd") if self._split_ok() else ("all",)
+            g = []
+            for part in parts:
+                gp = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gp, capture_error_mode="thread_local"):
+                    self._launch(loss_scale, part)
+                g.append(gp)
             self.graph_launches = int(L.lib().dll.pc_launch_count() - l0)
             self._graphs[key] = g
-        g.replay()
+        g[0].replay()
+        if len(g) > 1:
+            self._mark_fwd_done()
+            g[1].replay()
         self.replays += 1
+
+    def _mark_fwd_done(self):
+        """Event after the forward (loss, label flag and the input buffers consumed)."""
+        if self._split_ok():
+            self.fwd_done = torch.cuda.Event()
+            self.fwd_done.record()
 
     def _graph_enabled(self) -> bool:
         if os.environ.get("PC_GRAPH", "1") == "0":
             return False
         return not self.fabric.dist or os.environ.get("PC_GRAPH_DIST", "0") == "1"
 
-    def _launch(self, loss_scale: float):
+    def _split_ok(self) -> bool:
+        """One local replica: the forward (and so the loss) is complete before any
+        backward work, so the step can be two graphs with the loss read in between."""
+        return len(self.replicas) == 1 and os.environ.get("PC_SPLIT_STEP", "1") != "0"
+
+    def _launch(self, loss_scale: float, part: str = "all"):
+        if part in ("all", "fwd"):
+            self._launch_fwd(loss_scale)
+        if part in ("all", "bwd"):
+            self._launch_bwd()
+
+    def _launch_fwd(self, loss_scale: float):
         shard = self.shard
         for eng in self.engines.values():
             lo = eng.replica * shard
             eng.load_batch(self.x_dev[lo:lo + shard], self.y_dev[lo:lo + shard])
         n = len(self.cs.col_layers)
-        overlap = self.reducer is not None and hasattr(self.reducer, "layer_done")
         if self.wt_side is not None:   # fork: data-gradient filters, joined before the backward
             self.wt_side.wait_stream(torch.cuda.current_stream())
             for eng in self.engines.values():
                 eng.prepare_dgrad_weights(self.wt_side.cuda_stream)
                 eng.wt_ready = True
+        single = len(self.replicas) == 1
         for engines in self.replicas.values():
             for i in range(n):
                 if self.cs.col_layers[i].cross and self.exchange is not None:
@@ -273,6 +318,20 @@ class _Runner:
                     e.forward(i, loss_scale)
             if self.wt_side is not None:
                 torch.cuda.current_stream().wait_stream(self.wt_side)
+            if not single:   # several local replicas: each replica's backward follows its forward
+                self._backward_replica(engines)
+        self._fwd_single = single
+
+    def _launch_bwd(self):
+        if self._fwd_single:
+            for engines in self.replicas.values():
+                self._backward_replica(engines)
+        self._finish()
+
+    def _backward_replica(self, engines):
+        n = len(self.cs.col_layers)
+        overlap = self.reducer is not None and hasattr(self.reducer, "layer_done")
+        if True:
             for i in range(n - 1, -1, -1):
                 for e in engines:
                     e.backward(i)
@@ -286,6 +345,8 @@ class _Runner:
                             e.sgd_table(self.split_sgd[e.wid][0], ctas_per_sm=self.sgd_bg_ctas)
                 if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
                     self.exchange.reduce_scatter(i, engines)
+
+    def _finish(self):
         if self.reducer is not None:
             self.reducer.reduce(self.columns)
         for eng in self.engines.values():
@@ -299,7 +360,20 @@ class _Runner:
             torch.cuda.current_stream().wait_stream(self.side)
 
     def loss(self) -> float:
-        """Sum over replicas of column 0's loss (host read-back; raises on bad labels)."""
+        """Sum over replicas of column 0's loss (host read-back; raises on bad labels).
+        With a split step the read waits only for the forward (fwd_done), on its own
+        stream: the backward keeps running while the caller gets the loss."""
+        if getattr(self, "fwd_done", None) is not None and not self.fabric.dist:
+            ls = self.loss_stream
+            ls.wait_event(self.fwd_done)
+            with torch.cuda.stream(ls):
+                parts = [e.loss for e in self.engines.values() if e.column == 0]
+                bad = [e.bad_label for e in self.engines.values()]
+                vals = torch.stack([torch.stack(parts).sum().reshape(()).double(),
+                                    torch.stack(bad).sum().reshape(()).double()])
+                self.loss_host.copy_(vals, non_blocking=True)
+            ls.synchronize()
+            return self._check_loss(self.loss_host.numpy())
         m = self.plan.model_columns
         parts = [e.loss for e in self.engines.values() if e.column == 0]
         bad = [e.bad_label for e in self.engines.values()]
@@ -311,6 +385,9 @@ class _Runner:
             torch.distributed.all_reduce(buf)
             total, flag = buf[0], buf[1]
         host = torch.stack([total.reshape(()).double(), flag.reshape(()).double()]).cpu().numpy()
+        return self._check_loss(host)
+
+    def _check_loss(self, host) -> float:
         if host[1] != 0:
             raise ValidationError(f"labels must lie in [0, {self.cs.base.classes})")
         return float(host[0])
