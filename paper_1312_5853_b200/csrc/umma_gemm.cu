@@ -131,6 +131,10 @@ struct alignas(64) Params {
   // instead of zero-filled / unused 64-channel ones — a quarter fewer operand
   // bytes for the layer, whose GEMMs are limited by operand delivery
   int half_chunk;
+  // half_chunk with one full chunk per tap (64 < C <= 96): k-blocks 0..taps-1 are the
+  // taps' full 64-channel chunks, then each k-block pairs the 32-channel remainders
+  // of two taps (two SW64 A/B halves in one stage): 38 k-blocks for conv2, not 50
+  int half_pair;
   CUtensorMap tma_a32, tma_b32;
   // A_IM2COL_MN2_32: 32-channel groups per tap (M row m -> tap (m/32)/m_grp, group (m/32)%m_grp)
   int m_grp;
@@ -1154,7 +1158,26 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             for (int i = 0; i < p.i2c_k; ++i)
               tma_load_3d<CG>(&p.tma_b, &full[s], st0 + HALO_SLOT_BYTES + i * B_STAGE_BYTES,
                               (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
-        } else if (!HALO && elect_one()) {
+        } else if (AM == A_IM2COL_K && p.half_pair && elect_one()) {
+          const int taps = p.i2c_k * p.i2c_k;
+          const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES), dB = smem_u32(sB + s * B_STAGE_BYTES);
+          const int ax = t_ox * p.i2c_s + p.i2c_lw, ay = t_oy * p.i2c_s + p.i2c_lh;
+          if (kb < taps) {  // full chunk (channels 0..63) of tap kb
+            if (leader) mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + A_STAGE_BYTES));
+            tma_load_3d<CG>(&p.tma_b, &full[s], dB, kb * p.i2c_C, n0, 0);
+            tma_im2col_5d<CG>(&p.tma_a, &full[s], dA, 0, ax, ay, t_b, 0, (uint16_t)(kb % p.i2c_k),
+                              (uint16_t)(kb / p.i2c_k));
+          } else {          // remainders (channels 64..) of taps t0, t0 + 1
+            const int t0 = 2 * (kb - taps), nt = t0 + 1 < taps ? 2 : 1;
+            if (leader) mbar_arrive_expect_tx(&full[s], CG * nt * (B_STAGE_BYTES + A_STAGE_BYTES) / 2);
+            for (int q = 0; q < nt; ++q) {
+              const int tq = t0 + q;
+              tma_load_3d<CG>(&p.tma_b32, &full[s], dB + q * (B_STAGE_BYTES / 2), tq * p.i2c_C + BK, n0, 0);
+              tma_im2col_5d<CG>(&p.tma_a32, &full[s], dA + q * (A_STAGE_BYTES / 2), BK, ax, ay, t_b, 0,
+                                (uint16_t)(tq % p.i2c_k), (uint16_t)(tq / p.i2c_k));
+            }
+          }
+        } else if (!HALO && !(AM == A_IM2COL_K && p.half_pair) && elect_one()) {
           // A_IM2COL_K: the k-block of a last chunk with <= 32 channels moves 32-channel boxes
           const bool half = AM == A_IM2COL_K && p.half_chunk && kc + 32 >= p.i2c_C;
           if (leader)
@@ -1398,7 +1421,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         const uint32_t tacc = tmem + acc * TCOLS;
         long long tr_wait = 0, tr_issue = 0;
         // K-major im2col with a partial last channel chunk: k16 steps with real channels
-        const bool partial = AM == A_IM2COL_K && (p.i2c_C % BK) != 0;
+        const bool partial = AM == A_IM2COL_K && (p.i2c_C % BK) != 0 && !p.half_pair;
         int mchunk = partial ? tc.kb_begin % p.i2c_cpt : 0;
         // halo: k-block = (channel chunk, filter column j): k filter rows per stage
         int hj = HALO ? tc.kb_begin % p.i2c_k : 0, hch = HALO ? tc.kb_begin / p.i2c_k : 0;
@@ -1452,6 +1475,16 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
                 for (int kk = 0; kk < BK / 16; ++kk)
                   tc_mma<CG>(tacc + (MACC == 2 ? a * tmem_cols<BN>() : a * p.N), aa + kk * A_KSTEP, bd + kk * B_KSTEP,
                              IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+              }
+            } else if (AM == A_IM2COL_K && p.half_pair && tc.kb_begin + it >= p.i2c_k * p.i2c_k) {
+              // paired remainders: two 32-channel (SW64) halves, 2 k16 steps each
+              const int t0 = 2 * (tc.kb_begin + it - p.i2c_k * p.i2c_k);
+              const int nt = t0 + 1 < p.i2c_k * p.i2c_k ? 2 : 1;
+              for (int q = 0; q < nt; ++q) {
+                const uint64_t aq = a0h + (uint64_t)((s * A_STRIDE + q * (A_STAGE_BYTES / 2)) >> 4);
+                const uint64_t bq = b0h + (uint64_t)((s * B_STRIDE + q * (B_STAGE_BYTES / 2)) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) tc_mma<CG>(tacc, aq + kk * A_KSTEP, bq + kk * B_KSTEP, IDESC, 1u);
               }
             } else {
 #pragma unroll
@@ -2090,6 +2123,15 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
       if (!rc) rc = make_map(&p.tma_b32, w, K, g.N, 1, K, 0, t.bn / t.cg, 32);
       if (rc) return rc;
       p.half_chunk = 1;
+      static const int pair = [] {  // opt-in: measured no faster (the loop is operand-bound)
+        const char* e = getenv("PC_HALF_PAIR");
+        return e ? atoi(e) : 0;
+      }();
+      if (pair && g.C > BK && g.C < 2 * BK) {  // one full + one remainder chunk per tap
+        p.half_pair = 1;
+        p.num_kb = g.k * g.k + (g.k * g.k + 1) / 2;
+        p.kb_per_split = p.num_kb;
+      }
     }
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
