@@ -20,6 +20,7 @@ void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::me
 
 __global__ void reduce_partials_k(const float* __restrict__ ws, int splits, long long n,
                                   float* __restrict__ out, pc_sgd_fuse upd, int fused) {
+  PC_PDL_TRIGGER();
   for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n;
        i += (long long)gridDim.x * blockDim.x * 4) {
     if (i + 4 <= n && (n & 3) == 0) {
@@ -50,6 +51,7 @@ __global__ void reduce_partials_k(const float* __restrict__ ws, int splits, long
 // of one thread walking all slices.
 __global__ void __launch_bounds__(256) reduce_partials_wide_k(const float* __restrict__ ws, int splits, long long n,
                                                               float* __restrict__ out, pc_sgd_fuse upd, int fused) {
+  PC_PDL_TRIGGER();
   const long long i = ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3) * 4;
   const int lane = threadIdx.x & 7;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -170,6 +172,7 @@ template <> struct V8<float> {
 template <typename T>
 __global__ void __launch_bounds__(256) colsum1_v8_k(const T* __restrict__ g, long long P, int N, int RB,
                                                     float* __restrict__ part) {
+  PC_PDL_TRIGGER();
   __shared__ float sh[256 * 8];
   const int groups = N / 8;
   const int CB = min(groups, 256), lanes = 256 / CB;
@@ -200,6 +203,7 @@ __global__ void __launch_bounds__(256) colsum1_v8_k(const T* __restrict__ g, lon
 constexpr int CS2_LANES = 128;
 __global__ void __launch_bounds__(8 * CS2_LANES) colsum2_k(const float* __restrict__ part, int R, int N,
                                                            float* __restrict__ out) {
+  PC_PDL_TRIGGER();
   __shared__ float sh[CS2_LANES][9];
   __shared__ float sh2[8][9];
   const int cx = threadIdx.x & 7, ry = threadIdx.x >> 3;
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(8 * CS2_LANES) colsum2_k(const float* __restri
 // 8) x 32 row lanes; the lanes are combined in a fixed order.
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_short_k(const T* __restrict__ g, int P, int N, float* __restrict__ out) {
+  PC_PDL_TRIGGER();
   __shared__ float sh[32][64 + 1];
   const int q = threadIdx.x & 7, lane = threadIdx.x >> 3;
   const int grp = blockIdx.x * 8 + q;

@@ -27,6 +27,12 @@ void set_error(const std::string& msg);
 
 void count_launches(int n);
 
+// Programmatic dependent launch: a bandwidth kernel lets the next tensor-core
+// GEMM (launched with programmatic stream serialization) start its prologue
+// (barrier init, TMEM allocation, descriptor prefetch) while this kernel's last
+// blocks run; the GEMM waits (griddepcontrol.wait) before touching global memory.
+#define PC_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+
 // Every kernel launch site is followed by this check; it also feeds the
 // launch counter behind pc_launch_count() (one launch per check unless the
 // site calls count_launches() for the extra ones).

@@ -89,6 +89,7 @@ __global__ void relu_bwd_k(long long n, const T* __restrict__ x, const T* __rest
 __global__ void maxpool_fwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int Wo,
                                         const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                         uint8_t* __restrict__ arg) {
+  PC_PDL_TRIGGER();
   const unsigned cg = (unsigned)(C >> 3);
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (unsigned)B * Ho * Wo * cg) return;
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
                                                                const uint8_t* __restrict__ arg,
                                                                const __nv_bfloat16* __restrict__ mask,
                                                                __nv_bfloat16* __restrict__ gx) {
+  PC_PDL_TRIGGER();
   const int H2 = (H + 1) >> 1, W2 = (W + 1) >> 1;
   const unsigned cg = (unsigned)(C >> 3);
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H
                                                                     const __nv_bfloat16* __restrict__ mask,
                                                                     __nv_bfloat16* __restrict__ gx,
                                                                     float* __restrict__ part) {
+  PC_PDL_TRIGGER();
   __shared__ float red[256][9];
   const int H2 = (H + 1) >> 1, W2 = (W + 1) >> 1;
   const unsigned cg = (unsigned)(C >> 3);
@@ -457,6 +460,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H
 // threads. Deterministic.
 __global__ void __launch_bounds__(256) pool_bias_rows_k(const float* __restrict__ part, int R, int N,
                                                         float* __restrict__ out) {
+  PC_PDL_TRIGGER();
   __shared__ float sh[256][9];
   const int grp = blockIdx.x;
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -592,6 +596,7 @@ __global__ void __launch_bounds__(256) softmax_xent_warp_k(int B, int K, const T
                                                           const int32_t* __restrict__ labels, double scale,
                                                           T* __restrict__ grad, double* __restrict__ row_loss,
                                                           int* __restrict__ bad) {
+  PC_PDL_TRIGGER();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= B) return;
   const T* z = logits + (long long)row * K;
@@ -633,6 +638,7 @@ __global__ void __launch_bounds__(256) softmax_xent_warp_k(int B, int K, const T
 // fixed tree (warp xor-shuffles, then the 8 warp sums in order): deterministic,
 // and the row losses load in parallel instead of one dependent chain.
 __global__ void __launch_bounds__(256) sum_f64_k(int n, const double* __restrict__ v, double* __restrict__ out) {
+  PC_PDL_TRIGGER();
   __shared__ double sh[8];
   double acc = 0.0;
   for (int i = threadIdx.x; i < n; i += 256) acc += v[i];
@@ -649,6 +655,7 @@ __global__ void __launch_bounds__(256) sum_f64_k(int n, const double* __restrict
 
 // Multi-tensor momentum SGD: blockIdx.y = tensor --------------------------------------
 __global__ void sgd_k(const pc_sgd_tensor* __restrict__ tab, float lr, float mom, float wd) {
+  PC_PDL_TRIGGER();
   pc_sgd_tensor t = tab[blockIdx.y];
   long long stride = (long long)gridDim.x * blockDim.x * 4;
   for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < t.n; i += stride) {
@@ -847,6 +854,7 @@ template <int CS, int SS, int CC>
 __global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, int Ws, long long total,
                                                  const __nv_bfloat16* __restrict__ x,
                                                  __nv_bfloat16* __restrict__ dst, int ones) {
+  PC_PDL_TRIGGER();
   extern __shared__ __align__(16) uint8_t s2d_sm[];
   const int span = SS * W;                    // elements of SS consecutive rows
   const int slot = ((span + 7) / 8 + 1) * 8;  // per-channel staging (aligned-down start)
@@ -1235,6 +1243,7 @@ extern "C" int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, in
 // pixels of gy * 1), then the structural zeros are pinned (keep mask).
 __global__ void s2d_wgrad_finish_k(int N, int K, int ones, const uint8_t* __restrict__ keep,
                                    float* __restrict__ gw, float* __restrict__ gb) {
+  PC_PDL_TRIGGER();
   const long long n = (long long)N * K;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(i / K), c = (int)(i - (long long)r * K);

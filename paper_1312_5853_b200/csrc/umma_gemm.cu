@@ -2144,6 +2144,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
 __global__ void __launch_bounds__(256) transpose_w_k(const __nv_bfloat16* __restrict__ w,
                                                      __nv_bfloat16* __restrict__ wt, int N, int KK, int C,
                                                      int flip) {
+  PC_PDL_TRIGGER();
   __shared__ __nv_bfloat16 tile[32][33];
   const int ij = blockIdx.z, src_ij = flip ? KK - 1 - ij : ij;
   const int c0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
@@ -2485,6 +2486,7 @@ __global__ void fc_reduce_epilogue_k(const float* __restrict__ part, int splits,
                                      const float* __restrict__ bias, int relu, const __nv_bfloat16* __restrict__ mask,
                                      __nv_bfloat16* __restrict__ out, long long o_ld, long long o_cb,
                                      long long o_bstride) {
+  PC_PDL_TRIGGER();
   const int groups = N / 8;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)M * groups) return;
