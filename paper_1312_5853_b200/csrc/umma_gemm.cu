@@ -5,11 +5,12 @@
 // convolution operand, and a fused epilogue (bias, ReLU, ReLU-mask of the
 // producer, bf16 / fp32 / transposed-fp32 stores, split-K partials).
 //
-// One CTA computes one BM x BN output tile over a K range (grid.z = split-K):
-//   warps 0-3  epilogue: tcgen05.ld 32 lanes x 16 columns at a time
-//   warp  4    TMEM allocator + single-thread MMA issuer
-//   warp  5    TMA producer
-//   warps 6-9  im2col gather producers (conv operand only)
+// Persistent CTAs (or CTA pairs, cta_group::2) walk a static tile schedule:
+//   warps 0-3 (+6-9)  epilogue: 2 warps per TMEM lane quadrant (1 in the GATHER modes),
+//                     tcgen05.ld 32 lanes x 16/32 columns
+//   warp  4           TMEM allocator + elected-lane MMA issuer
+//   warp  5           TMA producer
+//   warps 6-21        cp.async gather producers (GATHER modes only)
 // A STAGES-deep full/empty mbarrier ring connects producers and the MMA
 // issuer; tcgen05.commit frees a stage and finally signals the epilogue.
 //
@@ -134,7 +135,6 @@ struct alignas(64) Params {
   // half_chunk with one full chunk per tap (64 < C <= 96): k-blocks 0..taps-1 are the
   // taps' full 64-channel chunks, then each k-block pairs the 32-channel remainders
   // of two taps (two SW64 A/B halves in one stage): 38 k-blocks for conv2, not 50
-  int half_pair;
   CUtensorMap tma_a32, tma_b32;
   // A_IM2COL_MN2_32: 32-channel groups per tap (M row m -> tap (m/32)/m_grp, group (m/32)%m_grp)
   int m_grp;
@@ -334,6 +334,23 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 32 columns in one tcgen05.ld (one wait per 32 columns instead of per 16)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ int blk_off(int idx, int cb) { return cb ? (int)((unsigned)idx % (unsigned)cb) : idx; }
@@ -660,8 +677,7 @@ __device__ __forceinline__ void epilogue_sgd_tma(const Params& p, uint32_t tmem,
       }
       float g[32];
       if (tc.nkb > 0) {
-        tmem_ld16(tbase + c0, g);
-        tmem_ld16(tbase + c0 + 16, g + 16);
+        tmem_ld32(tbase + c0, g);
       } else {
 #pragma unroll
         for (int q = 0; q < 32; ++q) g[q] = 0.f;
@@ -749,8 +765,7 @@ __device__ __forceinline__ void epilogue_f32_tma(const Params& p, uint32_t tmem,
     for (int c0 = grp * 32; c0 < BN; c0 += 32 * EPW) {
       float v[32];
       if (tc.nkb > 0) {
-        tmem_ld16(tbase + c0, v);
-        tmem_ld16(tbase + c0 + 16, v + 16);
+        tmem_ld32(tbase + c0, v);
       } else {
 #pragma unroll
         for (int q = 0; q < 32; ++q) v[q] = 0.f;
@@ -828,7 +843,8 @@ __device__ __forceinline__ void epilogue_bf16_halo(const Params& p, uint32_t tme
     const uint32_t tbase = tmem + acc * TCOLS + sub * tmem_cols<BN>() + grp * HALF + ((uint32_t)(quad * 32) << 16);
     float v[HALF];
 #pragma unroll
-    for (int c = 0; c < HALF / 16; ++c) tmem_ld16(tbase + 16 * c, v + 16 * c);
+    for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tbase + 32 * c, v + 32 * c);
+    if constexpr (HALF % 32 != 0) tmem_ld16(tbase + HALF - 16, v + HALF - 16);
     if (sub == HSUB - 1) {  // every sub-tile read: release the buffer to the MMA warp
       tc_fence_before();
       __syncwarp();
@@ -1158,26 +1174,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
             for (int i = 0; i < p.i2c_k; ++i)
               tma_load_3d<CG>(&p.tma_b, &full[s], st0 + HALO_SLOT_BYTES + i * B_STAGE_BYTES,
                               (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
-        } else if (AM == A_IM2COL_K && p.half_pair && elect_one()) {
-          const int taps = p.i2c_k * p.i2c_k;
-          const uint32_t dA = smem_u32(sA + s * A_STAGE_BYTES), dB = smem_u32(sB + s * B_STAGE_BYTES);
-          const int ax = t_ox * p.i2c_s + p.i2c_lw, ay = t_oy * p.i2c_s + p.i2c_lh;
-          if (kb < taps) {  // full chunk (channels 0..63) of tap kb
-            if (leader) mbar_arrive_expect_tx(&full[s], CG * (B_STAGE_BYTES + A_STAGE_BYTES));
-            tma_load_3d<CG>(&p.tma_b, &full[s], dB, kb * p.i2c_C, n0, 0);
-            tma_im2col_5d<CG>(&p.tma_a, &full[s], dA, 0, ax, ay, t_b, 0, (uint16_t)(kb % p.i2c_k),
-                              (uint16_t)(kb / p.i2c_k));
-          } else {          // remainders (channels 64..) of taps t0, t0 + 1
-            const int t0 = 2 * (kb - taps), nt = t0 + 1 < taps ? 2 : 1;
-            if (leader) mbar_arrive_expect_tx(&full[s], CG * nt * (B_STAGE_BYTES + A_STAGE_BYTES) / 2);
-            for (int q = 0; q < nt; ++q) {
-              const int tq = t0 + q;
-              tma_load_3d<CG>(&p.tma_b32, &full[s], dB + q * (B_STAGE_BYTES / 2), tq * p.i2c_C + BK, n0, 0);
-              tma_im2col_5d<CG>(&p.tma_a32, &full[s], dA + q * (A_STAGE_BYTES / 2), BK, ax, ay, t_b, 0,
-                                (uint16_t)(tq % p.i2c_k), (uint16_t)(tq / p.i2c_k));
-            }
-          }
-        } else if (!HALO && !(AM == A_IM2COL_K && p.half_pair) && elect_one()) {
+        } else if (!HALO && elect_one()) {
           // A_IM2COL_K: the k-block of a last chunk with <= 32 channels moves 32-channel boxes
           const bool half = AM == A_IM2COL_K && p.half_chunk && kc + 32 >= p.i2c_C;
           if (leader)
@@ -1421,7 +1418,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         const uint32_t tacc = tmem + acc * TCOLS;
         long long tr_wait = 0, tr_issue = 0;
         // K-major im2col with a partial last channel chunk: k16 steps with real channels
-        const bool partial = AM == A_IM2COL_K && (p.i2c_C % BK) != 0 && !p.half_pair;
+        const bool partial = AM == A_IM2COL_K && (p.i2c_C % BK) != 0;
         int mchunk = partial ? tc.kb_begin % p.i2c_cpt : 0;
         // halo: k-block = (channel chunk, filter column j): k filter rows per stage
         int hj = HALO ? tc.kb_begin % p.i2c_k : 0, hch = HALO ? tc.kb_begin / p.i2c_k : 0;
@@ -1475,16 +1472,6 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
                 for (int kk = 0; kk < BK / 16; ++kk)
                   tc_mma<CG>(tacc + (MACC == 2 ? a * tmem_cols<BN>() : a * p.N), aa + kk * A_KSTEP, bd + kk * B_KSTEP,
                              IDESC, (it > 0 || kk > 0) ? 1u : 0u);
-              }
-            } else if (AM == A_IM2COL_K && p.half_pair && tc.kb_begin + it >= p.i2c_k * p.i2c_k) {
-              // paired remainders: two 32-channel (SW64) halves, 2 k16 steps each
-              const int t0 = 2 * (tc.kb_begin + it - p.i2c_k * p.i2c_k);
-              const int nt = t0 + 1 < p.i2c_k * p.i2c_k ? 2 : 1;
-              for (int q = 0; q < nt; ++q) {
-                const uint64_t aq = a0h + (uint64_t)((s * A_STRIDE + q * (A_STAGE_BYTES / 2)) >> 4);
-                const uint64_t bq = b0h + (uint64_t)((s * B_STRIDE + q * (B_STAGE_BYTES / 2)) >> 4);
-#pragma unroll
-                for (int kk = 0; kk < 2; ++kk) tc_mma<CG>(tacc, aq + kk * A_KSTEP, bq + kk * B_KSTEP, IDESC, 1u);
               }
             } else {
 #pragma unroll
@@ -2123,15 +2110,6 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
       if (!rc) rc = make_map(&p.tma_b32, w, K, g.N, 1, K, 0, t.bn / t.cg, 32);
       if (rc) return rc;
       p.half_chunk = 1;
-      static const int pair = [] {  // opt-in: measured no faster (the loop is operand-bound)
-        const char* e = getenv("PC_HALF_PAIR");
-        return e ? atoi(e) : 0;
-      }();
-      if (pair && g.C > BK && g.C < 2 * BK) {  // one full + one remainder chunk per tap
-        p.half_pair = 1;
-        p.num_kb = g.k * g.k + (g.k * g.k + 1) / 2;
-        p.kb_per_split = p.num_kb;
-      }
     }
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }

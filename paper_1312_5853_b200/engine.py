@@ -480,6 +480,7 @@ class ColumnEngine:
         tabs = [L.SgdTensor(self.p32[o:].data_ptr(), self.v32[o:].data_ptr(), self.g32[o:].data_ptr(),
                             self.plow[o:].data_ptr(), n) for o, n in rest]
         arr = (L.SgdTensor * len(tabs))(*tabs)
+        self.sgd_numel_fused = sum(n for _, n in rest)
         self._sgd_regions = (len(tabs), max(n for _, n in rest),
                              torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.device))
 
@@ -586,13 +587,16 @@ class ColumnEngine:
     def _call(self, st, name: str, *args, tag: str = ""):
         """C-ABI call of one layer pass; with ``PROFILE`` set, bracketed by CUDA
         events on the launching stream (bench.py's per-kernel roofline)."""
+        return self._pcall(st.cl.index, st.kind, name, *args, tag=tag)
+
+    def _pcall(self, idx: int, kind: str, name: str, *args, tag: str = ""):
         if PROFILE is None:
             return self.lib.call(name, *args)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         self.lib.call(name, *args)
         b.record()
-        PROFILE.append((self.wid, st.cl.index, st.kind, name + tag, a, b))
+        PROFILE.append((self.wid, idx, kind, name + tag, a, b))
 
     def _split_backward(self, st, name: str, flags: int, call):
         """Under ``PROFILE``, issue a backward pass as its data-gradient and its
@@ -608,17 +612,18 @@ class ColumnEngine:
         apply anyway, done by the caller's input pipeline)."""
         c, h, w = self.cs.base.input_shape
         src_prec = L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32
+        self.x_src_es = x_nchw.element_size()
         if self.s2d:
             lay = self.cs.col_layers[0].layer
-            self.lib.call("pc_space_to_depth_ex", self.B, c, h, w, lay.stride, lay.pad, 64, x_nchw.data_ptr(),
+            self._pcall(-1, "input", "pc_space_to_depth_ex", self.B, c, h, w, lay.stride, lay.pad, 64, x_nchw.data_ptr(),
                           src_prec, self.s2d_ones, self.x.data_ptr(), self.stream)
         elif self.col_kp:
             lay = self.cs.col_layers[0].layer
-            self.lib.call("pc_im2col", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
+            self._pcall(-1, "input", "pc_im2col", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
                           x_nchw.data_ptr(), L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32,
                           self.x.data_ptr(), self.stream)
         else:
-            self.lib.call("pc_nchw_to_nhwc", self.B, c, h, w, self.in_cp, x_nchw.data_ptr(),
+            self._pcall(-1, "input", "pc_nchw_to_nhwc", self.B, c, h, w, self.in_cp, x_nchw.data_ptr(),
                           self.x.data_ptr(), self.prec, self.stream)
         self.labels[: self.B].copy_(labels_i32, non_blocking=True)
 
@@ -785,7 +790,7 @@ class ColumnEngine:
                                st.cl.layer.stride, st.gout.data_ptr(), st.argmax.data_ptr(),
                                st.inp.data_ptr() if st.mask_dx else None, st.gin.data_ptr(), self.prec, s)
         if st.keep is not None and self.s2d_ones >= 0:
-            self.lib.call("pc_s2d_wgrad_finish", st.w_shape[0], st.keep.numel() // st.w_shape[0], self.s2d_ones,
+            self._call(st, "pc_s2d_wgrad_finish", st.w_shape[0], st.keep.numel() // st.w_shape[0], self.s2d_ones,
                           st.keep.data_ptr(), self.g32[st.w_off:].data_ptr(), self.g32[st.b_off:].data_ptr(), s)
         elif st.keep is not None:
             self.lib.call("pc_mask_f32", st.keep.numel(), st.keep.data_ptr(), self.g32[st.w_off:].data_ptr(),
@@ -794,14 +799,20 @@ class ColumnEngine:
             n = st.gin.numel()
             self._call(st, "pc_scale", n, st.gin.data_ptr(), st.gin.data_ptr(), 1.0 / self.m, self.prec, s)
 
+    def sgd_numel(self) -> int:
+        """Elements the final pc_sgd_step launch updates (bench.py's byte count)."""
+        if getattr(self, "_sgd_regions", None) is not None:
+            return int(self.sgd_numel_fused)
+        return int(self.n_flat)
+
     def sgd(self):
         if self.has_dropout:  # next step draws fresh masks
             self.lib.call("pc_counter_add", self.step_ctr.data_ptr(), 1, self.stream)
         if getattr(self, "_sgd_regions", None) is not None:
             n, mx, tab = self._sgd_regions
-            self.lib.call("pc_sgd_step", n, tab.data_ptr(), mx, self.lr, self.mom, self.wd, self.stream)
+            self._pcall(-1, "sgd", "pc_sgd_step", n, tab.data_ptr(), mx, self.lr, self.mom, self.wd, self.stream)
             return
-        self.lib.call("pc_sgd_step", 1, self._sgd_dev.data_ptr(), self.n_flat, self.lr, self.mom, self.wd,
+        self._pcall(-1, "sgd", "pc_sgd_step", 1, self._sgd_dev.data_ptr(), self.n_flat, self.lr, self.mom, self.wd,
                       self.stream)
 
     @property

@@ -215,7 +215,17 @@ class _Runner:
         # forward has consumed the input buffers: the upload overlaps that step's backward
         cs = self.copy_stream if self.copy_stream is not None else torch.cuda.current_stream()
         if self.copy_stream is not None:
-            cs.wait_stream(torch.cuda.current_stream()) if self.fwd_done is None else cs.wait_event(self.fwd_done)
+            if self.fwd_done is None or (xs is not None) or y.is_cuda:
+                # a device-resident source (e.g. the trainer's on-device batch gather) is
+                # produced on the current stream, behind the previous step's backward:
+                # the copy must wait for that producer, not only for the forward
+                cs.wait_stream(torch.cuda.current_stream())
+            else:
+                cs.wait_event(self.fwd_done)
+            if xs is not None:
+                xs.record_stream(cs)
+            if y.is_cuda:
+                y.record_stream(cs)
         with torch.cuda.stream(cs):
             if xs is not None:
                 self.x_dev.copy_(xs)
@@ -331,20 +341,19 @@ class _Runner:
     def _backward_replica(self, engines):
         n = len(self.cs.col_layers)
         overlap = self.reducer is not None and hasattr(self.reducer, "layer_done")
-        if True:
-            for i in range(n - 1, -1, -1):
-                for e in engines:
-                    e.backward(i)
-                    if overlap and e.layers[i].w_off >= 0:
-                        self.reducer.layer_done(e, *e.param_region(i))
-                    if i == self.head_pos and e.wid in self.split_sgd:   # fork: head update on the side stream
-                        self.side.wait_stream(torch.cuda.current_stream())
-                        if e.bias_side is not None:   # the head's bias gradients
-                            self.side.wait_stream(e.bias_side)
-                        with torch.cuda.stream(self.side):
-                            e.sgd_table(self.split_sgd[e.wid][0], ctas_per_sm=self.sgd_bg_ctas)
-                if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
-                    self.exchange.reduce_scatter(i, engines)
+        for i in range(n - 1, -1, -1):
+            for e in engines:
+                e.backward(i)
+                if overlap and e.layers[i].w_off >= 0:
+                    self.reducer.layer_done(e, *e.param_region(i))
+                if i == self.head_pos and e.wid in self.split_sgd:   # fork: head update on the side stream
+                    self.side.wait_stream(torch.cuda.current_stream())
+                    if e.bias_side is not None:   # the head's bias gradients
+                        self.side.wait_stream(e.bias_side)
+                    with torch.cuda.stream(self.side):
+                        e.sgd_table(self.split_sgd[e.wid][0], ctas_per_sm=self.sgd_bg_ctas)
+            if self.cs.col_layers[i].cross and self.exchange is not None and i > 0:
+                self.exchange.reduce_scatter(i, engines)
 
     def _finish(self):
         if self.reducer is not None:

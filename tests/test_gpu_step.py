@@ -324,3 +324,34 @@ def test_train_device_resident_feed_matches_host_feed_and_oracle():
     assert len(want) == len(runs[0])
     for got, ref in zip(runs[0], want):
         assert abs(got - ref) / abs(ref) < 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_train_device_resident_feed_single_replica_pipelined_upload(precision):
+    """d = 1 (the pipelined-upload path: the batch copy runs on its own stream,
+    overlapping the previous step's backward). With the batch gathered on the
+    device, the copy must wait for the gather, which queues behind that backward
+    (ADVICE r01): the device feed must reproduce the host feed bit for bit, and
+    follow the oracle."""
+    import paper_1312_5853_b200 as P
+    from oracle.ref_engine import OracleFabric
+    from paper_1312_5853_b200 import rng
+    net = P.load_network(CONFIGS / "alexnet_small64.net")
+    train_set, _ = P.gen_synthetic(100, 1, net.input_shape, seed=3)
+    plan = P.ParallelPlan(1, 1)
+    runs = []
+    for dev in (True, False):
+        cfg = P.TrainConfig(net=net, plan=plan, epochs=2, batch=16, seed=5, train_data=train_set,
+                            precision=precision, device_data=dev)
+        runs.append([r.train_loss for r in P.train(cfg).records])
+    assert runs[0] == runs[1]
+    if precision == "fp32":
+        of = OracleFabric(net, plan, P.init_dense_params(net, 5))
+        want = []
+        for epoch in range(2):
+            order = rng.permutation(5, epoch, train_set.size)
+            for step in range(train_set.size // 16):
+                idx = order[step * 16:(step + 1) * 16]
+                want.append(of.step(train_set.images[idx], train_set.labels[idx]))
+        for got, ref in zip(runs[0], want):
+            assert abs(got - ref) / abs(ref) < 1e-5
