@@ -333,6 +333,19 @@ def main():
     launches = lib().dll.pc_launch_count() - l0 + run.graph_launches * (run.replays - r0)
     ms = e0.elapsed_time(e1) / args.steps
 
+    # ---- per-kernel timing (resident bf16 batch, as in "value"): one eager step with CUDA events around every C-ABI call on the
+    # launching stream (passes serialised; backward split into data / weight gradients)
+    E.PROFILE = []
+    run.program(scale, eager=True)
+    torch.cuda.synchronize()
+    prof, E.PROFILE = E.PROFILE, None
+    t_by, n_by = {}, {}
+    for wid, idx, kind, name, a, b in prof:
+        key = (wid, idx, kind, name)
+        t_by[key] = t_by.get(key, 0.0) + a.elapsed_time(b)
+        n_by[key] = n_by.get(key, 0) + 1
+    step_prof_ms = sum(t_by.values())
+
     # ---- end to end through the public API: host batch -> device copy, step, loss read-back
     def e2e(xh, steps):
         for _ in range(2):
@@ -356,19 +369,6 @@ def main():
         # host-side conversion dominates, so fewer steps
         ms_f64, _ = e2e(xb.astype(np.float64), max(2, min(args.steps, 5)))
         variants["float64_numpy"] = ms_f64
-
-    # ---- per-kernel timing: one eager step with CUDA events around every C-ABI call on the
-    # launching stream (passes serialised; backward split into data / weight gradients)
-    E.PROFILE = []
-    run.program(scale, eager=True)
-    torch.cuda.synchronize()
-    prof, E.PROFILE = E.PROFILE, None
-    t_by, n_by = {}, {}
-    for wid, idx, kind, name, a, b in prof:
-        key = (wid, idx, kind, name)
-        t_by[key] = t_by.get(key, 0.0) + a.elapsed_time(b)
-        n_by[key] = n_by.get(key, 0) + 1
-    step_prof_ms = sum(t_by.values())
 
     if world > 1:
         t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)

@@ -16,14 +16,18 @@ namespace pc {
 
 constexpr int SB_M = 64, SB_N = 64, SB_K = 16, S_NT = 256;
 
-template <class AL, class BL, class EP>
+// ACC = double for the weight gradients: their reductions run over every pixel of
+// the batch (AlexNet conv1 at B = 256: 774,400 terms), where a float chain of a
+// split's ~30k dependent adds loses ~1e-3 relative to cancellation; products of
+// two floats are exact in double, so only the fp32 operands' own rounding remains.
+template <class AL, class BL, class EP, typename ACC = float>
 __global__ void __launch_bounds__(S_NT) simt_gemm_k(int M, int N, int K, int kps, AL a, BL b, EP ep) {
   __shared__ float As[SB_K][SB_M + 4];
   __shared__ float Bs[SB_K][SB_N + 4];
   const int t = threadIdx.x, tx = t % 16, ty = t / 16;
   const int m0 = blockIdx.y * SB_M, n0 = blockIdx.x * SB_N;
   const int kbeg = blockIdx.z * kps, kend = min(K, kbeg + kps);
-  float acc[4][4] = {};
+  ACC acc[4][4] = {};
   for (int k0 = kbeg; k0 < kend; k0 += SB_K) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -41,7 +45,12 @@ __global__ void __launch_bounds__(S_NT) simt_gemm_k(int M, int N, int K, int kps
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) {
+          if constexpr (sizeof(ACC) == 8)
+            acc[i][j] = fma((double)av[i], (double)bv[j], acc[i][j]);
+          else
+            acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
     }
     __syncthreads();
   }
@@ -50,18 +59,18 @@ __global__ void __launch_bounds__(S_NT) simt_gemm_k(int M, int N, int K, int kps
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
-      if (m < M && n < N) ep(m, n, blockIdx.z, acc[i][j]);
+      if (m < M && n < N) ep(m, n, blockIdx.z, (float)acc[i][j]);
     }
 }
 
-template <class AL, class BL, class EP>
+template <typename ACC = float, class AL, class BL, class EP>
 int simt_gemm(int M, int N, int K, int splits, const AL& a, const BL& b, const EP& ep, cudaStream_t st) {
   if (M <= 0 || N <= 0) return PC_OK;
   int kps = ceil_div(K, splits);
   kps = ceil_div(kps, SB_K) * SB_K;
   splits = ceil_div(K, kps);
   dim3 grid(ceil_div(N, SB_N), ceil_div(M, SB_M), splits > 0 ? splits : 1);
-  simt_gemm_k<<<grid, S_NT, 0, st>>>(M, N, K, kps, a, b, ep);
+  simt_gemm_k<AL, BL, EP, ACC><<<grid, S_NT, 0, st>>>(M, N, K, kps, a, b, ep);
   PC_CUDA_CHECK_LAUNCH("simt_gemm");
   return PC_OK;
 }
@@ -115,10 +124,10 @@ int simt_conv_wgrad(const pc_conv_geom& g, const void* x, const void* gy, float*
     ImColLoaderT<T> b{ImColLoader<T>{static_cast<const T*>(x), g}};
     if (splits <= 1) {
       PartialEpi ep{gw, 0, N};
-      return simt_gemm(M, N, K, 1, a, b, ep, st);
+      return simt_gemm<double>(M, N, K, 1, a, b, ep, st);
     }
     PartialEpi ep{ws, (long long)M * N, N};
-    int rc = simt_gemm(M, N, K, splits, a, b, ep, st);
+    int rc = simt_gemm<double>(M, N, K, splits, a, b, ep, st);
     if (rc) return rc;
     return reduce_partials(ws, splits, (long long)M * N, gw, st);
   });
@@ -152,7 +161,7 @@ int simt_fc_wgrad(int B, int D, int U, const pc_mat& x, const void* gy, float* g
     DenseMNLoader<T> a{static_cast<const T*>(gy), Blocked{U, kNoBlock, 0}};
     DenseMNLoader<T> b{static_cast<const T*>(x.ptr), Blocked{x.ld, x.cb, x.bstride}};
     PartialEpi ep{gw, 0, D};
-    return simt_gemm(U, D, B, 1, a, b, ep, st);
+    return simt_gemm<double>(U, D, B, 1, a, b, ep, st);
   });
 }
 
