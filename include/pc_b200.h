@@ -213,6 +213,21 @@ PC_API int pc_dropout(int B, int H, int W, int C, int C_dense, int c_off, long l
 /* *counter += delta (device; advances the dropout step inside a CUDA graph). */
 PC_API int pc_counter_add(unsigned long long* counter, long long delta, pc_stream_t stream);
 
+/* --- trainer feed on the device ------------------------------ */
+/* Rows idx[0..n) (DEVICE int64 sample indices) of the synthetic split
+ * gen_synthetic(classes, per_class, shape, seed) with prod(shape) = dim, written
+ * as NCHW rows in out_prec (PC_FP32 = the reference's float32-quantised values;
+ * PC_BF16 = those rounded to bf16). domain = rng.DOMAIN_TRAIN (4) / DOMAIN_TEST (5),
+ * std_ = the blob standard deviation (0.5). Replaces the host loop of
+ * `pkg/src/parconv/data.py:52-96` (templates `rng.py:94-100`, noise `rng.py:75-88`). */
+PC_API int pc_synthetic_rows(int classes, int per_class, long long dim, unsigned long long seed, int domain,
+                             const long long* idx, int n, float std_, void* out, int out_prec, pc_stream_t stream);
+/* dst[r] = src[idx[r]] for n rows of row_bytes (multiple of 4, 4-byte aligned
+ * buffers): the batch of an HBM-resident split by the epoch permutation
+ * (`pkg/src/parconv/trainer.py:120-133` indexes the host array instead). */
+PC_API int pc_gather_rows(int n, long long row_bytes, const void* src, const long long* idx, void* dst,
+                          pc_stream_t stream);
+
 /* --- layout / reduction helpers used by the engine -------------------------- */
 /* Explicit im2col of the NCHW network input (float32 or bf16 in, bf16 out):
  * col[(b*Ho + oy)*Wo + ox][(c*k + i)*k + j] = x[b][c][oy*s+i-p][ox*s+j-p] (0 outside),

@@ -70,7 +70,8 @@ def column_split_before(cs, index):
     raise ValueError(index)
 
 
-def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argmax=None, dropout=None):
+def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argmax=None, dropout=None,
+                   force_relu=None):
     """All m columns of one replica; returns (per-column losses, per-column grads).
 
     ``dropout`` = (seed, step, row0): the training step's dropout stream and the
@@ -80,7 +81,10 @@ def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argm
     ``force_argmax`` ({layer: [per-column argmax]}) replays another engine's
     max-pool decisions ("teacher forcing"): where a window holds a near-tie
     that float32 and float64 rank differently, the checker then measures the
-    arithmetic of the rest of the step instead of the tie's routing."""
+    arithmetic of the rest of the step instead of the tie's routing.
+    ``force_relu`` ({layer: [per-column bool mask]}) does the same for ReLU
+    decisions at pre-activations within rounding of zero: the backward passes
+    the gradient where the forced mask is set."""
     m = cs.columns
     acts = [np.asarray(x, dtype=np.float64)] * m
     caches = []
@@ -141,7 +145,10 @@ def column_fwd_bwd(cs, col_params, x, labels, loss_scale, trace=None, force_argm
                 grads[j][cl.index] = {"w": gw, "b": gb}
                 gi = gi.reshape(c["in"].shape)
             elif isinstance(L, ReLU):
-                gi = K.relu_backward(c["in"], g[j])
+                if force_relu is not None and cl.index in force_relu:
+                    gi = np.where(np.asarray(force_relu[cl.index][j], dtype=bool), g[j], 0.0)
+                else:
+                    gi = K.relu_backward(c["in"], g[j])
             elif isinstance(L, LRN):
                 gi = K.lrn_backward(c["in"], g[j], L.size, L.k, L.alpha, L.beta)
             elif isinstance(L, Dropout):
@@ -193,8 +200,8 @@ class OracleFabric:
         self.hyper = (lr, momentum, weight_decay)
         self.dropout_seed, self.steps = 0, 0   # dropout stream (rng.dropout_state): seed, step counter
 
-    def step(self, x, y, trace=None, force_argmax=None):
-        """force_argmax: {layer: [replica][column] argmax arrays} (see column_fwd_bwd)."""
+    def step(self, x, y, trace=None, force_argmax=None, force_relu=None):
+        """force_argmax / force_relu: {layer: [replica][column] arrays} (see column_fwd_bwd)."""
         d, m = self.plan.data_shards, self.plan.model_columns
         b = x.shape[0]
         if b % d:
@@ -206,9 +213,10 @@ class OracleFabric:
         for r in range(d):
             lo, hi = r * shard, (r + 1) * shard
             fa = None if force_argmax is None else {k: v[r] for k, v in force_argmax.items()}
+            fr = None if force_relu is None else {k: v[r] for k, v in force_relu.items()}
             losses, grads = column_fwd_bwd(self.cs, self.params, x[lo:hi], labels[lo:hi], scale,
                                            trace=trace if r == 0 else None, force_argmax=fa,
-                                           dropout=(self.dropout_seed, self.steps, lo))
+                                           dropout=(self.dropout_seed, self.steps, lo), force_relu=fr)
             per_replica.append(grads)
             total += losses[0]
         for j in range(m):
@@ -225,6 +233,20 @@ class OracleFabric:
             self.velocity[j] = newv
         self.steps += 1
         return total
+
+    def evaluation_errors(self, x, labels):
+        """`schemes.py:600-645`: misclassifications of replica 0's columns (forward
+        only, the head's logits, argmax ties -> lowest class)."""
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape[0] == 0:
+            return 0
+        trace = {}
+        head = [cl.index for cl in self.cs.col_layers if isinstance(cl.layer, FC)][-1]
+        column_fwd_bwd(self.cs, self.params, x, np.zeros(x.shape[0], dtype=np.int64), 1.0, trace=trace,
+                       dropout=None if not any(isinstance(cl.layer, Dropout) for cl in self.cs.col_layers)
+                       else (self.dropout_seed, self.steps, 0))
+        logits = trace["fwd"][head][0].reshape(x.shape[0], -1)
+        return int(np.count_nonzero(np.argmax(logits, axis=1) != np.asarray(labels, dtype=np.int64)))
 
     def dense_params(self):
         return merge_params(self.params, self.cs)

@@ -79,6 +79,8 @@ SIGNATURES = {
     "pc_s2d_wgrad_finish": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
     "pc_lrn_forward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _i, _vp]),
     "pc_lrn_backward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _vp, _i, _vp]),
+    "pc_synthetic_rows": (_i, [_i, _i, _ll, C.c_ulonglong, _i, _vp, _i, _f, _vp, _i, _vp]),
+    "pc_gather_rows": (_i, [_i, _ll, _vp, _vp, _vp, _vp]),
     "pc_dropout": (_i, [_i, _i, _i, _i, _i, _i, _ll, C.c_ulonglong, _vp, _i, C.c_ulonglong, _f, _vp, _vp, _i, _vp]),
     "pc_counter_add": (_i, [_vp, _ll, _vp]),
     "pc_nchw_to_nhwc": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i, _vp]),

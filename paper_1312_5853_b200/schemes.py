@@ -15,6 +15,7 @@ replaced by bit-identical local updates; the ledger still books it).
 from __future__ import annotations
 
 import gc
+import math
 import os
 from dataclasses import dataclass
 
@@ -487,47 +488,95 @@ def gather_dense_params(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec) 
     return merge_params(cols, cs)
 
 
+def _eval_engines(fabric: Fabric, cs: ColumnizedSpec, b: int, wids: list) -> list:
+    """Forward-only engines of replica 0's hosted columns for evaluation batch b,
+    cached on the fabric (train() evaluates shard after shard of the test split:
+    one allocation per batch size, not per call); parameters are refreshed from
+    the training engines (or the host copy before the first step) at every call."""
+    cache = fabric.__dict__.setdefault("_eval_cache", {})
+    key = (id(cs), b, tuple(wids))
+    engines = cache.get(key)
+    if engines is None:
+        if len(cache) >= 2:          # full shards + one ragged tail
+            cache.pop(next(iter(cache)))
+        engines = []
+        for j in wids:
+            eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, fabric.torch_device, fabric._hyper)
+            eng.training = False     # dropout is the identity at evaluation
+            engines.append(eng)
+        cache[key] = engines
+    for eng in engines:
+        src = fabric._engines.get(eng.wid)
+        if src is not None:
+            eng.p32.copy_(src.p32)
+            if eng.plow is not None:
+                eng.plow.copy_(src.plow)
+        else:
+            eng.load_params(dict.__getitem__(fabric._local[eng.wid], "host_params"))
+    return engines
+
+
+def _book_eval(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, b: int) -> None:
+    """The reference's evaluation ledgers replica 0's cross-layer forward exchange
+    like any other message (`schemes.py:600-645`, FabricExchange.cross_forward)."""
+    m, wire = plan.model_columns, fabric.device.wire_element_size
+    for cl in cs.col_layers:
+        if not cl.cross:
+            continue
+        nbytes = b * (math.prod(cl.in_shape) // m) * wire
+        for j in range(m):
+            for k in range(m):
+                if k != j:
+                    fabric.ledger.record(j, k, nbytes)
+
+
 def evaluation_errors(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, x, labels) -> int:
-    """Misclassifications of replica 0's columns (forward only; ties -> lowest class)."""
+    """Misclassifications of replica 0's columns (forward only; argmax ties ->
+    lowest class), `schemes.py:600-645`. Under torchrun the ranks of replica 0
+    run their column's forward with the column group's all-gather; every rank
+    returns rank 0's count."""
     labels = np.asarray(labels, dtype=np.int64)
     b = int(np.shape(x)[0])
     if b == 0:
         return 0
-    eval_plan = ParallelPlan(1, plan.model_columns, plan.cross_layers)
-    if fabric.dist:
-        raise ValidationError("evaluation_errors under torchrun: gather params and evaluate on rank 0")
-    run = _Runner.__new__(_Runner)
-    run.fabric, run.plan, run.cs, run.shard = fabric, eval_plan, cs, b
+    d, m = plan.data_shards, plan.model_columns
+    if fabric.n != plan.workers:
+        raise ValidationError(f"plan grid {plan.describe()} needs {plan.workers} workers, "
+                              f"fabric has {fabric.n}")
+    if getattr(fabric, "_hyper", None) is None:
+        raise ValidationError("setup_workers must run before evaluation_errors")
+    _book_eval(fabric, plan, cs, b)
     dev = fabric.torch_device
-    m = plan.model_columns
-    with torch.cuda.device(dev):
-        engines = []
-        for j in range(m):
-            src = fabric._engines.get(j)
-            eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, dev, fabric._hyper)
-            eng.training = False   # dropout is the identity at evaluation
-            if src is not None:
-                eng.p32.copy_(src.p32)
-                if eng.plow is not None:
-                    eng.plow.copy_(src.plow)
-            else:
-                eng.load_params(dict.__getitem__(fabric._local[j], "host_params"))
-            engines.append(eng)
+    wids = [w for w in fabric.local_wids if w < m]      # replica 0 = workers 0 .. m-1
+    if fabric.dist:
+        col_g, _ = fabric.groups(d, m)                  # collective: every rank creates the groups
+        ex = NcclExchange(col_g) if m > 1 else None
+    else:
         ex = LocalExchange(dev) if m > 1 else None
-        xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
-        yd = torch.zeros(b, dtype=torch.int32, device=dev)
-        for e in engines:
-            e.load_batch(xd, yd)
-        n = len(cs.col_layers)
-        for i in range(n - 1):          # stop before the softmax: logits = head output
-            if cs.col_layers[i].cross and ex is not None:
-                ex.all_gather(i, engines)
+    count = -1
+    if wids:
+        with torch.cuda.device(dev):
+            engines = _eval_engines(fabric, cs, b, wids)
+            xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+            yd = torch.zeros(b, dtype=torch.int32, device=dev)
             for e in engines:
-                e.forward(i, 1.0)
-        head = engines[0].layers[n - 2]
-        logits = head.out[: b * cs.base.classes].float().reshape(b, cs.base.classes).cpu().numpy()
-    pred = np.argmax(logits, axis=1)
-    return int(np.count_nonzero(pred != labels))
+                e.load_batch(xd, yd)
+            n = len(cs.col_layers)
+            for i in range(n - 1):      # stop before the softmax: logits = head output
+                if cs.col_layers[i].cross and ex is not None:
+                    ex.all_gather(i, engines)
+                for e in engines:
+                    e.forward(i, 1.0)
+            if engines[0].wid == 0:
+                head = engines[0].layers[n - 2]
+                logits = head.out[: b * cs.base.classes].float().reshape(b, cs.base.classes)
+                pred = torch.argmax(logits, dim=1).cpu().numpy()   # first maximum, like np.argmax
+                count = int(np.count_nonzero(pred != labels))
+    if fabric.dist:
+        t = torch.tensor([count], dtype=torch.int64, device=dev)
+        torch.distributed.broadcast(t, src=0)
+        count = int(t.item())
+    return count
 
 
 def reference_step(net: NetworkSpec, params: dict, batch, sgd, precision: str = "fp32") -> StepResult:

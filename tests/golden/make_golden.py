@@ -14,6 +14,8 @@ the reference's own functions on seeded inputs:
                  digests (sum, L2) of gradients-as-updates.
 * host.npz     — SplitMix64 streams, permutations, synthetic data, comm
                  volumes, shape reports (host-logic KATs).
+* eval.npz     — evaluation_errors after one hybrid_step of four plans:
+                 misclassification counts and the exchange bytes it ledgers.
 """
 
 from __future__ import annotations
@@ -197,7 +199,37 @@ def host_fixture():
     np.savez_compressed(OUT / "host.npz", **out)
 
 
+def eval_fixture():
+    """evaluation_errors (`schemes.py:600-645`) after one step of several plans:
+    misclassification counts and the ledger bytes / messages the evaluation books."""
+    out = {}
+    tiny = N.load_network(CONFIGS / "tinynet.net")
+    small = N.load_network(CONFIGS / "alexnet_small64.net")
+    cases = {"tiny_d1m2x3": (tiny, S.ParallelPlan(1, 2, (3,)), 8, 7),
+             "tiny_d2m2x3": (tiny, S.ParallelPlan(2, 2, (3,)), 8, 7),
+             "tiny_d2m1": (tiny, S.ParallelPlan(2, 1), 8, 7),
+             "small64_d1m2x6": (small, S.ParallelPlan(1, 2, (6,)), 4, 3)}
+    for name, (net, plan, batch, seed) in cases.items():
+        train, test = D.gen_synthetic(net.classes, 2, net.input_shape, seed=seed, test_per_class=1)
+        params = S.init_dense_params(net, 3)
+        params = {i: {k: f32(v) for k, v in t.items()} for i, t in params.items()}
+        cs = S.plan_columnized(net, plan)
+        fab = spawn(plan.workers)
+        S.setup_workers(fab, plan, cs, params, K.SgdState())
+        x, y = train.images[:batch], train.labels[:batch]
+        S.hybrid_step(fab, plan, cs, x, y)
+        n_eval = min(test.size, 40 if net is tiny else 16)
+        b0, m0 = fab.ledger.total_bytes, fab.ledger.total_messages
+        wrong = S.evaluation_errors(fab, plan, cs, test.images[:n_eval], test.labels[:n_eval])
+        out[f"{name}_x"], out[f"{name}_y"] = x.astype(np.float32), y      # float32-exact
+        out[f"{name}_tx"], out[f"{name}_ty"] = test.images[:n_eval].astype(np.float32), test.labels[:n_eval]
+        out[f"{name}_wrong"] = np.array(wrong)
+        out[f"{name}_ledger"] = np.array([fab.ledger.total_bytes - b0, fab.ledger.total_messages - m0])
+    np.savez_compressed(OUT / "eval.npz", **out)
+
+
 if __name__ == "__main__":
+    eval_fixture()
     kernels_fixture()
     host_fixture()
     steps_fixture()

@@ -1,5 +1,11 @@
 """Parity helpers shared by the GPU step tests.
 
+ReLU decisions get the same treatment as max-pool ties below: a pre-activation
+within the step's rounding of zero can be positive in one precision and not in
+the other (AlexNet fp32 at b256: a few dozen of 74M conv1 outputs), which moves
+one pixel's whole gradient; the checker asserts each such flip is a near-zero
+and replays the device's mask in the oracle.
+
 End-to-end protocol: max-pool argmax is bit-exact at kernel
 level; end to end, a window whose two largest inputs differ by less than the
 float32 rounding of the step can legitimately rank differently in float32
@@ -34,6 +40,37 @@ def device_argmax(fab, plan):
     return per
 
 
+def device_relu_masks(fab, plan):
+    """{relu layer: [replica][column] bool NCHW mask (device ReLU output > 0)}: the
+    decisions the device's backward applies (fused producer ReLU, consumer mask)."""
+    d, m = plan.data_shards, plan.model_columns
+    per = {}
+    for r in range(d):
+        for j in range(m):
+            eng = fab._engines[plan.worker_of(r, j)]
+            for pos, st in enumerate(eng.layers):
+                if st.kind == "relu":
+                    mask = eng.activation_host(pos, "out") > 0
+                    per.setdefault(st.cl.index, [[None] * m for _ in range(d)])[r][j] = mask
+    return per
+
+
+def assert_relu_near_ties(trace, forced, tie_tol):
+    """Every ReLU decision the device made differently (replica 0) sits at a
+    pre-activation within rounding of zero; returns the number of flips."""
+    flips = 0
+    for layer, per_rep in forced.items():
+        for j, mask in enumerate(per_rep[0]):
+            a = trace["fwd"][layer - 1][j]
+            bad = mask != (a > 0)
+            if bad.any():
+                scale = max(float(np.max(np.abs(a))), 1e-30)
+                worst = float(np.max(np.abs(a[bad])))
+                assert worst <= tie_tol * scale, (layer, j, int(bad.sum()), worst, scale)
+                flips += int(bad.sum())
+    return flips
+
+
 def assert_near_ties(trace, forced, cs, tie_tol=1e-5):
     """Every device/oracle argmax disagreement (replica 0) must be a near-tie."""
     flips = 0
@@ -61,8 +98,10 @@ def oracle_replay(net, plan, dense, x, y, fab, tie_tol=None):
     if tie_tol is None:
         tie_tol = 2e-2 if fab.precision == "bf16" else 1e-5
     forced = device_argmax(fab, plan)
+    relu = device_relu_masks(fab, plan)
     trace = {}
     of = OracleFabric(net, plan, dense)
-    loss = of.step(x, y, trace=trace, force_argmax=forced)
+    loss = of.step(x, y, trace=trace, force_argmax=forced, force_relu=relu)
     flips = assert_near_ties(trace, forced, of.cs, tie_tol)
+    flips += assert_relu_near_ties(trace, relu, tie_tol)
     return of, loss, trace, flips

@@ -56,8 +56,9 @@ def run_steps(net, dense, x, y, precision, steps, graph: bool, monkeypatch):
         eng = fab._engines[0]
         snap = {"loss": res.loss, "p32": eng.p32.clone()}
         if s == 0:
-            from parity import device_argmax
+            from parity import device_argmax, device_relu_masks
             snap["argmax"] = device_argmax(fab, plan)
+            snap["relu"] = device_relu_masks(fab, plan)
             snap["velocity"] = eng.velocity_host()   # zero start: v1 = p1 - p0 = the first update
         out.append(snap)
     run = fab._runner
@@ -74,16 +75,17 @@ def alexnet():
 
 
 def _oracle_first_step(net, dense, x, y, snap, tie_tol):
-    """Oracle step 1 replaying the device's step-1 pool decisions."""
-    from parity import assert_near_ties
+    """Oracle step 1 replaying the device's step-1 pool and ReLU decisions."""
+    from parity import assert_near_ties, assert_relu_near_ties
     from oracle.ref_engine import OracleFabric
     import paper_1312_5853_b200 as P
     from paper_1312_5853_b200.plan import lists_as_params
     plan = P.ParallelPlan(1, 1)
     trace = {}
     of = OracleFabric(net, plan, dense)
-    loss = of.step(x, y, trace=trace, force_argmax=snap["argmax"])
+    loss = of.step(x, y, trace=trace, force_argmax=snap["argmax"], force_relu=snap["relu"])
     flips = assert_near_ties(trace, snap["argmax"], of.cs, tie_tol)
+    flips += assert_relu_near_ties(trace, snap["relu"], tie_tol)
     return loss, lists_as_params(of.velocity[0], of.cs), flips
 
 
@@ -135,7 +137,7 @@ def test_small64_config1_b32_two_steps(precision, loss_tol, upd_tol):
     from oracle.ref_engine import OracleFabric
     from paper_1312_5853_b200 import rng
     from paper_1312_5853_b200.plan import lists_as_params, params_as_lists, split_params
-    from parity import assert_near_ties, device_argmax
+    from parity import assert_near_ties, assert_relu_near_ties, device_argmax, device_relu_masks
     net = P.load_network(CONFIGS / "alexnet_small64.net")
     tr, _ = P.gen_synthetic(100, 4, net.input_shape, seed=0)
     dense = f32_params(P.init_dense_params(net, 0))
@@ -150,10 +152,11 @@ def test_small64_config1_b32_two_steps(precision, loss_tol, upd_tol):
         idx = order[step * 32:(step + 1) * 32]
         x, y = tr.images[idx], tr.labels[idx]
         res = P.hybrid_step(fab, plan, cs, x, y)
-        forced = device_argmax(fab, plan)
+        forced, relu = device_argmax(fab, plan), device_relu_masks(fab, plan)
         trace = {}
-        oloss = of.step(x, y, trace=trace, force_argmax=forced)
+        oloss = of.step(x, y, trace=trace, force_argmax=forced, force_relu=relu)
         assert_near_ties(trace, forced, of.cs, tie)
+        assert_relu_near_ties(trace, relu, tie)
         assert abs(res.loss - oloss) / abs(oloss) < loss_tol, (step, res.loss, oloss)
         eng = fab._engines[0]
         got = eng.velocity_host()

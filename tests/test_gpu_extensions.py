@@ -21,13 +21,16 @@ def _dev(a, dtype):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
-def test_lrn_kernels_match_definition(prec):
+@pytest.mark.parametrize("C,size", [(48, 5), (96, 5), (256, 9), (44, 5), (16, 3)])
+def test_lrn_kernels_match_definition(prec, C, size):
+    """C % 8 == 0 and size <= 9: the 8-channel vector kernels (sliding window sums
+    across neighbouring groups and the tensor's channel edges); C = 44: scalar."""
     import torch
     from oracle import ref_kernels as O
     from paper_1312_5853_b200 import _lib as L
     lib = L.lib()
     rs = np.random.RandomState(3)
-    B, C, H, W = 3, 48, 5, 7
+    B, H, W = 3, 5, 7
     x = np.maximum(rs.randn(B, C, H, W), 0.0) * 3.0
     g = rs.randn(B, C, H, W)
     dt, pc = (torch.float32, L.PC_FP32) if prec == "fp32" else (torch.bfloat16, L.PC_BF16)
@@ -36,7 +39,7 @@ def test_lrn_kernels_match_definition(prec):
     xd, gd = _dev(xr.transpose(0, 2, 3, 1), dt), _dev(gr.transpose(0, 2, 3, 1), dt)
     y, gx = torch.empty_like(xd), torch.empty_like(xd)
     st = torch.cuda.current_stream().cuda_stream
-    args = (5, 2.0, 1e-2, 0.75)
+    args = (size, 2.0, 1e-2, 0.75)
     lib.call("pc_lrn_forward", B * H * W, C, *args, xd.data_ptr(), y.data_ptr(), pc, st)
     lib.call("pc_lrn_backward", B * H * W, C, *args, xd.data_ptr(), gd.data_ptr(), gx.data_ptr(), pc, st)
     want_y = O.lrn_forward(xr, *args)

@@ -185,3 +185,25 @@ def test_alexnet_reference_step_digest():
             d = newp[i][k] - params[i][k]
             dig = g[f"d_{i}_{k}"]
             assert abs(np.sqrt((d ** 2).sum()) - dig[1]) <= 1e-9 * max(dig[1], 1e-15)
+
+
+EVAL = np.load(GOLDEN / "eval.npz")
+EVAL_CASES = {"tiny_d1m2x3": ("tinynet", (1, 2, (3,))), "tiny_d2m2x3": ("tinynet", (2, 2, (3,))),
+              "tiny_d2m1": ("tinynet", (2, 1, ())), "small64_d1m2x6": ("alexnet_small64", (1, 2, (6,)))}
+
+
+@pytest.mark.parametrize("name", sorted(EVAL_CASES))
+def test_oracle_evaluation_errors_match_reference(name):
+    """evaluation_errors after one step (`schemes.py:600-645`) vs the reference's count.
+    (Dropout-free nets: the forward is deterministic in the oracle.)"""
+    from paper_1312_5853_b200.netdef import load_network
+    from paper_1312_5853_b200.plan import ParallelPlan, init_dense_params
+    from oracle.ref_engine import OracleFabric
+    net_name, (d, m, cross) = EVAL_CASES[name]
+    net = load_network(CONFIGS / f"{net_name}.net")
+    params = {i: {k: v.astype(np.float32).astype(np.float64) for k, v in t.items()}
+              for i, t in init_dense_params(net, 3).items()}
+    of = OracleFabric(net, ParallelPlan(d, m, cross), params)
+    of.step(EVAL[f"{name}_x"].astype(np.float64), EVAL[f"{name}_y"])
+    got = of.evaluation_errors(EVAL[f"{name}_tx"], EVAL[f"{name}_ty"])
+    assert got == int(EVAL[f"{name}_wrong"])
