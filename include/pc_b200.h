@@ -12,6 +12,9 @@
  *  - All pointers are DEVICE pointers unless noted; sizes are element counts.
  *  - Activations are NHWC ("channels last"), row = pixel (b, y, x), in the
  *    storage precision `prec` (PC_FP32 -> float, PC_BF16 -> __nv_bfloat16).
+ *    The contraction entry points (conv / FC forward and backward and their
+ *    workspace queries) also take PC_TF32: float storage, tcgen05 kind::tf32
+ *    tensor-core math (geometries it cannot tile fall back to the fp32 SIMT path).
  *    Master weights, velocities and weight gradients are always float.
  *  - A channel-blocked activation (the cross-layer concatenation of m column
  *    slices) stores channel c at  base + (c / cs) * cstride + pixel * cs + c % cs.
@@ -42,7 +45,7 @@ extern "C" {
 
 typedef void* pc_stream_t; /* cudaStream_t */
 
-enum pc_prec { PC_FP32 = 0, PC_BF16 = 1 };
+enum pc_prec { PC_FP32 = 0, PC_BF16 = 1, PC_TF32 = 2 };
 enum pc_status { PC_OK = 0, PC_ESHAPE = 1, PC_EVALUE = 2, PC_ECUDA = 3, PC_ENCCL = 4 };
 enum pc_conv_flags { PC_RELU = 1, PC_WANT_DX = 2, PC_WANT_DW = 4, PC_MASK_DX = 8, PC_WT_PRESET = 16,
                      /* forward: the last 16 input channels have structural-zero filter
@@ -73,6 +76,8 @@ PC_API unsigned long long pc_launch_count(void);
  * CUDA-core kernel used only for extents the tensor-core path cannot tile
  * (e.g. a 10-class head: rows not 16-byte aligned). */
 PC_API void pc_contraction_counts(unsigned long long* tensor_core, unsigned long long* simt);
+/* Launches of the tf32 tensor-core kernels (tcgen05.mma kind::tf32) so far. */
+PC_API unsigned long long pc_tf32_contractions(void);
 /* Debug (tools/trace_gemm.py): per-tile clock64 timeline of the following tensor-core
  * GEMM launches into a device buffer of >= grid x 64 tiles x 8 u64; NULL turns it off. */
 PC_API void pc_debug_trace_gemm(void* buf);
@@ -236,6 +241,10 @@ PC_API int pc_gather_rows(int n, long long row_bytes, const void* src, const lon
  * pc_fc_forward / pc_fc_backward over pixels with weights [N][Kp]. */
 PC_API int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const void* src, int src_prec,
                      void* dst, pc_stream_t stream);
+/* Same with the output precision selectable (PC_BF16 or PC_FP32: the tf32 mode's
+ * input layer, columns padded to a multiple of 32). */
+PC_API int pc_im2col_ex(int B, int C, int H, int W, int k, int s, int p, int Kp, const void* src, int src_prec,
+                        void* dst, int dst_prec, pc_stream_t stream);
 /* Space-to-depth of the NCHW network input (float32 or bf16 in, bf16 out) for a
  * strided input conv: dst[b][Y][X][(dy*s + dx)*C + c] = x[b][c][Y*s+dy-p][X*s+dx-p]
  * (0 outside the image and for channels >= s*s*C), Y < ceil((H+2p)/s), channels

@@ -16,7 +16,7 @@ from .errors import status_error
 
 LIB_PATH = Path(__file__).resolve().parent / "libpcb200.so"
 
-PC_FP32, PC_BF16 = 0, 1
+PC_FP32, PC_BF16, PC_TF32 = 0, 1, 2
 PC_RELU, PC_WANT_DX, PC_WANT_DW, PC_MASK_DX, PC_WT_PRESET, PC_ZERO_TAIL16 = 1, 2, 4, 8, 16, 32
 
 _vp, _i, _ll, _sz, _f, _d = C.c_void_p, C.c_int, C.c_longlong, C.c_size_t, C.c_float, C.c_double
@@ -46,6 +46,7 @@ SIGNATURES = {
     "pc_launch_count": (C.c_ulonglong, []),
     "pc_contraction_counts": (None, [_vp, _vp]),
     "pc_has_tcgen05": (_i, []),
+    "pc_tf32_contractions": (C.c_ulonglong, []),
     "pc_debug_trace_gemm": (None, [_vp]),
     "pc_conv2d_forward": (_i, [_P(ConvGeom), _vp, _vp, _vp, _vp, _i, _i, _vp]),
     "pc_conv2d_backward_workspace": (_sz, [_P(ConvGeom), _i]),
@@ -79,6 +80,7 @@ SIGNATURES = {
     "pc_s2d_wgrad_finish": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
     "pc_lrn_forward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _i, _vp]),
     "pc_lrn_backward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _vp, _i, _vp]),
+    "pc_im2col_ex": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp]),
     "pc_synthetic_rows": (_i, [_i, _i, _ll, C.c_ulonglong, _i, _vp, _i, _f, _vp, _i, _vp]),
     "pc_gather_rows": (_i, [_i, _ll, _vp, _vp, _vp, _vp]),
     "pc_dropout": (_i, [_i, _i, _i, _i, _i, _i, _ll, C.c_ulonglong, _vp, _i, C.c_ulonglong, _f, _vp, _vp, _i, _vp]),

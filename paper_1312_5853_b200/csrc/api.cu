@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "gemm_ops.cuh"
+#include "tf32.cuh"
 #include "umma.cuh"
 
 namespace pc {
@@ -380,6 +381,12 @@ static int check_prec(int prec) {
   PC_REQUIRE(prec == PC_FP32 || prec == PC_BF16, PC_EVALUE, "unknown precision %d", prec);
   return PC_OK;
 }
+// contraction entry points also take PC_TF32: float storage, tf32 tensor-core math
+static int check_cprec(int prec) {
+  PC_REQUIRE(prec == PC_FP32 || prec == PC_BF16 || prec == PC_TF32, PC_EVALUE, "unknown precision %d", prec);
+  return PC_OK;
+}
+static int storage(int prec) { return prec == PC_TF32 ? PC_FP32 : prec; }
 
 }  // namespace pc
 
@@ -398,19 +405,28 @@ extern "C" int pc_has_tcgen05(void) { return umma_available() ? 1 : 0; }
 extern "C" int pc_conv2d_forward(const pc_conv_geom* g, const void* x, const void* w, const float* bias,
                                  void* y, int prec, int flags, pc_stream_t st) {
   int rc = check_geom(g);
-  if (rc || (rc = check_prec(prec))) return rc;
+  if (rc || (rc = check_cprec(prec))) return rc;
   if (g->B == 0) return PC_OK;
   if (prec == PC_BF16) return umma_conv_forward(*g, x, w, bias, y, flags, S(st));
-  return simt_conv_forward(*g, x, w, bias, y, prec, flags, S(st));
+  if (prec == PC_TF32 && tf32_conv_ok(*g))
+    return tf32_conv_forward(*g, static_cast<const float*>(x), static_cast<const float*>(w), bias,
+                             static_cast<float*>(y), flags, S(st));
+  return simt_conv_forward(*g, x, w, bias, y, storage(prec), flags, S(st));
 }
+
+static bool tf32_conv_dgrad_ok(const pc_conv_geom& g) { return tf32_conv_ok(g) && g.stride == 1 && g.N % 32 == 0; }
 
 extern "C" size_t pc_conv2d_backward_workspace(const pc_conv_geom* g, int prec) {
   if (check_geom(g)) return 0;
   long long P = (long long)g->B * g->Ho * g->Wo;
   long long MN = (long long)g->N * g->k * g->k * g->C;
-  long long splits = prec == PC_BF16 ? umma_wgrad_splits(*g) : simt_splits(g->N, g->k * g->k * g->C, P);
+  const bool tc32 = prec == PC_TF32 && tf32_conv_ok(*g);
+  long long splits = prec == PC_BF16 ? umma_wgrad_splits(*g)
+                     : tc32 ? tf32_wgrad_splits(*g) : simt_splits(g->N, g->k * g->k * g->C, P);
   long long floats = (splits > 1 ? splits * MN : 0) + colsum_ws(P, g->N);
-  return (size_t)floats * sizeof(float) + umma_conv_extra_ws(*g, prec);
+  size_t extra = prec == PC_BF16 ? umma_conv_extra_ws(*g, prec)
+                 : (prec == PC_TF32 && tf32_conv_dgrad_ok(*g)) ? tf32_dgrad_ws(*g) : 0;
+  return (size_t)floats * sizeof(float) + extra;
 }
 
 extern "C" int pc_conv2d_backward(const pc_conv_geom* g, const void* x, const void* w, const void* gy,
@@ -423,7 +439,7 @@ extern "C" int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const
                                      void* gx, const void* mask, float* gw, float* gb, int prec, int flags,
                                      void* workspace, size_t ws_bytes, const pc_sgd_fuse* upd, pc_stream_t st) {
   int rc = check_geom(g);
-  if (rc || (rc = check_prec(prec))) return rc;
+  if (rc || (rc = check_cprec(prec))) return rc;
   size_t need = pc_conv2d_backward_workspace(g, prec);
   PC_REQUIRE(!(flags & PC_WANT_DW) || ws_bytes >= need, PC_EVALUE,
              "conv2d_backward: workspace %zu B < required %zu B", ws_bytes, need);
@@ -432,8 +448,16 @@ extern "C" int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const
     if (g->B == 0) return PC_OK;
     const void* mk = (flags & PC_MASK_DX) ? mask : nullptr;
     PC_REQUIRE(!(flags & PC_WT_PRESET) || prec == PC_BF16, PC_EVALUE, "PC_WT_PRESET: bf16 path only");
-    rc = prec == PC_BF16 ? umma_conv_dgrad(*g, w, gy, gx, mk, S(st), workspace, ws_bytes, (flags & PC_WT_PRESET) != 0)
-                         : simt_conv_dgrad(*g, w, gy, gx, mk, S(st), prec);
+    if (prec == PC_TF32 && tf32_conv_dgrad_ok(*g)) {
+      // the rotated filters live at the end of the workspace (after the colsum / split-K regions)
+      PC_REQUIRE(workspace != nullptr && ws_bytes >= need, PC_EVALUE, "conv2d_backward: tf32 needs the workspace");
+      float* wt = reinterpret_cast<float*>(static_cast<char*>(workspace) + need - tf32_dgrad_ws(*g));
+      rc = tf32_conv_dgrad(*g, static_cast<const float*>(w), static_cast<const float*>(gy), static_cast<float*>(gx),
+                           static_cast<const float*>(mk), wt, S(st));
+    } else {
+      rc = prec == PC_BF16 ? umma_conv_dgrad(*g, w, gy, gx, mk, S(st), workspace, ws_bytes, (flags & PC_WT_PRESET) != 0)
+                           : simt_conv_dgrad(*g, w, gy, gx, mk, S(st), storage(prec));
+    }
     if (rc) return rc;
   }
   if (flags & PC_WANT_DW) {
@@ -444,15 +468,18 @@ extern "C" int pc_conv2d_backward_ex(const pc_conv_geom* g, const void* x, const
       return PC_OK;
     }
     if (gb) {  // null: the caller derives the bias gradient otherwise (pc_s2d_wgrad_finish)
-      rc = colsum(gy, P, g->N, prec, gb, ws, S(st));
+      rc = colsum(gy, P, g->N, storage(prec), gb, ws, S(st));
       if (rc) return rc;
     }
     float* part = ws + colsum_ws(P, g->N);
     if (prec == PC_BF16) {
       rc = umma_conv_wgrad(*g, x, gy, gw, part, S(st), upd);
+    } else if (prec == PC_TF32 && tf32_conv_ok(*g)) {
+      PC_REQUIRE(upd == nullptr, PC_EVALUE, "fused SGD update: bf16 tensor-core path only");
+      rc = tf32_conv_wgrad(*g, static_cast<const float*>(x), static_cast<const float*>(gy), gw, part, S(st));
     } else {
       PC_REQUIRE(upd == nullptr, PC_EVALUE, "fused SGD update: bf16 tensor-core path only");
-      rc = simt_conv_wgrad(*g, x, gy, gw, part, simt_splits(g->N, g->k * g->k * g->C, P), S(st), prec);
+      rc = simt_conv_wgrad(*g, x, gy, gw, part, simt_splits(g->N, g->k * g->k * g->C, P), S(st), storage(prec));
     }
     if (rc) return rc;
   }
@@ -477,13 +504,15 @@ extern "C" size_t pc_fc_forward_workspace(int B, int D, int U, int prec) {
 
 extern "C" int pc_fc_forward_ex(int B, int D, int U, const pc_mat* x, const void* w, const float* bias, void* y,
                                 int prec, int flags, void* workspace, size_t ws_bytes, pc_stream_t st) {
-  int rc = check_prec(prec);
+  int rc = check_cprec(prec);
   if (rc) return rc;
   PC_REQUIRE(B >= 0 && D > 0 && U > 0, PC_ESHAPE, "fc: bad extents B=%d D=%d U=%d", B, D, U);
   if (B == 0) return PC_OK;
   if ((rc = check_mat(x, "fc_forward x"))) return rc;
   if (prec == PC_BF16) return umma_fc_forward(B, D, U, *x, w, bias, y, flags, S(st), workspace, ws_bytes);
-  return simt_fc_forward(B, D, U, *x, w, bias, y, prec, flags, S(st));
+  if (prec == PC_TF32 && tf32_fc_ok(D, U, *x))
+    return tf32_fc_forward(B, D, U, *x, static_cast<const float*>(w), bias, static_cast<float*>(y), flags, S(st));
+  return simt_fc_forward(B, D, U, *x, w, bias, y, storage(prec), flags, S(st));
 }
 
 extern "C" int pc_fc_forward(int B, int D, int U, const pc_mat* x, const void* w, const float* bias,
@@ -494,6 +523,10 @@ extern "C" int pc_fc_forward(int B, int D, int U, const pc_mat* x, const void* w
 extern "C" size_t pc_fc_backward_workspace(int B, int D, int U, int prec) {
   // the data gradient's split-K partials run first and reuse the weight gradient's region
   size_t dg = prec == PC_BF16 && B > 0 ? umma_fc_dgrad_ws(B, D, U) : 0;
+  if (prec == PC_TF32) {  // split-K partials of the tf32 weight gradient
+    const long long sp = B > 0 ? tf32_fc_wgrad_splits(B, D, U) : 1;
+    return (size_t)colsum_ws(B, U) * sizeof(float) + (sp > 1 ? (size_t)sp * U * D * sizeof(float) : 0);
+  }
   return (size_t)colsum_ws(B, U) * sizeof(float) + std::max(umma_fc_extra_ws(B, D, U, prec), dg);
 }
 
@@ -506,7 +539,7 @@ extern "C" int pc_fc_backward(int B, int D, int U, const pc_mat* x, const void* 
 extern "C" int pc_fc_backward_ex(int B, int D, int U, const pc_mat* x, const void* w, const void* gy,
                                  const pc_mat* gx, const void* mask, float* gw, float* gb, int prec, int flags,
                                  void* workspace, size_t ws_bytes, const pc_sgd_fuse* upd, pc_stream_t st) {
-  int rc = check_prec(prec);
+  int rc = check_cprec(prec);
   if (rc) return rc;
   PC_REQUIRE(B >= 0 && D > 0 && U > 0, PC_ESHAPE, "fc: bad extents B=%d D=%d U=%d", B, D, U);
   size_t need = pc_fc_backward_workspace(B, D, U, prec);
@@ -515,8 +548,12 @@ extern "C" int pc_fc_backward_ex(int B, int D, int U, const pc_mat* x, const voi
     if ((rc = check_mat(gx, "fc_backward gx"))) return rc;
     if (B > 0) {
       const void* mk = (flags & PC_MASK_DX) ? mask : nullptr;
-      rc = prec == PC_BF16 ? umma_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st), workspace, ws_bytes)
-                           : simt_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st), prec);
+      if (prec == PC_TF32 && tf32_fc_ok(D, U, *gx))
+        rc = tf32_fc_dgrad(B, D, U, static_cast<const float*>(w), static_cast<const float*>(gy), *gx,
+                           static_cast<const float*>(mk), S(st));
+      else
+        rc = prec == PC_BF16 ? umma_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st), workspace, ws_bytes)
+                             : simt_fc_dgrad(B, D, U, w, gy, *gx, mk, S(st), storage(prec));
       if (rc) return rc;
     }
   }
@@ -529,12 +566,15 @@ extern "C" int pc_fc_backward_ex(int B, int D, int U, const pc_mat* x, const voi
     }
     float* ws = static_cast<float*>(workspace);
     if (gb) {  // null: the caller derives the bias gradient otherwise (pc_bias_grad)
-      rc = colsum(gy, B, U, prec, gb, ws, S(st));
+      rc = colsum(gy, B, U, storage(prec), gb, ws, S(st));
       if (rc) return rc;
     }
     PC_REQUIRE(upd == nullptr || prec == PC_BF16, PC_EVALUE, "fused SGD update: bf16 tensor-core path only");
-    rc = prec == PC_BF16 ? umma_fc_wgrad(B, D, U, *x, gy, gw, ws + colsum_ws(B, U), S(st), upd)
-                         : simt_fc_wgrad(B, D, U, *x, gy, gw, S(st), prec);
+    if (prec == PC_TF32 && tf32_fc_ok(D, U, *x))
+      rc = tf32_fc_wgrad(B, D, U, *x, static_cast<const float*>(gy), gw, ws + colsum_ws(B, U), S(st));
+    else
+      rc = prec == PC_BF16 ? umma_fc_wgrad(B, D, U, *x, gy, gw, ws + colsum_ws(B, U), S(st), upd)
+                           : simt_fc_wgrad(B, D, U, *x, gy, gw, S(st), storage(prec));
     if (rc) return rc;
   }
   return PC_OK;

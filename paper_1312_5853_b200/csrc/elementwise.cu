@@ -757,9 +757,9 @@ __global__ void nchw_to_nhwc_k(int B, int C, int H, int W, int Cp, const float* 
 // zero-padded to Kp columns, straight from the float32 NCHW batch. One CTA per
 // output row (b, oy): the C*k input rows it needs are staged in shared memory,
 // then the Wo x Kp output rows are written with 16-byte stores.
-template <typename TS>
+template <typename TS, typename TD>
 __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, int Wo, int Kp,
-                              const TS* __restrict__ x, __nv_bfloat16* __restrict__ col) {
+                              const TS* __restrict__ x, TD* __restrict__ col) {
   extern __shared__ float rows[];  // [C][k][W]
   const int bo = blockIdx.x;
   const int b = bo / Ho, oy = bo - b * Ho;
@@ -771,7 +771,7 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
   }
   __syncthreads();
   const int K = C * k * k, chunks = Kp / 8;
-  __nv_bfloat16* out = col + (long long)bo * Wo * Kp;
+  TD* out = col + (long long)bo * Wo * Kp;
   for (int t = threadIdx.x; t < Wo * chunks; t += blockDim.x) {
     int ox = t / chunks, q = t - ox * chunks;
     float v[8];
@@ -786,7 +786,7 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
       }
       v[e] = val;
     }
-    Vec8<__nv_bfloat16>::store(out + (long long)ox * Kp + q * 8, v);
+    Vec8<TD>::store(out + (long long)ox * Kp + q * 8, v);
   }
 }
 
@@ -1180,6 +1180,11 @@ extern "C" int pc_nchw_to_nhwc(int B, int C, int H, int W, int Cp, const float* 
 
 extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp, const void* src, int src_prec,
                          void* dst, pc_stream_t st) {
+  return pc_im2col_ex(B, C, H, W, k, s, p, Kp, src, src_prec, dst, PC_BF16, st);
+}
+
+extern "C" int pc_im2col_ex(int B, int C, int H, int W, int k, int s, int p, int Kp, const void* src, int src_prec,
+                            void* dst, int dst_prec, pc_stream_t st) {
   PC_REQUIRE(B >= 0 && C > 0 && k > 0 && s > 0 && p >= 0 && Kp % 8 == 0 && Kp >= C * k * k, PC_EVALUE,
              "im2col: bad arguments (Kp must be a multiple of 8 and >= C*k*k)");
   int sh = H + 2 * p - k, sw = W + 2 * p - k;
@@ -1189,10 +1194,12 @@ extern "C" int pc_im2col(int B, int C, int H, int W, int k, int s, int p, int Kp
   PC_REQUIRE(smem <= 200 * 1024, PC_EVALUE, "im2col: input rows do not fit shared memory");
   if (B == 0) return PC_OK;
   DISPATCH_PREC(src_prec, TS, {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(im2col_rows_k<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    im2col_rows_k<TS><<<B * Ho, 256, smem, S(st)>>>(C, H, W, k, s, p, Ho, Wo, Kp, static_cast<const TS*>(src),
-                                                    static_cast<__nv_bfloat16*>(dst));
+    DISPATCH_PREC(dst_prec, TD, {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(im2col_rows_k<TS, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      im2col_rows_k<TS, TD><<<B * Ho, 256, smem, S(st)>>>(C, H, W, k, s, p, Ho, Wo, Kp, static_cast<const TS*>(src),
+                                                          static_cast<TD*>(dst));
+    });
   });
   PC_CUDA_CHECK_LAUNCH("im2col");
   return PC_OK;

@@ -80,10 +80,13 @@ class ColumnEngine:
     """One worker's buffers and step program on one device."""
 
     def __init__(self, cs: ColumnizedSpec, wid: int, replica: int, column: int, shard: int,
-                 prec: int, device: torch.device, hyper: tuple):
+                 prec: int, device: torch.device, hyper: tuple, cprec: int | None = None):
         self.cs, self.m = cs, cs.columns
         self.wid, self.replica, self.column = wid, replica, column
+        # prec: storage precision of activations (PC_FP32 / PC_BF16); cprec: the
+        # contractions' (PC_TF32 = float storage, tf32 tensor-core math)
         self.B, self.prec, self.device = shard, prec, device
+        self.cprec = prec if cprec is None else cprec
         self.lr, self.mom, self.wd = (float(h) for h in hyper)
         self.dtype = torch_dtype(prec)
         self.lib = L.lib()
@@ -133,9 +136,11 @@ class ColumnEngine:
             # layer's bias gradient (pc_s2d_wgrad_finish); its weights stay 0
             self.s2d_ones = c * lay0.stride ** 2 if c * lay0.stride ** 2 < 64 and \
                 os.environ.get("PC_S2D_ONES", "1") != "0" else -1
-        elif self.prec == L.PC_BF16 and lay0 is not None and c % 64:
+        elif (self.prec == L.PC_BF16 or self.cprec == L.PC_TF32) and lay0 is not None and c % 32:
+            # tf32: the tensor-core im2col path needs 32-channel (128-byte) rows too
             k0 = lay0.kernel
-            self.col_kp = (c * k0 * k0 + 7) // 8 * 8
+            q = 8 if self.prec == L.PC_BF16 else 32
+            self.col_kp = (c * k0 * k0 + q - 1) // q * q
             ho0, wo0 = first.out_shape[1], first.out_shape[2]
             self.x = self._new(B * ho0 * wo0 * self.col_kp)
         else:
@@ -308,13 +313,13 @@ class ColumnEngine:
         for st in self.layers:
             if st.kind == "conv" and st.col:
                 g = st.geom
-                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B * g.Ho * g.Wo, st.col, g.N, self.prec))
+                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B * g.Ho * g.Wo, st.col, g.N, self.cprec))
             elif st.kind == "conv":
-                ws = max(ws, self.lib.raw("pc_conv2d_backward_workspace")(C.byref(st.geom), self.prec))
+                ws = max(ws, self.lib.raw("pc_conv2d_backward_workspace")(C.byref(st.geom), self.cprec))
             elif st.kind == "fc":
                 d = math.prod(st.in_nhwc)
-                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B, d, st.cl.out_shape[0], self.prec),
-                         self.lib.raw("pc_fc_forward_workspace")(self.B, d, st.cl.out_shape[0], self.prec))
+                ws = max(ws, self.lib.raw("pc_fc_backward_workspace")(self.B, d, st.cl.out_shape[0], self.cprec),
+                         self.lib.raw("pc_fc_forward_workspace")(self.B, d, st.cl.out_shape[0], self.cprec))
         self.ws_bytes = int(ws)
         self.ws = torch.empty(max(self.ws_bytes, 16), dtype=torch.uint8, device=self.device)
 
@@ -619,9 +624,9 @@ class ColumnEngine:
                           src_prec, self.s2d_ones, self.x.data_ptr(), self.stream)
         elif self.col_kp:
             lay = self.cs.col_layers[0].layer
-            self._pcall(-1, "input", "pc_im2col", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
+            self._pcall(-1, "input", "pc_im2col_ex", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
                           x_nchw.data_ptr(), L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32,
-                          self.x.data_ptr(), self.stream)
+                          self.x.data_ptr(), self.prec, self.stream)
         else:
             self._pcall(-1, "input", "pc_nchw_to_nhwc", self.B, c, h, w, self.in_cp, x_nchw.data_ptr(),
                           self.x.data_ptr(), self.prec, self.stream)
@@ -633,20 +638,20 @@ class ColumnEngine:
             g = st.geom
             mat = L.Mat(st.inp.data_ptr(), st.col, st.col, 0)
             self._call(st, "pc_fc_forward", self.B * g.Ho * g.Wo, st.col, g.N, C.byref(mat), self._w_lowp(st),
-                       self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec,
+                       self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.cprec,
                        L.PC_RELU if st.relu_after else 0, s)
         elif st.kind == "conv":
             flags = L.PC_RELU if st.relu_after else 0
             if st.s2d and st.cp - self.in_c * st.s2d ** 2 >= 16 and os.environ.get("PC_ZERO_TAIL", "1") != "0":
                 flags |= L.PC_ZERO_TAIL16   # channels >= 48 of the 64 are structural zeros (and the ones channel)
             self._call(st, "pc_conv2d_forward", C.byref(st.geom), st.inp.data_ptr(), self._w_lowp(st),
-                     self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, s)
+                     self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.cprec, flags, s)
         elif st.kind == "fc":
             d = math.prod(st.in_nhwc)
             mat = self._in_mat(st)
             flags = L.PC_RELU if st.relu_after else 0
             self._call(st, "pc_fc_forward_ex", self.B, d, st.cl.out_shape[0], C.byref(mat), self._w_lowp(st),
-                       self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.prec, flags, self.ws.data_ptr(),
+                       self.p32[st.b_off:].data_ptr(), st.out.data_ptr(), self.cprec, flags, self.ws.data_ptr(),
                        self.ws_bytes, s)
         elif st.kind == "relu":
             if not st.relu_fused_fwd:
@@ -700,7 +705,7 @@ class ColumnEngine:
             mat = L.Mat(st.inp.data_ptr(), st.col, st.col, 0)
             self._call(st, "pc_fc_backward", self.B * g.Ho * g.Wo, st.col, g.N, C.byref(mat), self._w_lowp(st),
                        st.gout.data_ptr(), C.byref(mat), None, self.g32[st.w_off:].data_ptr(),
-                       self.g32[st.b_off:].data_ptr(), self.prec, L.PC_WANT_DW, self.ws.data_ptr(),
+                       self.g32[st.b_off:].data_ptr(), self.cprec, L.PC_WANT_DW, self.ws.data_ptr(),
                        self.ws_bytes, s)
         elif st.kind == "conv":
             flags = L.PC_WANT_DW | (L.PC_WANT_DX if want_dx else 0) | (L.PC_MASK_DX if st.mask_dx else 0)
@@ -718,10 +723,10 @@ class ColumnEngine:
                 if want_dx:
                     self.lib.call("pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
                                   st.gout.data_ptr(), st.gin.data_ptr(), st.inp.data_ptr() if st.mask_dx else None,
-                                  None, None, self.prec, flags & ~L.PC_WANT_DW, None, 0, None, s)
+                                  None, None, self.cprec, flags & ~L.PC_WANT_DW, None, 0, None, s)
                 self._fork(wg)
                 self.lib.call("pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
-                              st.gout.data_ptr(), None, None, self.g32[st.w_off:].data_ptr(), gb, self.prec,
+                              st.gout.data_ptr(), None, None, self.g32[st.w_off:].data_ptr(), gb, self.cprec,
                               L.PC_WANT_DW, self.ws_wg.data_ptr(), self.ws_bytes, C.byref(upd), wg.cuda_stream)
                 if st.keep is not None:   # (not reached: the input layer's update is not fused)
                     raise RuntimeError("weight-gradient side stream: masked layer")
@@ -730,7 +735,7 @@ class ColumnEngine:
                 st, "pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
                 st.gout.data_ptr(), st.gin.data_ptr() if want_dx else None,
                 st.inp.data_ptr() if st.mask_dx else None,
-                self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(), self.prec, f,
+                self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(), self.cprec, f,
                 self.ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None, s, tag=tag))
         elif st.kind == "fc":
             d = math.prod(st.in_nhwc)
@@ -745,7 +750,7 @@ class ColumnEngine:
                 self._call(st, "pc_fc_backward_ex", self.B, d, u, C.byref(xm), self._w_lowp(st), st.gout.data_ptr(),
                            C.byref(gm), st.inp.data_ptr() if st.mask_dx else None,
                            self.g32[st.w_off:].data_ptr(), None if no_gb else self.g32[st.b_off:].data_ptr(),
-                           self.prec, f, ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None,
+                           self.cprec, f, ws.data_ptr(), self.ws_bytes, C.byref(upd) if upd is not None else None,
                            stream, tag=tag)
 
             side = getattr(self, "fc_side", None)

@@ -148,13 +148,16 @@ class Fabric:
             raise ValidationError(f"fabric needs at least one worker, got {n}")
         if scheduling not in ("lockstep", "threads"):
             raise ValidationError(f"unknown scheduling mode {scheduling!r}")
-        if precision not in ("bf16", "fp32"):
-            raise ValidationError(f"unknown precision {precision!r} (bf16 | fp32)")
+        if precision not in ("bf16", "fp32", "tf32"):
+            raise ValidationError(f"unknown precision {precision!r} (bf16 | tf32 | fp32)")
         self.n = n
         self.device = device or DeviceSpec()
         self.scheduling, self.idle_timeout = scheduling, idle_timeout
         self.precision = precision
+        # storage precision of activations, and the contractions' (tf32: float storage,
+        # tcgen05 kind::tf32 tensor-core math; fp32: the exact SIMT verification mode)
         self.prec = L.PC_BF16 if precision == "bf16" else L.PC_FP32
+        self.cprec = L.PC_TF32 if precision == "tf32" else self.prec
         self.ledger = CommLedger()
         self.meter = MemoryMeter(n)
         self._local = [_LocalState(self, w) for w in range(n)]

@@ -4,7 +4,8 @@ NCHW numpy arguments, same errors, computed on the B200 through the C ABI.
 These are the unit-parity entry points (the reference's tests call kernels
 one at a time on host arrays). Each call uploads its operands, runs the
 device kernel in the module precision (``set_precision``; "fp32" =
-verification mode by default, "bf16" = tensor-core mode) and returns
+verification mode by default, "bf16" = tensor-core mode, "tf32" = float
+storage with tf32 tensor-core contractions) and returns
 float64 numpy arrays. Like the reference they are pure: inputs are never
 aliased or modified. The training step itself never goes through this
 module — it keeps everything resident (``engine.py``).
@@ -22,7 +23,7 @@ from . import _lib as L
 from .errors import ShapeError, ValidationError
 from .netdef import conv_output_size
 
-_PREC = {"fp32": L.PC_FP32, "bf16": L.PC_BF16}
+_PREC = {"fp32": L.PC_FP32, "bf16": L.PC_BF16, "tf32": L.PC_TF32}
 _state = {"prec": L.PC_FP32}
 
 
@@ -30,6 +31,11 @@ def set_precision(name: str) -> None:
     if name not in _PREC:
         raise ValidationError(f"unknown precision {name!r}")
     _state["prec"] = _PREC[name]
+
+
+def _storage() -> int:
+    """Storage precision of the module precision (tf32 keeps float32 tensors)."""
+    return L.PC_FP32 if _state["prec"] == L.PC_TF32 else _state["prec"]
 
 
 def tensor(values) -> np.ndarray:
@@ -105,7 +111,7 @@ def _conv_setup(x, p: ConvParams, prec):
     b, c, h, w = x.shape
     n, _, k, _ = p.weights.shape
     ho, wo = conv_output_size(h, k, p.stride, p.pad), conv_output_size(w, k, p.stride, p.pad)
-    cp = c if prec == L.PC_FP32 or c % 8 == 0 else (c + 7) // 8 * 8
+    cp = c if prec != L.PC_BF16 or c % 8 == 0 else (c + 7) // 8 * 8
     xn = np.zeros((b, h, w, cp))
     xn[..., :c] = _nhwc(x)
     wd = np.zeros((n, k, k, cp))
@@ -185,7 +191,7 @@ def fc_backward(x: np.ndarray, weights: np.ndarray, grad_out: np.ndarray):
 
 
 def relu_forward(x: np.ndarray) -> np.ndarray:
-    prec = _state["prec"]
+    prec = _storage()
     xd = _up(x, prec)
     y = torch.empty_like(xd)
     L.lib().call("pc_relu_forward", xd.numel(), xd.data_ptr(), y.data_ptr(), prec, _stream())
@@ -194,7 +200,7 @@ def relu_forward(x: np.ndarray) -> np.ndarray:
 
 def relu_backward(x: np.ndarray, grad_out: np.ndarray) -> np.ndarray:
     _require(x.shape == grad_out.shape, "relu grad_out shape mismatch")
-    prec = _state["prec"]
+    prec = _storage()
     xd, gd = _up(x, prec), _up(grad_out, prec)
     gx = torch.empty_like(xd)
     L.lib().call("pc_relu_backward", xd.numel(), xd.data_ptr(), gd.data_ptr(), gx.data_ptr(), prec,
@@ -204,7 +210,7 @@ def relu_backward(x: np.ndarray, grad_out: np.ndarray) -> np.ndarray:
 
 def maxpool_forward(x: np.ndarray, k: int, stride: int):
     _require(x.ndim == 4, f"maxpool input must be 4-d, got {x.shape}")
-    prec = _state["prec"]
+    prec = _storage()
     b, c, h, w = x.shape
     ho, wo = conv_output_size(h, k, stride, 0), conv_output_size(w, k, stride, 0)
     xd = _up(_nhwc(x), prec)
@@ -221,7 +227,7 @@ def maxpool_forward(x: np.ndarray, k: int, stride: int):
 def maxpool_backward(x: np.ndarray, k: int, stride: int, grad_out: np.ndarray, argmax=None) -> np.ndarray:
     if argmax is None:
         _, argmax = maxpool_forward(x, k, stride)
-    prec = _state["prec"]
+    prec = _storage()
     b, c, h, w = x.shape
     ho, wo = conv_output_size(h, k, stride, 0), conv_output_size(w, k, stride, 0)
     _require(grad_out.shape == (b, c, ho, wo), "maxpool grad_out shape mismatch")
@@ -240,7 +246,7 @@ def softmax_xent_scaled(logits: np.ndarray, labels, scale: float):
     k = logits.shape[1]
     if labels.size and (labels.min() < 0 or labels.max() >= k):
         raise ValidationError(f"labels must lie in [0, {k})")
-    prec = _state["prec"]
+    prec = _storage()
     b = logits.shape[0]
     zd = _up(logits, prec)
     yd = torch.as_tensor(labels.astype(np.int32)).to(_dev())

@@ -87,7 +87,7 @@ class _Runner:
             for wid in fabric.local_wids:
                 replica, column = divmod(wid, m)
                 old = fabric._engines.get(wid)
-                eng = ColumnEngine(cs, wid, replica, column, shard, fabric.prec, dev, fabric._hyper)
+                eng = ColumnEngine(cs, wid, replica, column, shard, fabric.prec, dev, fabric._hyper, fabric.cprec)
                 eng.dropout_seed = int(getattr(fabric, "dropout_seed", 0))
                 if old is not None:
                     eng.p32.copy_(old.p32)
@@ -501,7 +501,7 @@ def _eval_engines(fabric: Fabric, cs: ColumnizedSpec, b: int, wids: list) -> lis
             cache.pop(next(iter(cache)))
         engines = []
         for j in wids:
-            eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, fabric.torch_device, fabric._hyper)
+            eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, fabric.torch_device, fabric._hyper, fabric.cprec)
             eng.training = False     # dropout is the identity at evaluation
             engines.append(eng)
         cache[key] = engines
