@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scheme", default="auto", choices=["auto", "dp", "mp", "hybrid"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "fp32"])
     ap.add_argument("--batch", type=int, default=256, help="images per replica group")
     ap.add_argument("--net", default=str(ROOT / "configs" / "alexnet.net"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -306,7 +306,9 @@ def main():
     # Gaussian std 0.01 (the paper's cited Krizhevsky init, reference SPEC.md:120): the He-normal
     # default diverges to inf within 4 steps on AlexNet at lr 0.01 in the reference as well
     P.setup_workers(fab, plan, cs, P.init_dense_params(net, 0, std=0.01), P.SgdState())
-    res = P.hybrid_step(fab, plan, cs, x_bf16, y_host)     # builds engines; device-resident batch in bf16
+    # builds the engines; the device-resident batch is bf16 in the bf16 mode (the rounding
+    # the input layer applies anyway), float32 otherwise
+    res = P.hybrid_step(fab, plan, cs, x_bf16 if args.precision == "bf16" else x_f32, y_host)
     run = S._runner(fab, plan, cs, gbatch // plan.data_shards)
     stream = torch.cuda.current_stream()
     scale = 1.0 / gbatch
@@ -382,6 +384,8 @@ def main():
         return
 
     tc_peak, tc_src = choose_tc_peak(clk)
+    if args.precision == "tf32":   # kind::tf32 runs at half the bf16 rate (B200_PROFILING.md: 1.1 PF dense)
+        tc_peak, tc_src = tc_peak / 2, "half of " + tc_src + " (tf32 tensor-core rate)"
     _, _, hbm, hbm_src = measured_peaks()
     shard = gbatch // plan.data_shards
     kernels = []
@@ -436,7 +440,8 @@ def main():
                    "per_gpu_batch": shard, "plan": plan.describe(),
                    "cross_layers": list(plan.cross_layers), "parallelism": label,
                    "l2": "activations >> 126 MB L2 (no flush needed)",
-                   "resident_input": "bf16 NCHW (value); e2e from the host format named in e2e.input_dtype"},
+                   "resident_input": ("bf16" if args.precision == "bf16" else "float32") +
+                          " NCHW (value); e2e from the host format named in e2e.input_dtype"},
         "tflops_achieved_step": step_flops / (ms * 1e-3) / 1e12,
         "roofline_step": {"achieved": step_flops / (ms * 1e-3) / 1e12, "peak": tc_peak,
                           "frac": step_flops / (ms * 1e-3) / 1e12 / tc_peak},

@@ -194,7 +194,7 @@ class _Runner:
         # bf16 when every engine's input layer is the explicit-im2col GEMM, which rounds
         # to bf16 first anyway (identical results, half the host->device bytes)
         keep_bf16 = isinstance(batch_x, torch.Tensor) and batch_x.dtype == torch.bfloat16 and \
-            all(e.col_kp or e.s2d for e in self.engines.values())
+            all((e.col_kp or e.s2d) and e.prec == L.PC_BF16 for e in self.engines.values())
         xdt = torch.bfloat16 if keep_bf16 else torch.float32
         if isinstance(batch_x, torch.Tensor) and batch_x.is_cuda and batch_x.dtype == xdt:
             xs = batch_x.contiguous()
