@@ -218,6 +218,14 @@ PC_API int pc_dropout(int B, int H, int W, int C, int C_dense, int c_off, long l
 /* *counter += delta (device; advances the dropout step inside a CUDA graph). */
 PC_API int pc_counter_add(unsigned long long* counter, long long delta, pc_stream_t stream);
 
+/* --- single-process multi-GPU fabric (spawn(n) over the visible GPUs) --------
+ * Replaces the reference's in-process message fabric (`fabric.py:102-339`):
+ * the column exchange and the replica reduction read peer memory directly. */
+/* Let the calling thread's current device read `peer`'s memory (idempotent). */
+PC_API int pc_enable_peer_access(int peer);
+/* Asynchronous copy between any two device (or pinned host) buffers on `stream`. */
+PC_API int pc_copy_async(void* dst, const void* src, size_t bytes, pc_stream_t stream);
+
 /* --- trainer feed on the device ------------------------------ */
 /* Rows idx[0..n) (DEVICE int64 sample indices) of the synthetic split
  * gen_synthetic(classes, per_class, shape, seed) with prod(shape) = dim, written

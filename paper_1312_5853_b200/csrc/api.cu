@@ -400,6 +400,33 @@ extern "C" PC_API int pc_set_grid_cap(int ctas) {
   return PC_OK;
 }
 extern "C" unsigned long long pc_launch_count(void) { return g_launches.load(); }
+
+// Single-process multi-GPU fabric: the calling thread's current device may read
+// `peer`'s memory directly (pc_sum_buffers over peer pointers, peer copies over NVLink).
+extern "C" PC_API int pc_enable_peer_access(int peer) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "enable_peer_access: %s", cudaGetErrorString(e));
+  if (peer == dev) return PC_OK;
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, dev, peer);
+  PC_REQUIRE(can, PC_ECUDA, "device %d cannot access device %d's memory (no P2P path)", dev, peer);
+  e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return PC_OK;
+  }
+  PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "cudaDeviceEnablePeerAccess(%d): %s", peer, cudaGetErrorString(e));
+  return PC_OK;
+}
+
+// dst <- src (bytes), either device (unified addressing; a peer copy between GPUs), on `stream`.
+extern "C" PC_API int pc_copy_async(void* dst, const void* src, size_t bytes, pc_stream_t st) {
+  if (bytes == 0) return PC_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, S(st));
+  PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "copy_async: %s", cudaGetErrorString(e));
+  return PC_OK;
+}
 extern "C" int pc_has_tcgen05(void) { return umma_available() ? 1 : 0; }
 
 extern "C" int pc_conv2d_forward(const pc_conv_geom* g, const void* x, const void* w, const float* bias,

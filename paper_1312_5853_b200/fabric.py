@@ -6,11 +6,14 @@ initialised, world size == plan workers): worker w = rank w, its column group
 and replica group are NCCL sub-communicators, the cross-layer exchange is
 ``all_gather_into_tensor`` / ``reduce_scatter_tensor`` in the column group
 and the data-parallel leg is one ``all_reduce`` over the flat gradient in
-the replica group. Without a process group (one GPU, or the parity tests),
-every worker of the plan lives on the one device and the same exchange is
-done with device copies and the deterministic ``pc_sum_buffers`` kernel in
-ascending worker order — the reference's summation order exactly
-(`fabric.py:146-156`, `schemes.py:307-318`).
+the replica group. Without a process group, one process drives every worker
+of the plan like the reference's ``Fabric.run`` threads: on several visible
+GPUs (or with ``devices=``) one host thread per worker on its own GPU and
+stream, exchanging through peer memory (``multidev.py``); on one GPU every
+worker shares the device and the same exchange is done with device copies and
+the deterministic ``pc_sum_buffers`` kernel in ascending worker order — the
+reference's summation order exactly (`fabric.py:146-156`, `schemes.py:307-318`);
+both single-process forms give bit-identical results.
 
 Bookkeeping kept from the reference so its callers keep working:
 ``ledger`` books every logical message the reference protocol would send
@@ -143,7 +146,7 @@ class Fabric:
     """n workers of a plan mapped onto B200s (see module docstring)."""
 
     def __init__(self, n: int, device: DeviceSpec | None = None, scheduling: str = "lockstep",
-                 idle_timeout: float = 5.0, precision: str = "bf16"):
+                 idle_timeout: float = 5.0, precision: str = "bf16", devices: list | None = None):
         if n < 1:
             raise ValidationError(f"fabric needs at least one worker, got {n}")
         if scheduling not in ("lockstep", "threads"):
@@ -182,6 +185,31 @@ class Fabric:
             torch.cuda.set_device(idx)
         self.torch_device = torch.device("cuda", idx)
         self._groups = {}
+        # single process, several workers: one host thread + stream per worker on its GPU
+        # (multidev.PeerRunner), the workers spread over the visible GPUs in contiguous
+        # blocks (the columns of a replica share a GPU when there are fewer GPUs than
+        # workers). devices=[...] pins worker w to GPU devices[w] (repeats allowed: the
+        # same machinery on one GPU, which is how a one-GPU box tests it).
+        self.multi = False
+        self._device_of = [self.torch_device] * n
+        if not self.dist and n > 1:
+            if devices is not None:
+                if len(devices) != n:
+                    raise ValidationError(f"devices: need one GPU index per worker ({n}), got {len(devices)}")
+                count = torch.cuda.device_count()
+                if any(not 0 <= int(g) < count for g in devices):
+                    raise ValidationError(f"devices {list(devices)}: only {count} GPU(s) visible")
+                self._device_of = [torch.device("cuda", int(g)) for g in devices]
+                self.multi = True
+            elif torch.cuda.device_count() > 1:
+                c = min(n, torch.cuda.device_count())
+                self._device_of = [torch.device("cuda", w * c // n) for w in range(n)]
+                self.multi = True
+        elif devices is not None and list(devices) not in ([idx], [idx] * n):
+            raise ValidationError("devices= applies to single-process fabrics")
+
+    def device_of(self, wid: int) -> torch.device:
+        return self._device_of[wid]
 
     @property
     def num_links(self) -> int:
@@ -239,9 +267,11 @@ def make_groups(d: int, m: int, rank: int):
 
 
 def spawn(n: int, device: DeviceSpec | None = None, scheduling: str = "lockstep",
-          idle_timeout: float = 5.0, precision: str = "bf16") -> Fabric:
+          idle_timeout: float = 5.0, precision: str = "bf16", devices: list | None = None) -> Fabric:
+    """`fabric.py:342-345`. Under torchrun: worker = rank. In one process: every
+    worker of the plan, spread over the visible GPUs (``devices`` to pin them)."""
     return Fabric(n, device=device, scheduling=scheduling, idle_timeout=idle_timeout,
-                  precision=precision)
+                  precision=precision, devices=devices)
 
 
 # ----------------------------------------------------------------------------

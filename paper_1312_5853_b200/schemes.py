@@ -403,10 +403,16 @@ class _Runner:
         return float(host[0])
 
 
-def _runner(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, shard: int) -> _Runner:
+def _runner(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, shard: int):
     r = getattr(fabric, "_runner", None)
     if r is None or r.shard != shard or r.cs is not cs:
-        r = _Runner(fabric, plan, cs, shard)
+        if r is not None and hasattr(r, "close"):
+            r.close()
+        if fabric.multi:
+            from .multidev import PeerRunner
+            r = PeerRunner(fabric, plan, cs, shard)
+        else:
+            r = _Runner(fabric, plan, cs, shard)
         fabric._runner = r
     return r
 
@@ -446,10 +452,15 @@ def hybrid_step(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, batch_x,
     if meter:
         _meter_step(fabric, cs, shard)
     run = _runner(fabric, plan, cs, shard)
-    with torch.cuda.device(fabric.torch_device):
+    if fabric.multi:      # one host thread per worker, each on its own GPU / stream
         run.upload(batch_x, labels)
-        run.program(1.0 / b)
+        run.step(1.0 / b)
         loss = run.loss()
+    else:
+        with torch.cuda.device(fabric.torch_device):
+            run.upload(batch_x, labels)
+            run.program(1.0 / b)
+            loss = run.loss()
     book_step(fabric, plan, cs, shard)
     return StepResult(loss=loss, ledger_bytes=fabric.ledger.total_bytes - before_b,
                       ledger_messages=fabric.ledger.total_messages - before_m)
@@ -501,7 +512,7 @@ def _eval_engines(fabric: Fabric, cs: ColumnizedSpec, b: int, wids: list) -> lis
             cache.pop(next(iter(cache)))
         engines = []
         for j in wids:
-            eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, fabric.torch_device, fabric._hyper, fabric.cprec)
+            eng = ColumnEngine(cs, j, 0, j, b, fabric.prec, fabric.device_of(j), fabric._hyper, fabric.cprec)
             eng.training = False     # dropout is the identity at evaluation
             engines.append(eng)
         cache[key] = engines
@@ -554,6 +565,10 @@ def evaluation_errors(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, x,
     else:
         ex = LocalExchange(dev) if m > 1 else None
     count = -1
+    if fabric.multi:
+        from .multidev import evaluate
+        engines = _eval_engines(fabric, cs, b, wids)
+        return evaluate(fabric, plan, cs, x, labels, {e.wid: e for e in engines})
     if wids:
         with torch.cuda.device(dev):
             engines = _eval_engines(fabric, cs, b, wids)

@@ -353,9 +353,9 @@ def test_train_device_resident_feed_single_replica_pipelined_upload(precision):
             for step in range(train_set.size // 16):
                 idx = order[step * 16:(step + 1) * 16]
                 want.append(of.step(train_set.images[idx], train_set.labels[idx]))
-        # the first two steps at the fp32 bound; later steps inherit the ReLU / pool
-        # decisions at near-zero pre-activations that fp32 and fp64 take differently
-        # (replayed per step in tests/parity.py, not over a free-running trajectory),
-        # and small64's He-init trajectory amplifies them: 1e-2 as a sanity bound
-        for n, (got, ref) in enumerate(zip(runs[0], want)):
-            assert abs(got - ref) / abs(ref) < (1e-5 if n < 2 else 1e-2), n
+        # the first two steps at the fp32 bound. The free-running trajectory is chaotic
+        # (small64, He init, lr 0.01: the loss climbs 9.8 -> 20 -> 60): the oracle itself,
+        # restarted from parameters perturbed by 1e-7, is 4e-2 off by step 12, so later
+        # steps are compared between the two device feeds only (bit-identical above)
+        for n, (got, ref) in enumerate(zip(runs[0][:2], want[:2])):
+            assert abs(got - ref) / abs(ref) < 1e-5, n
