@@ -258,7 +258,7 @@ class PeerRunner:
         total, bad = 0.0, 0
         for e in self.engines.values():
             self.streams[e.wid].synchronize()
-        for e in self.engines.values():
+        for e in sorted(self.engines.values(), key=lambda e: e.replica):   # ascending, schemes.py:562-564
             if e.column == 0:
                 total += float(e.loss.item())
             bad += int(e.bad_label.item())

@@ -370,37 +370,43 @@ class _Runner:
             torch.cuda.current_stream().wait_stream(self.side)
 
     def loss(self) -> float:
-        """Sum over replicas of column 0's loss (host read-back; raises on bad labels).
+        """Sum over replicas of column 0's loss, accumulated on the host in ascending
+        replica order like the reference (`schemes.py:562-564`); raises on bad labels.
         With a split step the read waits only for the forward (fwd_done), on its own
         stream: the backward keeps running while the caller gets the loss."""
+        parts = [e.loss.reshape(()) for e in sorted(self.engines.values(), key=lambda e: e.replica)
+                 if e.column == 0]
+        bad = torch.stack([e.bad_label.reshape(()) for e in self.engines.values()]).sum().double()
         if getattr(self, "fwd_done", None) is not None and not self.fabric.dist:
             ls = self.loss_stream
             ls.wait_event(self.fwd_done)
             with torch.cuda.stream(ls):
-                parts = [e.loss for e in self.engines.values() if e.column == 0]
-                bad = [e.bad_label for e in self.engines.values()]
-                vals = torch.stack([torch.stack(parts).sum().reshape(()).double(),
-                                    torch.stack(bad).sum().reshape(()).double()])
+                vals = torch.stack(parts + [bad])
+                if self.loss_host.numel() != vals.numel():
+                    self.loss_host = torch.zeros(vals.numel(), dtype=torch.float64).pin_memory()
                 self.loss_host.copy_(vals, non_blocking=True)
             ls.synchronize()
             return self._check_loss(self.loss_host.numpy())
-        m = self.plan.model_columns
-        parts = [e.loss for e in self.engines.values() if e.column == 0]
-        bad = [e.bad_label for e in self.engines.values()]
-        total = torch.stack(parts).sum() if parts else torch.zeros(1, dtype=torch.float64,
-                                                                    device=self.fabric.torch_device)
-        flag = torch.stack(bad).sum()
         if self.fabric.dist:
-            buf = torch.cat([total.reshape(1), flag.reshape(1).double()])
+            m = self.plan.model_columns
+            mine = parts[0] if parts else torch.zeros((), dtype=torch.float64, device=self.fabric.torch_device)
+            # every rank contributes its slot: rank r of column 0 fills entry r // m
+            buf = torch.zeros(self.plan.data_shards + 1, dtype=torch.float64, device=self.fabric.torch_device)
+            if parts:
+                buf[self.fabric.rank // m] = mine
+            buf[-1] = bad
             torch.distributed.all_reduce(buf)
-            total, flag = buf[0], buf[1]
-        host = torch.stack([total.reshape(()).double(), flag.reshape(()).double()]).cpu().numpy()
-        return self._check_loss(host)
+            return self._check_loss(buf.cpu().numpy())
+        return self._check_loss(torch.stack(parts + [bad]).cpu().numpy())
 
     def _check_loss(self, host) -> float:
-        if host[1] != 0:
+        """host = [replica losses (ascending replica), label-error count]."""
+        if host[-1] != 0:
             raise ValidationError(f"labels must lie in [0, {self.cs.base.classes})")
-        return float(host[0])
+        total = 0.0
+        for v in host[:-1]:
+            total += float(v)
+        return total
 
 
 def _runner(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, shard: int):
