@@ -376,12 +376,15 @@ class _Runner:
         stream: the backward keeps running while the caller gets the loss."""
         parts = [e.loss.reshape(()) for e in sorted(self.engines.values(), key=lambda e: e.replica)
                  if e.column == 0]
-        bad = torch.stack([e.bad_label.reshape(()) for e in self.engines.values()]).sum().double()
+
+        def flag():
+            return torch.stack([e.bad_label.reshape(()) for e in self.engines.values()]).sum().double()
+
         if getattr(self, "fwd_done", None) is not None and not self.fabric.dist:
             ls = self.loss_stream
             ls.wait_event(self.fwd_done)
-            with torch.cuda.stream(ls):
-                vals = torch.stack(parts + [bad])
+            with torch.cuda.stream(ls):     # everything here runs after the forward only
+                vals = torch.stack(parts + [flag()])
                 if self.loss_host.numel() != vals.numel():
                     self.loss_host = torch.zeros(vals.numel(), dtype=torch.float64).pin_memory()
                 self.loss_host.copy_(vals, non_blocking=True)
@@ -394,10 +397,10 @@ class _Runner:
             buf = torch.zeros(self.plan.data_shards + 1, dtype=torch.float64, device=self.fabric.torch_device)
             if parts:
                 buf[self.fabric.rank // m] = mine
-            buf[-1] = bad
+            buf[-1] = flag()
             torch.distributed.all_reduce(buf)
             return self._check_loss(buf.cpu().numpy())
-        return self._check_loss(torch.stack(parts + [bad]).cpu().numpy())
+        return self._check_loss(torch.stack(parts + [flag()]).cpu().numpy())
 
     def _check_loss(self, host) -> float:
         """host = [replica losses (ascending replica), label-error count]."""
