@@ -9,7 +9,8 @@ scheme, with the dominant contraction's fraction of the tensor-core roofline.
 N=1: plan d1m1, global batch 256. N>1 (torchrun, one rank per GPU):
 auto = model parallel d1m2 cross(conv3) at N=2, hybrid d(N/2) x m2 at N=4/8
 with 256 images per replica group (the paper's hybrid; weak scaling).
-``--scheme dp``: data parallel dN x m1, 256 images per GPU.
+``--scheme dp``: data parallel dN x m1, global batch 256 sharded 256/N per GPU
+(BASELINE configs[2]; strong scaling).
 
 ``value`` is measured with the batch already resident in HBM (device step
 program only); ``e2e`` goes through the public ``hybrid_step`` API with a
@@ -60,11 +61,17 @@ def parse():
 
 
 def choose_plan(n: int, scheme: str, per_group: int):
+    """(plan, global batch, label) of BASELINE configs[1..4]: dp = global 256 sharded
+    over the GPUs (configs[2], the paper's data-parallel scaling: strong scaling);
+    mp = the two-column net on 2 GPUs (configs[3]); hybrid = 2 columns x N/2 replicas,
+    256 per replica group (configs[4]: weak scaling)."""
     from paper_1312_5853_b200.plan import ParallelPlan
     if n == 1:
         return ParallelPlan(1, 1), per_group, "d1m1"
     if scheme == "dp":
-        return ParallelPlan(n, 1), per_group * n, f"dp{n}"
+        if per_group % n:
+            raise SystemExit(f"global batch {per_group} does not shard over {n} GPUs")
+        return ParallelPlan(n, 1), per_group, f"dp{n}"
     if scheme == "mp" or (scheme == "auto" and n == 2):
         if n != 2:
             raise SystemExit("model parallel runs on 2 GPUs (two columns)")
@@ -433,7 +440,8 @@ def main():
     h2d = int(x_e2e.numel() * x_e2e.element_size() + y_host.numel() * 4)
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if plan.model_columns == 1 and plan.data_shards > 1 else "weak",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic (gen_synthetic blobs, 1000 classes, "
         "3x227x227; Gaussian std 0.01 init, seed 0)",
         "config": {"workload": f"AlexNet-227 {label} train step", "global_batch": gbatch,

@@ -248,8 +248,8 @@ class _Runner:
         is a real update, and it warms every kernel's launch attributes); the
         second captures the same launch sequence into a CUDA graph, and every
         call from then on replays it, so the ~60 launches of a step cost one
-        host call. Under torchrun the NCCL collectives stay eager unless
-        ``PC_GRAPH_DIST=1``."""
+        host call. Under torchrun the NCCL collectives are captured too
+        (``PC_GRAPH_DIST=0``: eager); a failed capture falls back to eager launches."""
         self.fwd_done = None
         if self.copy_stream is not None:   # this step's batch upload (pipelined, see upload())
             torch.cuda.current_stream().wait_stream(self.copy_stream)
@@ -274,11 +274,25 @@ class _Runner:
             # loss can be read back while the backward runs
             parts = ("fwd", "bwd") if self._split_ok() else ("all",)
             g = []
-            for part in parts:
-                gp = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(gp, capture_error_mode="thread_local"):
-                    self._launch(loss_scale, part)
-                g.append(gp)
+            try:
+                for part in parts:
+                    gp = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gp, capture_error_mode="thread_local"):
+                        self._launch(loss_scale, part)
+                    g.append(gp)
+            except RuntimeError as err:
+                # a capture records and executes nothing: this step (and every later one)
+                # runs eagerly; under torchrun the collectives stay in the same order
+                # whether a rank replays a graph or launches eagerly
+                import warnings
+                warnings.warn(f"CUDA-graph capture of the step failed ({err}); running eagerly")
+                self._graph_broken = True
+                torch.cuda.synchronize(self.fabric.torch_device)
+                if self.fabric.dist and hasattr(self.reducer, "works"):
+                    self.reducer.works = []
+                self._launch(loss_scale, "fwd")
+                self._mark_fwd_done()
+                return self._launch(loss_scale, "bwd")
             self.graph_launches = int(L.lib().dll.pc_launch_count() - l0)
             self._graphs[key] = g
         g[0].replay()
@@ -294,9 +308,11 @@ class _Runner:
             self.fwd_done.record()
 
     def _graph_enabled(self) -> bool:
-        if os.environ.get("PC_GRAPH", "1") == "0":
+        """CUDA-graph replay: single process always; under torchrun too (the NCCL
+        collectives are captured with the kernels; PC_GRAPH_DIST=0 keeps them eager)."""
+        if os.environ.get("PC_GRAPH", "1") == "0" or getattr(self, "_graph_broken", False):
             return False
-        return not self.fabric.dist or os.environ.get("PC_GRAPH_DIST", "0") == "1"
+        return not self.fabric.dist or os.environ.get("PC_GRAPH_DIST", "1") == "1"
 
     def _split_ok(self) -> bool:
         """One local replica: the forward (and so the loss) is complete before any
