@@ -71,4 +71,17 @@ struct Blocked {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Division by a runtime-invariant divisor d (Granlund-Montgomery round-up method):
+// q = (umulhi(n, m) + n) >> l for n < 2^31 — three instructions instead of the
+// ~20-instruction reciprocal sequence of a runtime integer division.
+struct FastDiv {
+  uint32_t d, m, l;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div), m(0), l(0) {
+    while ((1ull << l) < div) ++l;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> l; }
+};
+
 }  // namespace pc

@@ -84,62 +84,72 @@ __global__ void relu_bwd_k(long long n, const T* __restrict__ x, const T* __rest
 // windows whose 9 x 8 values are all non-negative and not NaN (the network's
 // ReLU outputs): raw bf16 bit patterns are then order-preserving, so one 32-bit
 // integer max over (bits << 16 | 15 - index) gives the maximum and, among equal
-// values, the first window position — np.argmax's rule, bit-exact. Any negative value or NaN in the window falls back to the exact
-// float comparison (first NaN wins, -0 == +0).
-__global__ void maxpool_fwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int Wo,
-                                        const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                                        uint8_t* __restrict__ arg) {
+// values, the first window position — np.argmax's rule, bit-exact. Any negative
+// value or NaN in the window falls back to the exact float comparison (first NaN
+// wins, -0 == +0). The kernel was integer-ALU bound (ncu: ALU pipe 80%, 372
+// instructions per thread); the key build is one PRMT and the max tree DPX
+// three-input maxes.
+// Index math in 32 bits with precomputed divisors (the host guarantees every
+// offset < 2^31): the runtime divisions were a third of the instructions.
+__global__ void maxpool_fwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int Wo, FastDiv fcg, FastDiv fwo,
+                                        FastDiv fho, const __nv_bfloat16* __restrict__ x,
+                                        __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ arg) {
   PC_PDL_TRIGGER();
   const unsigned cg = (unsigned)(C >> 3);
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (unsigned)B * Ho * Wo * cg) return;
-  const unsigned pix = t / cg;
-  const int c0 = (int)(t - pix * cg) * 8;
-  const unsigned row = pix / (unsigned)Wo;
-  const int ox = (int)(pix - row * Wo);
-  const int b = (int)(row / (unsigned)Ho);
-  const int oy = (int)(row - (unsigned)b * Ho);
-  // keys: (bf16 bits << 16) | (15 - window index): one 32-bit max per channel and
-  // element gives the largest value and, among equal values, the first index.
-  // The 9 loads are consumed as they arrive (no window kept in registers: the
-  // rare fallback reloads it), so the kernel runs at high occupancy.
-  uint32_t sign = 0, mk[8];
+  const unsigned pix = fcg.div(t);
+  const unsigned c0 = (t - pix * cg) * 8;
+  const unsigned row = fwo.div(pix);
+  const unsigned ox = pix - row * (unsigned)Wo;
+  const unsigned b = fho.div(row);
+  const unsigned oy = row - b * (unsigned)Ho;
+  // keys: (bf16 bits << 16) | (15 - window index), built with one PRMT per channel
+  // and element; the 9-way max per channel is 4 three-input DPX maxes (VIMNMX3):
+  // the largest value and, among equal values, the first index. The window's 36
+  // words stay in registers (the rare fallback reuses them).
+  const __nv_bfloat16* x0 = x + (((b * (unsigned)H + oy * 2) * (unsigned)W + ox * 2) * (unsigned)C + c0);
+  const unsigned WC = (unsigned)W * C;
+  uint4 r[9];
 #pragma unroll
-  for (int v = 0; v < 8; ++v) mk[v] = 0u;
-  const __nv_bfloat16* x0 = x + (((long long)b * H + oy * 2) * W + ox * 2) * C + c0;
+  for (int e = 0; e < 9; ++e) r[e] = __ldg(reinterpret_cast<const uint4*>(x0 + ((e / 3) * WC + (e % 3) * (unsigned)C)));
+  uint32_t mk[8];
+  uint32_t sign = 0;
 #pragma unroll
-  for (int e = 0; e < 9; ++e) {
-    const uint4 r = __ldg(reinterpret_cast<const uint4*>(x0 + ((long long)(e / 3) * W + (e % 3)) * C));
-    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  for (int q = 0; q < 4; ++q) {
+    uint32_t lo[9], hi[9];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      sign |= w[q];
-      mk[2 * q] = max(mk[2 * q], (w[q] << 16) | (uint32_t)(15 - e));
-      mk[2 * q + 1] = max(mk[2 * q + 1], (w[q] & 0xFFFF0000u) | (uint32_t)(15 - e));
+    for (int e = 0; e < 9; ++e) {
+      const uint32_t w = q == 0 ? r[e].x : q == 1 ? r[e].y : q == 2 ? r[e].z : r[e].w;
+      sign |= w;
+      lo[e] = __byte_perm(w, 15u - e, 0x1054);  // (low channel bits << 16) | (15 - e)
+      hi[e] = __byte_perm(w, 15u - e, 0x3254);  // (high channel bits << 16) | (15 - e)
     }
+    mk[2 * q] = __vimax3_u32(__vimax3_u32(lo[0], lo[1], lo[2]), __vimax3_u32(lo[3], lo[4], lo[5]),
+                             __vimax3_u32(lo[6], lo[7], lo[8]));
+    mk[2 * q + 1] = __vimax3_u32(__vimax3_u32(hi[0], hi[1], hi[2]), __vimax3_u32(hi[3], hi[4], hi[5]),
+                                 __vimax3_u32(hi[6], hi[7], hi[8]));
   }
   bool nan = false;
 #pragma unroll
   for (int v = 0; v < 8; ++v) nan |= (mk[v] >> 16) > 0x7F80u;
-  const long long o = (long long)pix * C + c0;
+  const unsigned o = pix * (unsigned)C + c0;
   if ((sign & 0x80008000u) == 0u && !nan) {
     uint4 outv;
-    outv.x = (mk[0] >> 16) | (mk[1] & 0xFFFF0000u);
-    outv.y = (mk[2] >> 16) | (mk[3] & 0xFFFF0000u);
-    outv.z = (mk[4] >> 16) | (mk[5] & 0xFFFF0000u);
-    outv.w = (mk[6] >> 16) | (mk[7] & 0xFFFF0000u);
+    outv.x = __byte_perm(mk[0], mk[1], 0x7632);
+    outv.y = __byte_perm(mk[2], mk[3], 0x7632);
+    outv.z = __byte_perm(mk[4], mk[5], 0x7632);
+    outv.w = __byte_perm(mk[6], mk[7], 0x7632);
     *reinterpret_cast<uint4*>(y + o) = outv;
+    // index byte of channel v = 15 - (key & 15): bytes 0 of the keys, packed, then 0x0F - b
+    const uint32_t i0 = __byte_perm(__byte_perm(mk[0], mk[1], 0x0040), __byte_perm(mk[2], mk[3], 0x0040), 0x5410);
+    const uint32_t i1 = __byte_perm(__byte_perm(mk[4], mk[5], 0x0040), __byte_perm(mk[6], mk[7], 0x0040), 0x5410);
     uint2 packed;
-    packed.x = (15u - (mk[0] & 15u)) | ((15u - (mk[1] & 15u)) << 8) | ((15u - (mk[2] & 15u)) << 16) |
-               ((15u - (mk[3] & 15u)) << 24);
-    packed.y = (15u - (mk[4] & 15u)) | ((15u - (mk[5] & 15u)) << 8) | ((15u - (mk[6] & 15u)) << 16) |
-               ((15u - (mk[7] & 15u)) << 24);
+    packed.x = 0x0F0F0F0Fu - (i0 & 0x0F0F0F0Fu);
+    packed.y = 0x0F0F0F0Fu - (i1 & 0x0F0F0F0Fu);
     *reinterpret_cast<uint2*>(arg + o) = packed;
     return;
   }
-  uint4 r[9];
-#pragma unroll 1
-  for (int e = 0; e < 9; ++e) r[e] = __ldg(reinterpret_cast<const uint4*>(x0 + ((long long)(e / 3) * W + (e % 3)) * C));
   float best[8];
   int bi[8];
   unsigned short bits[8];  // the winner's original bits (NaN payload kept)
@@ -273,6 +283,19 @@ __global__ void maxpool_bwd_k(int B, int H, int W, int C, int k, int s, int Ho, 
   if constexpr (V == 8) Vec8<T>::store(gx + o, acc); else gx[o] = cvt<T>(acc[0]);
 }
 
+// acc[0..7] += the 8 bf16 values packed in s0..s3 (low half first), two lanes per
+// packed fp32x2 add (FADD2): the same per-element IEEE adds in the same order.
+__device__ __forceinline__ void bf16x8_accumulate(float* acc, uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3) {
+  const uint32_t w[4] = {s0, s1, s2, s3};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 a = make_float2(acc[2 * i], acc[2 * i + 1]);
+    a = __fadd2_rn(a, make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u)));
+    acc[2 * i] = a.x;
+    acc[2 * i + 1] = a.y;
+  }
+}
+
 // bf16 k=3, s=2 backward with byte-SIMD routing: for each covering window and
 // each of its (at most 4) window positions inside this 2x2 block, one __vcmpeq4
 // per 4 channels selects the channels whose argmax is that position, the byte
@@ -281,6 +304,7 @@ __global__ void maxpool_bwd_k(int B, int H, int W, int C, int k, int s, int Ho, 
 // compare/select/add per (pixel, window, channel). Same fixed order (ascending
 // (oy, ox) per pixel) and fp32 accumulation as maxpool_bwd_k3s2_k.
 __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int W, int C, int Ho, int Wo,
+                                                               FastDiv fcg, FastDiv fw2, FastDiv fh2,
                                                                const __nv_bfloat16* __restrict__ gy,
                                                                const uint8_t* __restrict__ arg,
                                                                const __nv_bfloat16* __restrict__ mask,
@@ -290,11 +314,11 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
   const unsigned cg = (unsigned)(C >> 3);
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (unsigned)B * H2 * W2 * cg) return;
-  const unsigned blk = t / cg;
+  const unsigned blk = fcg.div(t);
   const int c0 = (int)(t - blk * cg) * 8;
-  const unsigned r = blk / (unsigned)W2;
+  const unsigned r = fw2.div(blk);
   const int X = (int)(blk - r * W2);
-  const int b = (int)(r / (unsigned)H2);
+  const int b = (int)fh2.div(r);
   const int Y = (int)(r - (unsigned)b * H2);
   float acc[4][8];
 #pragma unroll
@@ -309,7 +333,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
     for (int dx = -1; dx <= 0; ++dx) {
       const int ox = X + dx;
       if (ox < 0 || ox >= Wo) continue;
-      const long long o = (((long long)b * Ho + oy) * Wo + ox) * C + c0;
+      const unsigned o = (((unsigned)b * Ho + oy) * Wo + ox) * (unsigned)C + c0;
       const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + o));
       const uint4 g = __ldg(reinterpret_cast<const uint4*>(gy + o));
 #pragma unroll
@@ -324,15 +348,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
           const unsigned m0 = __vcmpeq4(a.x, want), m1 = __vcmpeq4(a.y, want);
           const unsigned s0 = g.x & __byte_perm(m0, 0, 0x1100), s1 = g.y & __byte_perm(m0, 0, 0x3322);
           const unsigned s2 = g.z & __byte_perm(m1, 0, 0x1100), s3 = g.w & __byte_perm(m1, 0, 0x3322);
-          float* ac = acc[qy * 2 + qx];
-          ac[0] += __uint_as_float(s0 << 16);
-          ac[1] += __uint_as_float(s0 & 0xFFFF0000u);
-          ac[2] += __uint_as_float(s1 << 16);
-          ac[3] += __uint_as_float(s1 & 0xFFFF0000u);
-          ac[4] += __uint_as_float(s2 << 16);
-          ac[5] += __uint_as_float(s2 & 0xFFFF0000u);
-          ac[6] += __uint_as_float(s3 << 16);
-          ac[7] += __uint_as_float(s3 & 0xFFFF0000u);
+          bf16x8_accumulate(acc[qy * 2 + qx], s0, s1, s2, s3);
         }
       }
     }
@@ -341,7 +357,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
   for (int q = 0; q < 4; ++q) {
     const int y = 2 * Y + (q >> 1), x = 2 * X + (q & 1);
     if (y >= H || x >= W) continue;
-    const long long o = (((long long)b * H + y) * W + x) * C + c0;
+    const unsigned o = (((unsigned)b * H + y) * W + x) * (unsigned)C + c0;
     if (mask) {
       float mk[8];
       Vec8<__nv_bfloat16>::load(mask + o, mk);
@@ -360,6 +376,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_k(int B, int H, int
 // and pool_bias_rows_k sums the CTA rows (a CTA per 8 channels, fixed tree).
 // Deterministic; saves the separate two-pass reduction that re-read gx.
 __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H, int W, int C, int Ho, int Wo,
+                                                                    FastDiv fcg, FastDiv fw2, FastDiv fh2,
                                                                     const __nv_bfloat16* __restrict__ gy,
                                                                     const uint8_t* __restrict__ arg,
                                                                     const __nv_bfloat16* __restrict__ mask,
@@ -372,11 +389,11 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H
   const unsigned total = (unsigned)B * H2 * W2 * cg;
   float bsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const unsigned blk = t / cg;
+    const unsigned blk = fcg.div(t);
     const int c0 = (int)(t - blk * cg) * 8;
-    const unsigned r = blk / (unsigned)W2;
+    const unsigned r = fw2.div(blk);
     const int X = (int)(blk - r * W2);
-    const int b = (int)(r / (unsigned)H2);
+    const int b = (int)fh2.div(r);
     const int Y = (int)(r - (unsigned)b * H2);
     float acc[4][8];
 #pragma unroll
@@ -391,7 +408,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H
       for (int dx = -1; dx <= 0; ++dx) {
         const int ox = X + dx;
         if (ox < 0 || ox >= Wo) continue;
-        const long long o = (((long long)b * Ho + oy) * Wo + ox) * C + c0;
+        const unsigned o = (((unsigned)b * Ho + oy) * Wo + ox) * (unsigned)C + c0;
         const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + o));
         const uint4 g = __ldg(reinterpret_cast<const uint4*>(gy + o));
 #pragma unroll
@@ -406,15 +423,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H
             const unsigned m0 = __vcmpeq4(a.x, want), m1 = __vcmpeq4(a.y, want);
             const unsigned s0 = g.x & __byte_perm(m0, 0, 0x1100), s1 = g.y & __byte_perm(m0, 0, 0x3322);
             const unsigned s2 = g.z & __byte_perm(m1, 0, 0x1100), s3 = g.w & __byte_perm(m1, 0, 0x3322);
-            float* ac = acc[qy * 2 + qx];
-            ac[0] += __uint_as_float(s0 << 16);
-            ac[1] += __uint_as_float(s0 & 0xFFFF0000u);
-            ac[2] += __uint_as_float(s1 << 16);
-            ac[3] += __uint_as_float(s1 & 0xFFFF0000u);
-            ac[4] += __uint_as_float(s2 << 16);
-            ac[5] += __uint_as_float(s2 & 0xFFFF0000u);
-            ac[6] += __uint_as_float(s3 << 16);
-            ac[7] += __uint_as_float(s3 & 0xFFFF0000u);
+            bf16x8_accumulate(acc[qy * 2 + qx], s0, s1, s2, s3);
           }
         }
       }
@@ -423,7 +432,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_bf16_k3s2_bias_k(int B, int H
     for (int q = 0; q < 4; ++q) {
       const int y = 2 * Y + (q >> 1), x = 2 * X + (q & 1);
       if (y >= H || x >= W) continue;
-      const long long o = (((long long)b * H + y) * W + x) * C + c0;
+      const unsigned o = (((unsigned)b * H + y) * W + x) * (unsigned)C + c0;
       if (mask) {
         float mk[8];
         Vec8<__nv_bfloat16>::load(mask + o, mk);
@@ -531,7 +540,7 @@ __global__ void maxpool_bwd_k3s2_k(int B, int H, int W, int C, int Ho, int Wo, c
   for (int q = 0; q < 4; ++q) {
     const int y = 2 * Y + (q >> 1), x = 2 * X + (q & 1);
     if (y >= H || x >= W) continue;
-    const long long o = (((long long)b * H + y) * W + x) * C + c0;
+    const unsigned o = (((unsigned)b * H + y) * W + x) * (unsigned)C + c0;
     if (mask) {
       float mk[8];
       Vec8<T>::load(mask + o, mk);
@@ -1024,9 +1033,10 @@ extern "C" int pc_maxpool_forward(int B, int H, int W, int C, int k, int s, cons
   long long work = (long long)B * Ho * Wo * (vec ? C / 8 : C);
   PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
   DISPATCH_PREC(prec, T, {
-    if (vec && k == 3 && s == 2 && prec == PC_BF16 && aligned(x, 16))
+    if (vec && k == 3 && s == 2 && prec == PC_BF16 && aligned(x, 16) && (long long)B * H * W * C < (1LL << 31))
       maxpool_fwd_bf16_k3s2_k<<<grid_for(work, 256), 256, 0, S(st)>>>(
-          B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), argmax);
+          B, H, W, C, Ho, Wo, FastDiv(C / 8), FastDiv(Wo), FastDiv(Ho), static_cast<const __nv_bfloat16*>(x),
+          static_cast<__nv_bfloat16*>(y), argmax);
     else if (vec && k == 3 && s == 2)
       maxpool_fwd_k<T, 8, 3, 2><<<grid_for(work, 256), 256, 0, S(st)>>>(
           B, H, W, C, k, s, Ho, Wo, static_cast<const T*>(x), static_cast<T*>(y), argmax);
@@ -1060,8 +1070,9 @@ extern "C" int pc_maxpool_backward_bias(int B, int H, int W, int C, int k, int s
   int Ho, Wo, rc = pool_geom(H, W, k, s, &Ho, &Wo);
   if (rc) return rc;
   PC_REQUIRE(prec == PC_BF16 && k == 3 && s == 2 && C % 8 == 0 && 256 % (C / 8) == 0 && aligned(gy, 32) &&
-                 aligned(gx, 32) && aligned(argmax, 8) && (!mask || aligned(mask, 32)) && aligned(ws, 16),
-             PC_EVALUE, "maxpool_backward_bias: bf16 3x3/s2, C/8 dividing 256, aligned buffers");
+                 aligned(gx, 32) && aligned(argmax, 8) && (!mask || aligned(mask, 32)) && aligned(ws, 16) &&
+                 (long long)B * H * W * C < (1LL << 31),
+             PC_EVALUE, "maxpool_backward_bias: bf16 3x3/s2, C/8 dividing 256, aligned buffers, < 2^31 elements");
   PC_REQUIRE(ws_bytes >= pc_maxpool_backward_bias_workspace(C), PC_EVALUE, "maxpool_backward_bias: workspace");
   if ((long long)B * C == 0) {
     cudaMemsetAsync(gb, 0, sizeof(float) * C, S(st));
@@ -1069,7 +1080,8 @@ extern "C" int pc_maxpool_backward_bias(int B, int H, int W, int C, int k, int s
   }
   float* part = static_cast<float*>(ws);
   maxpool_bwd_bf16_k3s2_bias_k<<<pool_bias_ctas(), 256, 0, S(st)>>>(
-      B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(gy), argmax, static_cast<const __nv_bfloat16*>(mask),
+      B, H, W, C, Ho, Wo, FastDiv(C / 8), FastDiv((W + 1) / 2), FastDiv((H + 1) / 2),
+      static_cast<const __nv_bfloat16*>(gy), argmax, static_cast<const __nv_bfloat16*>(mask),
       static_cast<__nv_bfloat16*>(gx), part);
   pool_bias_rows_k<<<C / 8, 256, 0, S(st)>>>(part, pool_bias_ctas(), C, gb);
   count_launches(1);
@@ -1089,9 +1101,10 @@ extern "C" int pc_maxpool_backward(int B, int H, int W, int C, int k, int s, con
   PC_REQUIRE(work < (1LL << 31), PC_EVALUE, "maxpool: too many elements for one launch");
   const long long work22 = (long long)B * ((H + 1) / 2) * ((W + 1) / 2) * (C / 8);
   DISPATCH_PREC(prec, T, {
-    if (vec && k == 3 && s == 2 && prec == PC_BF16)
+    if (vec && k == 3 && s == 2 && prec == PC_BF16 && (long long)B * H * W * C < (1LL << 31))
       maxpool_bwd_bf16_k3s2_k<<<grid_for(work22, 256), 256, 0, S(st)>>>(
-          B, H, W, C, Ho, Wo, static_cast<const __nv_bfloat16*>(gy), argmax,
+          B, H, W, C, Ho, Wo, FastDiv(C / 8), FastDiv((W + 1) / 2), FastDiv((H + 1) / 2),
+          static_cast<const __nv_bfloat16*>(gy), argmax,
           static_cast<const __nv_bfloat16*>(mask), static_cast<__nv_bfloat16*>(gx));
     else if (vec && k == 3 && s == 2)
       maxpool_bwd_k3s2_k<T><<<grid_for(work22, 256), 256, 0, S(st)>>>(
