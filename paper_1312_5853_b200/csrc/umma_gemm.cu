@@ -71,7 +71,15 @@ enum AMode {
   // A_IM2COL_MN5 on a CTA pair: three M accumulators per CTA (768 rows per pair tile,
   // N <= 96 packed at p.N columns), the pair sharing the upstream-gradient tile; chunks
   // of rows past M are not loaded. Input layer weight gradient: 576 x 96.
-  A_IM2COL_MN3P = 14
+  A_IM2COL_MN3P = 14,
+  // A_IM2COL_K with TWO M accumulators per CTA (a CTA pair covers 512 output pixels,
+  // TMEM 2 x BN columns, not double-buffered): each stage brings two 16 KB im2col
+  // boxes and the CTA's one B half, so every B byte feeds twice the MMA work —
+  // 48 KB per 1024 MMA cycles instead of 32 KB per 512 (the forward / data
+  // gradient GEMMs are operand-delivery bound); the epilogue is not overlapped.
+  // Chosen when the 512-row tiles quantise onto the 74 pairs as well as 256-row
+  // ones (AlexNet conv2 forward: 365 tiles)
+  A_IM2COL_K2 = 15
 };
 enum BMode { B_TMA_K = 0, B_TMA_MN = 1 };
 enum EpiMode { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_T = 2, EPI_SGD = 3 };
@@ -398,7 +406,7 @@ template <int AM> constexpr bool a_is_mn() {
 }
 template <int AM> constexpr int macc_of() {
   return AM == A_IM2COL_MN5 ? 5 : AM == A_IM2COL_MN3P ? 3
-         : (AM == A_IM2COL_MN2 || AM == A_IM2COL_MN2_32 || AM == A_HALO_KR2) ? 2 : 1;
+         : (AM == A_IM2COL_MN2 || AM == A_IM2COL_MN2_32 || AM == A_HALO_KR2 || AM == A_IM2COL_K2) ? 2 : 1;
 }
 
 // Per-CTA shared memory: STAGES x (A 128 rows + B BN/CG rows) x 64 bf16, barriers.
@@ -1094,6 +1102,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       const int n0 = tc.n0 + (int)rank * (AM == A_IM2COL_MN3P ? p.N / 2 : BNC);
       // A_IM2COL_K: tile's first output pixel (fixed) and the K position (c, i, j) of kb
       int t_b = 0, t_oy = 0, t_ox = 0, kc = 0, ki = 0, kj = 0, kblk = 0, kcoff = 0, ktap = 0;
+      int t_b1 = 0, t_oy1 = 0, t_ox1 = 0;  // A_IM2COL_K2: the second accumulator's first pixel
       // A_IM2COL_MN: per-chunk (i, j, blk, coff) of the tile's M rows (fixed) and kb's pixel (b, oy, ox)
       constexpr bool A32 = AM == A_IM2COL_MN2_32;
       constexpr int ACH = A32 ? MACC * BM / 32 : MACC * BM / 64;  // A chunks per stage
@@ -1110,7 +1119,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         kc = (tc.kb_begin / p.i2c_k) * BK;
         kj = tc.kb_begin - (tc.kb_begin / p.i2c_k) * p.i2c_k;
       }
-      if constexpr (AM == A_IM2COL_K || IKR) {
+      if constexpr (AM == A_IM2COL_K || IKR || AM == A_IM2COL_K2) {
         // a CTA whose rows all lie past M (second half of a partial pair tile) loads
         // the first pixels instead (its rows are discarded by the epilogue): an
         // im2col start pixel outside the tensor faults the TMA unit
@@ -1119,6 +1128,13 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         const int q = mv / p.i2c_Wo;
         t_oy = q % p.i2c_Ho;
         t_b = q / p.i2c_Ho;
+        if constexpr (AM == A_IM2COL_K2) {  // accumulator 1: rows [m0 + 128 CG, +128)
+          const int m1 = m0 + BM * CG, mv1 = m1 < p.M ? m1 : 0;
+          t_ox1 = mv1 % p.i2c_Wo;
+          const int q1 = mv1 / p.i2c_Wo;
+          t_oy1 = q1 % p.i2c_Ho;
+          t_b1 = q1 / p.i2c_Ho;
+        }
         ktap = tc.kb_begin / p.i2c_cpt;
         kc = (tc.kb_begin - ktap * p.i2c_cpt) * BK;
         ki = ktap / p.i2c_k;
@@ -1176,9 +1192,10 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
                               (i * p.i2c_k + kj) * p.i2c_C + kc, n0, 0);
         } else if (!HALO && elect_one()) {
           // A_IM2COL_K: the k-block of a last chunk with <= 32 channels moves 32-channel boxes
-          const bool half = AM == A_IM2COL_K && p.half_chunk && kc + 32 >= p.i2c_C;
+          const bool half = (AM == A_IM2COL_K || AM == A_IM2COL_K2) && p.half_chunk && kc + 32 >= p.i2c_C;
           if (leader)
             mbar_arrive_expect_tx(&full[s], IKR ? CG * A_STAGE_BYTES
+                                  : AM == A_IM2COL_K2 ? CG * (B_STAGE_BYTES + 2 * A_STAGE_BYTES) / (half ? 2 : 1)
                                   : half ? CG * (B_STAGE_BYTES + A_STAGE_BYTES) / 2
                                   : AM == A_IM2COL_MN3P ? CG * B_STAGE_BYTES + p.macc_chunks * 64 * BK * 2
                                                  : CG * (B_STAGE_BYTES + (GATHER ? 0 : MACC > 1 ? p.macc_chunks * 64 * BK * 2
@@ -1198,13 +1215,20 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
               }
             }
           } else {
-            const int k = AM == A_IM2COL_K ? ktap * p.i2c_C + kc : kb * BK;
+            const int k = (AM == A_IM2COL_K || AM == A_IM2COL_K2) ? ktap * p.i2c_C + kc : kb * BK;
             tma_load_3d<CG>(half ? &p.tma_b32 : &p.tma_b, &full[s], dB, blk_off(k, p.b_cb), n0, blk_idx(k, p.b_cb));
           }
           if constexpr (AM == A_IM2COL_K || IKR) {
             // 128 output pixels from the tile's first pixel; K block = 64 (or 32) channels of tap (i, j)
             tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], smem_u32(sA + s * A_STAGE_BYTES), kcoff,
                               t_ox * p.i2c_s + p.i2c_lw, t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj,
+                              (uint16_t)ki);
+          } else if constexpr (AM == A_IM2COL_K2) {  // one box per accumulator, 16 KB apart
+            const uint32_t dA = smem_u32(sA + s * A_STRIDE);
+            tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], dA, kcoff, t_ox * p.i2c_s + p.i2c_lw,
+                              t_oy * p.i2c_s + p.i2c_lh, t_b, kblk, (uint16_t)kj, (uint16_t)ki);
+            tma_im2col_5d<CG>(half ? &p.tma_a32 : &p.tma_a, &full[s], dA + A_STAGE_BYTES, kcoff,
+                              t_ox1 * p.i2c_s + p.i2c_lw, t_oy1 * p.i2c_s + p.i2c_lh, t_b1, kblk, (uint16_t)kj,
                               (uint16_t)ki);
           } else if constexpr (AM == A_IM2COL_MN || AM == A_IM2COL_MN5 || AM == A_IM2COL_MN2 || A32 ||
                                AM == A_IM2COL_MN3P) {
@@ -1233,7 +1257,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         }
         __syncwarp();
         // advance the im2col K position / pixel walk to the next k-block
-        if constexpr (AM == A_IM2COL_K || IKR) {
+        if constexpr (AM == A_IM2COL_K || IKR || AM == A_IM2COL_K2) {
           kc += BK;
           kcoff += BK;
           if (kcoff >= p.i2c_cs) { kcoff = 0; ++kblk; }
@@ -1418,7 +1442,7 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
         const uint32_t tacc = tmem + acc * TCOLS;
         long long tr_wait = 0, tr_issue = 0;
         // K-major im2col with a partial last channel chunk: k16 steps with real channels
-        const bool partial = AM == A_IM2COL_K && (p.i2c_C % BK) != 0;
+        const bool partial = (AM == A_IM2COL_K || AM == A_IM2COL_K2) && (p.i2c_C % BK) != 0;
         int mchunk = partial ? tc.kb_begin % p.i2c_cpt : 0;
         // halo: k-block = (channel chunk, filter column j): k filter rows per stage
         int hj = HALO ? tc.kb_begin % p.i2c_k : 0, hch = HALO ? tc.kb_begin / p.i2c_k : 0;
@@ -1470,8 +1494,9 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
                 const uint64_t aa = ad + (uint64_t)((a * A_STAGE_BYTES) >> 4);
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
-                  tc_mma<CG>(tacc + (MACC == 2 ? a * tmem_cols<BN>() : a * p.N), aa + kk * A_KSTEP, bd + kk * B_KSTEP,
-                             IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+                  if (kk < nk16)   // A_IM2COL_K2: the remainder chunk's real k16 steps
+                    tc_mma<CG>(tacc + (MACC == 2 ? a * tmem_cols<BN>() : a * p.N), aa + kk * A_KSTEP,
+                               bd + kk * B_KSTEP, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
               }
             } else {
 #pragma unroll
@@ -1825,6 +1850,11 @@ static int launch_kb(const Params& p, Tile t, int splits, cudaStream_t st) {
     if (t.cg == 2 && t.bn <= 96 && kr_stages == 4) return launch<AM, B_TMA_K, EPI, 96, 4, 2>(p, splits, st);
     if (t.cg == 2 && t.bn <= 96) return launch<AM, B_TMA_K, EPI, 96, 5, 2>(p, splits, st);
     PC_REQUIRE(false, PC_ESHAPE, "resident-B halo: CTA pair with N <= 96 only");
+  } else if constexpr (AM == A_IM2COL_K2) {  // two 16 KB A boxes + the B half per stage; CTA pair only
+    if (t.cg == 2 && t.bn == 256) return launch<AM, B_TMA_K, EPI, 256, 4, 2>(p, splits, st);
+    if (t.cg == 2 && t.bn == 192) return launch<AM, B_TMA_K, EPI, 192, 4, 2>(p, splits, st);
+    if (t.cg == 2 && t.bn == 128) return launch<AM, B_TMA_K, EPI, 128, 5, 2>(p, splits, st);
+    PC_REQUIRE(false, PC_ESHAPE, "two-accumulator im2col: CTA pair with N in {128, 192, 256}");
   } else if constexpr (AM == A_HALO_K) {  // stages of (window + k B tiles); N <= 128
     if (t.cg == 2) {
       if (t.bn <= 64) return launch<AM, B_TMA_K, EPI, 64, 4, 2>(p, splits, st);
@@ -2022,6 +2052,28 @@ static bool halo_res_fits(const Params& p, int N) {
          pair_tiles >= 74;
 }
 
+// A_IM2COL_K2 (two accumulators per CTA) instead of A_IM2COL_K: the 512-row pair
+// tiles cut the operand bytes per FLOP by a quarter (~1.2x measured on conv2's
+// forward) but double the tile size, so they pay only where the tiles still fill
+// the pairs' waves: the share of busy pair-slots in the last wave, weighted by that
+// gain, must not drop below the 256-row tiling's. PC_K2=0: never, 2: always.
+static bool k2_wanted(long long M, int N, const Tile& t) {
+  static const int mode = [] {
+    const char* e = getenv("PC_K2");
+    return e ? atoi(e) : 1;
+  }();
+  if (mode == 0 || t.cg != 2 || (t.bn != 128 && t.bn != 192 && t.bn != 256)) return false;
+  if (mode == 2) return true;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long pairs = sms / 2, nt = (N + t.bn - 1) / t.bn;
+  const long long u1 = (M + 2 * BM - 1) / (2 * BM) * nt, u2 = (M + 4 * BM - 1) / (4 * BM) * nt;
+  const double e1 = (double)u1 / (double)(((u1 + pairs - 1) / pairs) * pairs);
+  const double e2 = (double)u2 / (double)(((u2 + pairs - 1) / pairs) * pairs);
+  return e2 * 1.15 > e1;
+}
+
 int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const float* bias, void* y,
                       int flags, cudaStream_t st) {
   if (!conv_tc_shape(g)) {
@@ -2111,6 +2163,7 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
       if (rc) return rc;
       p.half_chunk = 1;
     }
+    if (k2_wanted(g.B * g.Ho * g.Wo, g.N, t)) return launch_kb<A_IM2COL_K2, EPI_BF16>(p, t, 1, st);
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
   return launch_kb<A_GATHER_FWD, EPI_BF16>(p, t, 1, st);
@@ -2220,6 +2273,7 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
     if (rc) return rc;
     set_i2c(p, g.N, g.N, g.k, 1, lo, g.W, g.H);
     set_i2c_kloop(p, g.N, g.k);
+    if (k2_wanted(M, g.C, t)) return launch_kb<A_IM2COL_K2, EPI_BF16>(p, t, 1, st);
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
   return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, t, 1, st);
