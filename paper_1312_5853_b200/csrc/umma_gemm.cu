@@ -2177,10 +2177,13 @@ static int bf16_out_map(Params* p, void* y, int N, long long M) {
 }
 
 // A_IM2COL_K2 (two accumulators per CTA) instead of A_IM2COL_K: the 512-row pair
-// tiles cut the operand bytes per FLOP by a quarter (~1.2x measured on conv2's
-// forward) but double the tile size, so they pay only where the tiles still fill
-// the pairs' waves: the share of busy pair-slots in the last wave, weighted by that
-// gain, must not drop below the 256-row tiling's. PC_K2=0: never, 2: always.
+// tiles cut the TMA rows per MMA cycle by a quarter — the per-tile trace shows the
+// main loop MMA-bound at 1009 cycles per k-block (1024 ideal) where A_IM2COL_K needs
+// 719 for half the work — and with the TMA-store epilogue (6k cycles per tile, not
+// overlapped) conv2's forward runs 181 -> 159 us; but the tiles are twice as large,
+// so they pay only where they still fill the pairs' waves: the share of busy pair
+// slots, weighted by that gain, must beat the 256-row tiling's. Only with the TMA
+// epilogue (plain NHWC output, no ReLU mask). PC_K2=0: never, 2: always.
 static bool k2_wanted(long long M, int N, const Tile& t) {
   static const int mode = [] {
     const char* e = getenv("PC_K2");
@@ -2195,7 +2198,7 @@ static bool k2_wanted(long long M, int N, const Tile& t) {
   const long long u1 = (M + 2 * BM - 1) / (2 * BM) * nt, u2 = (M + 4 * BM - 1) / (4 * BM) * nt;
   const double e1 = (double)u1 / (double)(((u1 + pairs - 1) / pairs) * pairs);
   const double e2 = (double)u2 / (double)(((u2 + pairs - 1) / pairs) * pairs);
-  return e2 * 1.15 > e1;
+  return e2 * 1.25 > e1;
 }
 
 int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const float* bias, void* y,
@@ -2287,10 +2290,10 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
       if (rc) return rc;
       p.half_chunk = 1;
     }
-    if (k2_wanted(g.B * g.Ho * g.Wo, g.N, t)) {
+    if (g.N % 64 == 0 && k2_wanted(g.B * g.Ho * g.Wo, g.N, t)) {
       rc = bf16_out_map(&p, y, g.N, (long long)g.B * g.Ho * g.Wo);
       if (rc) return rc;
-      return launch_kb<A_IM2COL_K2, EPI_BF16>(p, t, 1, st);
+      if (p.out_tma) return launch_kb<A_IM2COL_K2, EPI_BF16>(p, t, 1, st);
     }
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
@@ -2401,7 +2404,11 @@ int umma_conv_dgrad(const pc_conv_geom& g, const void* w, const void* gy, void* 
     if (rc) return rc;
     set_i2c(p, g.N, g.N, g.k, 1, lo, g.W, g.H);
     set_i2c_kloop(p, g.N, g.k);
-    if (k2_wanted(M, g.C, t)) return launch_kb<A_IM2COL_K2, EPI_BF16>(p, t, 1, st);
+    if (!mask && g.cs == g.C && g.C % 64 == 0 && k2_wanted(M, g.C, t)) {
+      rc = bf16_out_map(&p, gx, g.C, M);
+      if (rc) return rc;
+      if (p.out_tma) return launch_kb<A_IM2COL_K2, EPI_BF16>(p, t, 1, st);
+    }
     return launch_kb<A_IM2COL_K, EPI_BF16>(p, t, 1, st);
   }
   return launch_kb<A_GATHER_DGRAD, EPI_BF16>(p, t, 1, st);
