@@ -17,9 +17,9 @@ namespace pc {
 constexpr int SB_M = 64, SB_N = 64, SB_K = 16, S_NT = 256;
 
 // ACC = double for the weight gradients: their reductions run over every pixel of
-// the batch (AlexNet conv1 at B = 256: 774,400 terms), where a float chain of a
-// split's ~30k dependent adds loses ~1e-3 relative to cancellation; products of
-// two floats are exact in double, so only the fp32 operands' own rounding remains.
+// the batch (AlexNet conv1 at B = 256: 774,400 terms, ~30k dependent adds per
+// split-K slice); products of two floats are exact in double, so only the fp32
+// operands' own rounding remains in the verification mode.
 template <class AL, class BL, class EP, typename ACC = float>
 __global__ void __launch_bounds__(S_NT) simt_gemm_k(int M, int N, int K, int kps, AL a, BL b, EP ep) {
   __shared__ float As[SB_K][SB_M + 4];
