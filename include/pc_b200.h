@@ -288,6 +288,9 @@ PC_API int pc_set_grid_cap(int ctas);
  * bias needs no separate reduction over the upstream gradient. */
 PC_API int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
                                 int ones, void* dst, pc_stream_t stream);
+/* pc_space_to_depth_ex with float32 output (the tf32 mode's input layer). */
+PC_API int pc_space_to_depth_f32(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
+                                 int ones, float* dst, pc_stream_t stream);
 /* gb[n] = gw[n * K + ones] for n < N, then gw[i] = 0 where keep[i] == 0 (the
  * structural zeros of the regrouped input-layer weights, including `ones`). */
 PC_API int pc_s2d_wgrad_finish(int N, int K, int ones, const uint8_t* keep, float* gw, float* gb,

@@ -80,6 +80,7 @@ SIGNATURES = {
     "pc_s2d_wgrad_finish": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
     "pc_lrn_forward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _i, _vp]),
     "pc_lrn_backward": (_i, [_ll, _i, _i, _f, _f, _f, _vp, _vp, _vp, _i, _vp]),
+    "pc_space_to_depth_f32": (_i, [_i, _i, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp]),
     "pc_im2col_ex": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp]),
     "pc_enable_peer_access": (_i, [_i]),
     "pc_copy_async": (_i, [_vp, _vp, _sz, _vp]),

@@ -808,9 +808,9 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
 __device__ __forceinline__ float ldg_ro(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float ldg_ro(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
 
-template <typename TS, int CS, int SS, int CC>  // SS, CC > 0: compile-time stride / channels
+template <typename TS, int CS, int SS, int CC, typename TD = __nv_bfloat16>  // SS, CC > 0: compile-time stride / channels
 __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_, int p, int Hs, int Ws,
-                                             const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst, int ones) {
+                                             const TS* __restrict__ x, TD* __restrict__ dst, int ones) {
   const int s = SS > 0 ? SS : s_, C = CC > 0 ? CC : C_;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)B * Hs * Ws) return;
@@ -849,9 +849,9 @@ __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_
       }
     }
   }
-  __nv_bfloat16* out = dst + t * CS;
+  TD* out = dst + t * CS;
 #pragma unroll
-  for (int q = 0; q < CS / 8; ++q) Vec8<__nv_bfloat16>::store(out + q * 8, v + q * 8);
+  for (int q = 0; q < CS / 8; ++q) Vec8<TD>::store(out + q * 8, v + q * 8);
 }
 
 // bf16 source, one CTA per output block row (b, Y): for each channel the SS input
@@ -1221,6 +1221,32 @@ extern "C" int pc_im2col_ex(int B, int C, int H, int W, int k, int s, int p, int
 extern "C" int pc_space_to_depth(int B, int C, int H, int W, int s, int p, int Cs, const void* src, int src_prec,
                                  void* dst, pc_stream_t st) {
   return pc_space_to_depth_ex(B, C, H, W, s, p, Cs, src, src_prec, -1, dst, st);
+}
+
+// Float32 output (the tf32 mode's input layer runs the same space-to-depth 3x3 conv).
+extern "C" int pc_space_to_depth_f32(int B, int C, int H, int W, int s, int p, int Cs, const void* src,
+                                     int src_prec, int ones, float* dst, pc_stream_t st) {
+  PC_REQUIRE(B >= 0 && C > 0 && H > 0 && W > 0 && s > 0 && p >= 0 && Cs >= s * s * C && (Cs == 64 || Cs == 32),
+             PC_EVALUE, "space_to_depth: bad arguments (Cs must be 32 or 64 and >= s*s*C)");
+  PC_REQUIRE(ones < 0 || (ones >= s * s * C && ones < Cs), PC_EVALUE,
+             "space_to_depth: the ones channel must be a padding channel");
+  const int Hs = (H + 2 * p + s - 1) / s, Ws = (W + 2 * p + s - 1) / s;
+  const long long n = (long long)B * Hs * Ws;
+  if (n == 0) return PC_OK;
+  const int g = grid_for(n, 256);
+  DISPATCH_PREC(src_prec, TS, {
+    const TS* x = static_cast<const TS*>(src);
+    if (Cs == 64 && s == 4 && C == 3)
+      s2d_k<TS, 64, 4, 3, float><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, dst, ones);
+    else if (Cs == 64 && s == 2 && C == 3)
+      s2d_k<TS, 64, 2, 3, float><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, dst, ones);
+    else if (Cs == 64)
+      s2d_k<TS, 64, 0, 0, float><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, dst, ones);
+    else
+      s2d_k<TS, 32, 0, 0, float><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, dst, ones);
+  });
+  PC_CUDA_CHECK_LAUNCH("space_to_depth");
+  return PC_OK;
 }
 
 extern "C" int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, int Cs, const void* src,

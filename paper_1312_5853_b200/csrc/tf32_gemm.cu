@@ -315,7 +315,26 @@ __global__ void __launch_bounds__(192, 1) tf32_gemm_k(const __grid_constant__ Pa
         const int nc = min(32, p.N - n0);
         if constexpr (EPI == E_PART) {
           float* o = p.part + ((long long)z * p.M + m) * p.N + n0;
-          for (int i = 0; i < nc; ++i) o[i] = v[i];
+          if (nc == 32 && (p.N & 3) == 0) {   // 128 contiguous bytes per lane: 8 x 16-byte stores
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              reinterpret_cast<float4*>(o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+            for (int i = 0; i < nc; ++i) o[i] = v[i];
+          }
+        } else if (nc == 32 && !p.mask && (p.o_cb & 31) == 0 && (n0 % p.o_cb) + 32 <= p.o_cb &&
+                   ((p.o_ld | p.o_bstride) & 3) == 0) {
+          // the 32 columns lie in one channel block: bias + ReLU, 8 x 16-byte stores
+          const long long blk = n0 / p.o_cb;
+          float* o = p.out + blk * p.o_bstride + m * p.o_ld + (n0 - blk * p.o_cb);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float val = p.bias ? v[i] + p.bias[n0 + i] : v[i];
+            v[i] = p.relu ? (val > 0.f ? val : 0.f) : val;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(o)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         } else {
           for (int i = 0; i < nc; ++i) {
             const long long n = n0 + i;

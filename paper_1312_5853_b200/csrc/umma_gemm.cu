@@ -1529,7 +1529,6 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
       // and of one KR2 sub-tile (R filter rows)
       const uint32_t hrstep = HALO ? (uint32_t)((p.halo_Wv * 128) >> 4) : 0u;
       const uint32_t hastep = HALO ? (uint32_t)p.halo_R * hrstep : 0u;
-      const int hk = HALO ? p.i2c_k : 0;
       if constexpr (BRES) {
         mbar_wait(bres, 0);
         tc_fence_after();
@@ -1577,23 +1576,18 @@ __global__ void __launch_bounds__(kernel_threads<AM>(), 1) umma_gemm_k(const __g
                                      : (half ? b0h : b0) + (uint64_t)((s * B_STRIDE) >> 4);
             if constexpr (HALO) {
               // filter row i: the window shifted by i * Wv rows (multiple of 8), B tile i;
-              // KR2 sub-tile a: further shifted by a * R * Wv rows, accumulator a. Fully
-              // unrolled over (a, i <= HALO_KMAX, kk) with the row shift in a register: the
-              // descriptor arithmetic per MMA is one add (an N = 96 MMA is 48 tensor cycles;
-              // the runtime-bounded loop spent ~55 issue cycles per MMA, trace_gemm.py)
+              // KR2 sub-tile a: further shifted by a * R * Wv rows, accumulator a
+              const int k = p.i2c_k;
 #pragma unroll
               for (int a = 0; a < (KR2 ? 2 : 1); ++a)
+              for (int i = 0; i < k; ++i) {
+                const uint64_t ai = ad + (uint64_t)(a * hastep + i * hrstep);
+                const uint64_t bi = bd + (uint64_t)((i * B_STAGE_BYTES) >> 4);
 #pragma unroll
-              for (int i = 0; i < HALO_KMAX; ++i) {
-                if (i < hk) {
-                  const uint64_t ai = ad + (uint64_t)(a * hastep + i * hrstep);
-                  const uint64_t bi = bd + (uint64_t)((i * B_STAGE_BYTES) >> 4);
-#pragma unroll
-                  for (int kk = 0; kk < BK / 16; ++kk)
-                    if (kk < nk16)
-                      tc_mma<CG>(tacc + a * tmem_cols<BN>(), ai + kk * A_KSTEP, bi + kk * B_KSTEP, IDESC,
-                                 (it > 0 || i > 0 || kk > 0) ? 1u : 0u);
-                }
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  if (kk < nk16)
+                    tc_mma<CG>(tacc + a * tmem_cols<BN>(), ai + kk * A_KSTEP, bi + kk * B_KSTEP, IDESC,
+                               (it > 0 || i > 0 || kk > 0) ? 1u : 0u);
               }
             } else if constexpr (MACC > 1) {
               // accumulator a: A rows [128 a, 128 a + 128) of the stage (two 64-row chunks)

@@ -125,8 +125,8 @@ class ColumnEngine:
         self.s2d = 0
         self.s2d_ones = -1
         lay0 = first.layer if isinstance(first.layer, Conv) else None
-        if self.prec == L.PC_BF16 and lay0 is not None and c % 64 and lay0.stride > 1 and \
-                c * lay0.stride ** 2 <= 64:
+        tc = self.prec == L.PC_BF16 or self.cprec == L.PC_TF32    # a tensor-core input layer
+        if tc and lay0 is not None and c % 64 and lay0.stride > 1 and c * lay0.stride ** 2 <= 64:
             self.s2d = lay0.stride
             self.s2d_hw = (layout.s2d_extent(h, lay0.kernel, lay0.stride, lay0.pad)[0],
                            layout.s2d_extent(w, lay0.kernel, lay0.stride, lay0.pad)[0])
@@ -620,8 +620,9 @@ class ColumnEngine:
         self.x_src_es = x_nchw.element_size()
         if self.s2d:
             lay = self.cs.col_layers[0].layer
-            self._pcall(-1, "input", "pc_space_to_depth_ex", self.B, c, h, w, lay.stride, lay.pad, 64, x_nchw.data_ptr(),
-                          src_prec, self.s2d_ones, self.x.data_ptr(), self.stream)
+            self._pcall(-1, "input", "pc_space_to_depth_ex" if self.prec == L.PC_BF16 else "pc_space_to_depth_f32",
+                        self.B, c, h, w, lay.stride, lay.pad, 64, x_nchw.data_ptr(), src_prec, self.s2d_ones,
+                        self.x.data_ptr(), self.stream)
         elif self.col_kp:
             lay = self.cs.col_layers[0].layer
             self._pcall(-1, "input", "pc_im2col_ex", self.B, c, h, w, lay.kernel, lay.stride, lay.pad, self.col_kp,
