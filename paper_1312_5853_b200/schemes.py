@@ -397,15 +397,21 @@ class _Runner:
             return torch.stack([e.bad_label.reshape(()) for e in self.engines.values()]).sum().double()
 
         if getattr(self, "fwd_done", None) is not None and not self.fabric.dist:
+            # after the forward only, on the loss stream: the losses (f64) and label flags
+            # (i32) go straight to pinned host memory by device-to-host copies (no kernels)
             ls = self.loss_stream
             ls.wait_event(self.fwd_done)
-            with torch.cuda.stream(ls):     # everything here runs after the forward only
-                vals = torch.stack(parts + [flag()])
-                if self.loss_host.numel() != vals.numel():
-                    self.loss_host = torch.zeros(vals.numel(), dtype=torch.float64).pin_memory()
-                self.loss_host.copy_(vals, non_blocking=True)
+            engines = list(self.engines.values())
+            if self.loss_host.numel() != len(parts) or getattr(self, "flag_host", None) is None:
+                self.loss_host = torch.zeros(len(parts), dtype=torch.float64).pin_memory()
+                self.flag_host = torch.zeros(len(engines), dtype=torch.int32).pin_memory()
+            lib = L.lib()
+            for i, t in enumerate(parts):
+                lib.call("pc_copy_async", self.loss_host.data_ptr() + 8 * i, t.data_ptr(), 8, ls.cuda_stream)
+            for j, e in enumerate(engines):
+                lib.call("pc_copy_async", self.flag_host.data_ptr() + 4 * j, e.bad_label.data_ptr(), 4, ls.cuda_stream)
             ls.synchronize()
-            return self._check_loss(self.loss_host.numpy())
+            return self._check_loss(np.append(self.loss_host.numpy(), float(self.flag_host.numpy().sum())))
         if self.fabric.dist:
             m = self.plan.model_columns
             mine = parts[0] if parts else torch.zeros((), dtype=torch.float64, device=self.fabric.torch_device)
