@@ -460,6 +460,14 @@ def _meter_step(fabric: Fabric, cs: ColumnizedSpec, shard: int) -> None:
 
 def hybrid_step(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, batch_x, batch_y,
                 meter: bool = True) -> StepResult:
+    """One synchronous update of the plan (`schemes.py:500-569`).
+
+    Asynchronous contract: the loss is read back as soon as the forward is done
+    (single replica per process), so the call returns while the backward and the
+    update still run on the device; the next call (or any read of the
+    parameters) is ordered after them. A device fault in the backward therefore
+    surfaces at the next call. ``fabric.sync_step = True`` (or PC_SYNC_STEP=1)
+    synchronises before returning."""
     d, m = plan.data_shards, plan.model_columns
     if fabric.n != plan.workers:
         raise ValidationError(f"plan grid {plan.describe()} needs {plan.workers} workers, "
@@ -492,6 +500,9 @@ def hybrid_step(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, batch_x,
             run.upload(batch_x, labels)
             run.program(1.0 / b)
             loss = run.loss()
+    if getattr(fabric, "sync_step", os.environ.get("PC_SYNC_STEP", "0") == "1"):
+        for dev in {fabric.device_of(w) for w in fabric.local_wids}:
+            torch.cuda.synchronize(dev)
     book_step(fabric, plan, cs, shard)
     return StepResult(loss=loss, ledger_bytes=fabric.ledger.total_bytes - before_b,
                       ledger_messages=fabric.ledger.total_messages - before_m)

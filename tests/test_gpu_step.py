@@ -359,3 +359,25 @@ def test_train_device_resident_feed_single_replica_pipelined_upload(precision):
         # steps are compared between the two device feeds only (bit-identical above)
         for n, (got, ref) in enumerate(zip(runs[0][:2], want[:2])):
             assert abs(got - ref) / abs(ref) < 1e-5, n
+
+
+def test_sync_step_option_returns_after_the_update():
+    """fabric.sync_step = True: hybrid_step returns only after the backward and the
+    update have finished (the default returns after the forward, ADVICE r01);
+    both give the same trajectory."""
+    import torch
+    import paper_1312_5853_b200 as P
+    net = P.load_network(CONFIGS / "tinynet.net")
+    plan = P.ParallelPlan(1, 1)
+    cs = P.columnize(net, 1)
+    out = []
+    for sync in (False, True):
+        fab = P.spawn(1, precision="bf16")
+        fab.sync_step = sync
+        P.setup_workers(fab, plan, cs, tree("tiny_p0", (0, 3, 5, 7)), P.SgdState())
+        losses = [P.hybrid_step(fab, plan, cs, STEPS[f"tiny_x{s % 2}"], STEPS[f"tiny_y{s % 2}"]).loss
+                  for s in range(3)]
+        if sync:
+            assert torch.cuda.current_stream().query()
+        out.append((losses, fab._engines[0].p32.clone()))
+    assert out[0][0] == out[1][0] and torch.equal(out[0][1], out[1][1])
