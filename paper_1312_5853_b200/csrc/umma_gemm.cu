@@ -2665,7 +2665,8 @@ __global__ void fc_reduce_epilogue_k(const float* __restrict__ part, int splits,
   const size_t stride = (size_t)M * N;
   const float* src = part + (size_t)m * N + n0;
   float4 a = __ldg(reinterpret_cast<const float4*>(src)), b = __ldg(reinterpret_cast<const float4*>(src) + 1);
-  for (int z = 1; z < splits; ++z) {
+#pragma unroll 4
+  for (int z = 1; z < splits; ++z) {  // unrolled: the slices' loads are in flight together
     const float4 c = __ldg(reinterpret_cast<const float4*>(src + z * stride));
     const float4 d = __ldg(reinterpret_cast<const float4*>(src + z * stride) + 1);
     a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
