@@ -520,14 +520,22 @@ int tf32_conv_forward(const pc_conv_geom& g, const float* x, const float* w, con
   return dispatch<A_I2C, B_K, E_STORE>(p, bn, st);
 }
 
-// wt[c][i][j][n] = w[n][k-1-i][k-1-j][c]: the filters of the data gradient
-__global__ void tf32_dgrad_w_k(const float* __restrict__ w, float* __restrict__ wt, int N, int KK, int C) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= (long long)N * KK * C) return;
-  const int n = (int)(t % N);
-  const long long r = t / N;
-  const int ij = (int)(r % KK), c = (int)(r / KK);
-  wt[t] = w[((long long)n * KK + (KK - 1 - ij)) * C + c];
+// wt[c][i][j][n] = w[n][k-1-i][k-1-j][c]: the filters of the data gradient, per tap
+// a 32 x 32 shared-memory tile transpose of [N][C] (coalesced on both sides)
+__global__ void __launch_bounds__(256) tf32_dgrad_w_k(const float* __restrict__ w, float* __restrict__ wt, int N,
+                                                      int KK, int C) {
+  __shared__ float tile[32][33];
+  const int ij = blockIdx.z, src = KK - 1 - ij;
+  const int c0 = blockIdx.x * 32, n0 = blockIdx.y * 32, tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int n = n0 + r, c = c0 + tx;
+    tile[r][tx] = (n < N && c < C) ? w[((long long)n * KK + src) * C + c] : 0.f;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int c = c0 + r, n = n0 + tx;
+    if (c < C && n < N) wt[((long long)c * KK + ij) * N + n] = tile[tx][r];
+  }
 }
 
 size_t tf32_dgrad_ws(const pc_conv_geom& g) { return ((size_t)g.N * g.k * g.k * g.C + 64) * sizeof(float); }
@@ -536,11 +544,9 @@ int tf32_conv_dgrad(const pc_conv_geom& g, const float* w, const float* gy, floa
                     float* wt, cudaStream_t st) {
   PC_REQUIRE(g.stride == 1 && g.N % 32 == 0, PC_EVALUE, "tf32 data gradient: stride-1 conv, N %% 32 == 0");
   const int KK = g.k * g.k;
-  {
-    const long long n = (long long)g.N * KK * g.C;
-    tf32_dgrad_w_k<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, wt, g.N, KK, g.C);
-    PC_CUDA_CHECK_LAUNCH("tf32_dgrad_w");
-  }
+  tf32_dgrad_w_k<<<dim3((unsigned)ceil_div(g.C, 32), (unsigned)ceil_div(g.N, 32), (unsigned)KK), 256, 0, st>>>(
+      w, wt, g.N, KK, g.C);
+  PC_CUDA_CHECK_LAUNCH("tf32_dgrad_w");
   // forward conv of gy [B][Ho][Wo][N] (stride 1, pad k-1-p) with wt [C][k][k][N] -> gx [B][H][W][C]
   const int M = g.B * g.H * g.W, K = KK * g.N, pad = g.k - 1 - g.pad;
   Params p = base(M, g.C, K);
@@ -555,7 +561,7 @@ int tf32_conv_dgrad(const pc_conv_geom& g, const float* w, const float* gy, floa
 
 long long tf32_wgrad_splits(const pc_conv_geom& g) {
   Params p = base(g.N, g.k * g.k * g.C, g.B * g.Ho * g.Wo);
-  set_splits(p, 128);
+  set_splits(p, g.k * g.k * g.C >= 256 ? 256 : 128);
   return p.splits;
 }
 
@@ -563,17 +569,20 @@ int tf32_conv_wgrad(const pc_conv_geom& g, const float* x, const float* gy, floa
   // gw[n][(i, j, c)] = sum_p gy[p][n] x_im2col[p][(i, j, c)]: A = gy (MN-major), B = im2col(x) (MN-major)
   const int P = g.B * g.Ho * g.Wo, NN = g.k * g.k * g.C;
   Params p = base(g.N, NN, P);
-  set_splits(p, 128);
+  set_splits(p, NN >= 256 ? 256 : 128);
   PC_REQUIRE(map2(&p.ta, gy, g.N, P, g.N, BK, true) &&
                  map_i2c(&p.tb, x, g.cs, g.W, g.H, g.B, g.C / g.cs, g.cstride, BK, g.k, g.stride, g.pad, true),
              PC_ECUDA, "tf32 conv wgrad: tensor maps");
   p.b_C = g.C, p.b_cs = g.cs, p.b_k = g.k, p.b_s = g.stride, p.b_lo = -g.pad, p.b_Ho = g.Ho, p.b_Wo = g.Wo;
+  // 256-wide N tiles: 48 KB of operands per 128 x 256 x 32 MMA step instead of 32 KB per
+  // 128 x 128 x 32 (the weight gradients are TMA-bound with 4-byte operands)
+  const bool wide = NN >= 256;
   if (p.splits == 1) {
     set_store(p, gw, NN, NN, 0, nullptr, nullptr, false);
-    return launch_bn<A_MN, B_I2C, E_STORE, 128>(p, st);
+    return wide ? launch_bn<A_MN, B_I2C, E_STORE, 256>(p, st) : launch_bn<A_MN, B_I2C, E_STORE, 128>(p, st);
   }
   p.part = part;
-  int rc = launch_bn<A_MN, B_I2C, E_PART, 128>(p, st);
+  int rc = wide ? launch_bn<A_MN, B_I2C, E_PART, 256>(p, st) : launch_bn<A_MN, B_I2C, E_PART, 128>(p, st);
   if (rc) return rc;
   return reduce_partials(part, p.splits, (long long)g.N * NN, gw, st);
 }
@@ -611,25 +620,26 @@ int tf32_fc_dgrad(int B, int D, int U, const float* w, const float* gy, const pc
 
 long long tf32_fc_wgrad_splits(int B, int D, int U) {
   Params p = base(U, D, B);
-  set_splits(p, 128);
+  set_splits(p, D >= 256 ? 256 : 128);
   return p.splits;
 }
 
 int tf32_fc_wgrad(int B, int D, int U, const pc_mat& x, const float* gy, float* gw, float* part, cudaStream_t st) {
   // gw[u][d] = sum_b gy[b][u] x[b][d]: A = gy (MN-major), B = x (MN-major, channel-blocked d)
   Params p = base(U, D, B);
-  set_splits(p, 128);
+  set_splits(p, D >= 256 ? 256 : 128);
   const long long cb = x.cb >= D ? D : x.cb, nblk = (D + cb - 1) / cb;
   PC_REQUIRE(map2(&p.ta, gy, U, B, U, BK, true) && map3(&p.tb, x.ptr, cb, B, nblk, x.ld, x.bstride, BK, true),
              PC_ECUDA,
              "tf32 fc wgrad: tensor maps");
   p.b_cb = (int)cb;
+  const bool wide = D >= 256;
   if (p.splits == 1) {
     set_store(p, gw, D, D, 0, nullptr, nullptr, false);
-    return launch_bn<A_MN, B_MN, E_STORE, 128>(p, st);
+    return wide ? launch_bn<A_MN, B_MN, E_STORE, 256>(p, st) : launch_bn<A_MN, B_MN, E_STORE, 128>(p, st);
   }
   p.part = part;
-  int rc = launch_bn<A_MN, B_MN, E_PART, 128>(p, st);
+  int rc = wide ? launch_bn<A_MN, B_MN, E_PART, 256>(p, st) : launch_bn<A_MN, B_MN, E_PART, 128>(p, st);
   if (rc) return rc;
   return reduce_partials(part, p.splits, (long long)U * D, gw, st);
 }
