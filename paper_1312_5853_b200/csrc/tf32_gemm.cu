@@ -322,15 +322,27 @@ __global__ void __launch_bounds__(192, 1) tf32_gemm_k(const __grid_constant__ Pa
           } else {
             for (int i = 0; i < nc; ++i) o[i] = v[i];
           }
-        } else if (nc == 32 && !p.mask && (p.o_cb & 31) == 0 && (n0 % p.o_cb) + 32 <= p.o_cb &&
+        } else if (nc == 32 && (p.o_cb & 31) == 0 && (n0 % p.o_cb) + 32 <= p.o_cb &&
                    ((p.o_ld | p.o_bstride) & 3) == 0) {
-          // the 32 columns lie in one channel block: bias + ReLU, 8 x 16-byte stores
+          // the 32 columns lie in one channel block: bias + ReLU + ReLU mask (16-byte mask
+          // loads of the same layout), 8 x 16-byte stores
           const long long blk = n0 / p.o_cb;
-          float* o = p.out + blk * p.o_bstride + m * p.o_ld + (n0 - blk * p.o_cb);
+          const long long off = blk * p.o_bstride + m * p.o_ld + (n0 - blk * p.o_cb);
+          float* o = p.out + off;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             float val = p.bias ? v[i] + p.bias[n0 + i] : v[i];
             v[i] = p.relu ? (val > 0.f ? val : 0.f) : val;
+          }
+          if (p.mask) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 mk = __ldg(reinterpret_cast<const float4*>(p.mask + off) + i);
+              v[4 * i] = mk.x > 0.f ? v[4 * i] : 0.f;
+              v[4 * i + 1] = mk.y > 0.f ? v[4 * i + 1] : 0.f;
+              v[4 * i + 2] = mk.z > 0.f ? v[4 * i + 2] : 0.f;
+              v[4 * i + 3] = mk.w > 0.f ? v[4 * i + 3] : 0.f;
+            }
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i)
