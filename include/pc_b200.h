@@ -45,7 +45,8 @@ extern "C" {
 
 typedef void* pc_stream_t; /* cudaStream_t */
 
-enum pc_prec { PC_FP32 = 0, PC_BF16 = 1, PC_TF32 = 2 };
+enum pc_prec { PC_FP32 = 0, PC_BF16 = 1, PC_TF32 = 2,
+               PC_FP64 = 3 /* source images only: pc_space_to_depth_ex / _f32 */ };
 enum pc_status { PC_OK = 0, PC_ESHAPE = 1, PC_EVALUE = 2, PC_ECUDA = 3, PC_ENCCL = 4 };
 enum pc_conv_flags { PC_RELU = 1, PC_WANT_DX = 2, PC_WANT_DW = 4, PC_MASK_DX = 8, PC_WT_PRESET = 16,
                      /* forward: the last 16 input channels have structural-zero filter

@@ -16,7 +16,7 @@ from .errors import status_error
 
 LIB_PATH = Path(__file__).resolve().parent / "libpcb200.so"
 
-PC_FP32, PC_BF16, PC_TF32 = 0, 1, 2
+PC_FP32, PC_BF16, PC_TF32, PC_FP64 = 0, 1, 2, 3
 PC_RELU, PC_WANT_DX, PC_WANT_DW, PC_MASK_DX, PC_WT_PRESET, PC_ZERO_TAIL16 = 1, 2, 4, 8, 16, 32
 
 _vp, _i, _ll, _sz, _f, _d = C.c_void_p, C.c_int, C.c_longlong, C.c_size_t, C.c_float, C.c_double

@@ -807,6 +807,9 @@ __global__ void im2col_rows_k(int C, int H, int W, int k, int s, int p, int Ho, 
 // read-only (non-coherent) scalar load of an input written by an earlier kernel
 __device__ __forceinline__ float ldg_ro(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float ldg_ro(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+// float64 source (a parconv caller's images): rounded to float first, exactly the value
+// the float32 host path uploads (the reference's images are float32-quantised)
+__device__ __forceinline__ float ldg_ro(const double* p) { return __double2float_rn(__ldg(p)); }
 
 template <typename TS, int CS, int SS, int CC, typename TD = __nv_bfloat16>  // SS, CC > 0: compile-time stride / channels
 __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_, int p, int Hs, int Ws,
@@ -1234,6 +1237,14 @@ extern "C" int pc_space_to_depth_f32(int B, int C, int H, int W, int s, int p, i
   const long long n = (long long)B * Hs * Ws;
   if (n == 0) return PC_OK;
   const int g = grid_for(n, 256);
+  if (src_prec == PC_FP64) {
+    const double* x = static_cast<const double*>(src);
+    PC_REQUIRE(Cs == 64 && C == 3 && (s == 4 || s == 2), PC_EVALUE, "space_to_depth: float64 source needs C=3, s=2|4");
+    if (s == 4) s2d_k<double, 64, 4, 3, float><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, dst, ones);
+    else s2d_k<double, 64, 2, 3, float><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, dst, ones);
+    PC_CUDA_CHECK_LAUNCH("space_to_depth");
+    return PC_OK;
+  }
   DISPATCH_PREC(src_prec, TS, {
     const TS* x = static_cast<const TS*>(src);
     if (Cs == 64 && s == 4 && C == 3)
@@ -1268,6 +1279,14 @@ extern "C" int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, in
       PC_CUDA_CHECK_LAUNCH("space_to_depth");
       return PC_OK;
     }
+  }
+  if (src_prec == PC_FP64) {   // float64 images straight from the caller (fixed-geometry kernels only)
+    const double* x = static_cast<const double*>(src);
+    PC_REQUIRE(Cs == 64 && C == 3 && (s == 4 || s == 2), PC_EVALUE, "space_to_depth: float64 source needs C=3, s=2|4");
+    if (s == 4) s2d_k<double, 64, 4, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d, ones);
+    else s2d_k<double, 64, 2, 3><<<g, 256, 0, S(st)>>>(B, C, H, W, s, p, Hs, Ws, x, d, ones);
+    PC_CUDA_CHECK_LAUNCH("space_to_depth");
+    return PC_OK;
   }
   DISPATCH_PREC(src_prec, TS, {
     const TS* x = static_cast<const TS*>(src);

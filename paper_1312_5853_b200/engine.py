@@ -616,7 +616,7 @@ class ColumnEngine:
         for the explicit-im2col input layer (the bf16 rounding the device would
         apply anyway, done by the caller's input pipeline)."""
         c, h, w = self.cs.base.input_shape
-        src_prec = L.PC_BF16 if x_nchw.dtype == torch.bfloat16 else L.PC_FP32
+        src_prec = {torch.bfloat16: L.PC_BF16, torch.float64: L.PC_FP64}.get(x_nchw.dtype, L.PC_FP32)
         self.x_src_es = x_nchw.element_size()
         if self.s2d:
             lay = self.cs.col_layers[0].layer
