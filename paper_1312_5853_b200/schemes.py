@@ -254,18 +254,13 @@ class _Runner:
                 xs.record_stream(cs)
             if y.is_cuda:
                 y.record_stream(cs)
+        if raw64:
+            _parallel_copy(self.x_host.numpy(), batch_x)
         with torch.cuda.stream(cs):
             if xs is not None:
                 self.x_dev.copy_(xs)
             elif raw64:
-                # in 4 row chunks: chunk i's host->device copy runs while the host
-                # threads stage chunk i + 1 into pinned memory
-                hn, n = self.x_host.numpy(), shape[0]
-                for c in range(4):
-                    lo, hi = c * n // 4, (c + 1) * n // 4
-                    if hi > lo:
-                        _parallel_copy(hn[lo:hi], batch_x[lo:hi])
-                        self.x_dev[lo:hi].copy_(self.x_host[lo:hi], non_blocking=True)
+                self.x_dev.copy_(self.x_host, non_blocking=True)
             elif x.is_pinned():
                 self.x_dev.copy_(x, non_blocking=True)
             else:
