@@ -316,3 +316,34 @@ def test_space_to_depth_bit_exact(case, src):
     blk = xp.reshape(b, c, hs, s, ws, s).transpose(0, 2, 4, 3, 5, 1).reshape(b, hs, ws, s * s * c)
     want[..., : s * s * c] = torch.as_tensor(blk).bfloat16().float().numpy()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("case", [(3, 3, 227, 227, 4, 0), (2, 3, 64, 64, 2, 1)])
+def test_space_to_depth_float64_source_and_float32_output(case):
+    """The float64 source (a parconv caller's images, PC_FP64) gives exactly the float32
+    source's result; the float32-output variant (tf32 mode) holds the unrounded values;
+    the all-ones padding channel is written by both."""
+    import torch
+    from paper_1312_5853_b200._lib import lib, PC_FP32, PC_FP64
+    b, c, h, w, s, p = case
+    rs = np.random.RandomState(7)
+    x64 = rs.randn(b, c, h, w).astype(np.float32).astype(np.float64)   # float32-exact, like the reference's
+    hs, ws = (h + 2 * p + s - 1) // s, (w + 2 * p + s - 1) // s
+    st = torch.cuda.current_stream().cuda_stream
+    ones = c * s * s
+    res = {}
+    for name, arr, pc in (("f32", torch.as_tensor(x64.astype(np.float32)), PC_FP32),
+                          ("f64", torch.as_tensor(x64), PC_FP64)):
+        xd = arr.cuda()
+        o16 = torch.empty((b, hs, ws, 64), dtype=torch.bfloat16, device="cuda")
+        o32 = torch.empty((b, hs, ws, 64), dtype=torch.float32, device="cuda")
+        lib().call("pc_space_to_depth_ex", b, c, h, w, s, p, 64, xd.data_ptr(), pc, ones, o16.data_ptr(), st)
+        lib().call("pc_space_to_depth_f32", b, c, h, w, s, p, 64, xd.data_ptr(), pc, ones, o32.data_ptr(), st)
+        res[name] = (o16.cpu(), o32.cpu())
+    assert torch.equal(res["f32"][0], res["f64"][0]) and torch.equal(res["f32"][1], res["f64"][1])
+    o32 = res["f64"][1].numpy()
+    assert np.all(o32[..., ones] == 1.0) and np.all(o32[..., ones + 1:] == 0.0)
+    xp = np.zeros((b, c, hs * s, ws * s), np.float32)
+    xp[:, :, p:p + h, p:p + w] = x64.astype(np.float32)[:, :, : hs * s - p, : ws * s - p]
+    blk = xp.reshape(b, c, hs, s, ws, s).transpose(0, 2, 4, 3, 5, 1).reshape(b, hs, ws, s * s * c)
+    assert np.array_equal(o32[..., :ones], blk)

@@ -381,3 +381,53 @@ def test_sync_step_option_returns_after_the_update():
             assert torch.cuda.current_stream().query()
         out.append((losses, fab._engines[0].p32.clone()))
     assert out[0][0] == out[1][0] and torch.equal(out[0][1], out[1][1])
+
+
+def test_float64_numpy_batch_matches_float32_batch_bit_for_bit():
+    """A parconv caller's float64 images travel raw (PC_FP64 source of the input
+    kernel): the step is bit-identical to the float32 upload of the same values."""
+    import torch
+    import paper_1312_5853_b200 as P
+    from paper_1312_5853_b200.data import synthetic_rows
+    net = P.load_network(CONFIGS / "alexnet.net")
+    plan = P.ParallelPlan(1, 1)
+    cs = P.columnize(net, 1)
+    x, y = synthetic_rows(1000, 1, net.input_shape, 2, np.arange(16) * 37)
+    dense = P.init_dense_params(net, 1, std=0.01)
+    out = []
+    for xb in (x.astype(np.float64), torch.from_numpy(x).pin_memory()):
+        fab = P.spawn(1, precision="bf16")
+        P.setup_workers(fab, plan, cs, dense, P.SgdState())
+        losses = [P.hybrid_step(fab, plan, cs, xb, y).loss for _ in range(3)]
+        out.append((losses, fab._engines[0].p32.clone(), fab._runner.x_dev.dtype))
+    assert out[0][2] == torch.float64 and out[1][2] == torch.float32
+    assert out[0][0] == out[1][0] and torch.equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("precision,loss_tol,upd_tol", [("bf16", 1e-2, 0.3), ("tf32", 5e-3, 0.1)])
+def test_alexnet_reference_plan_cross_3_6_8_10(precision, loss_tol, upd_tol):
+    """The reference's shipped two-column plan (cross at conv2, conv3, conv4, conv5 and the
+    FC layers) on AlexNet-227 vs the float64 oracle, per column."""
+    import paper_1312_5853_b200 as P
+    from paper_1312_5853_b200.data import synthetic_rows
+    from paper_1312_5853_b200.plan import plan_columnized, split_params
+    from paper_1312_5853_b200.schemes import column_params
+    net = P.load_network(CONFIGS / "alexnet.net")
+    plan = P.ParallelPlan(1, 2, (3, 6, 8, 10))
+    cs = plan_columnized(net, plan)
+    dense = {i: {k: v.astype(np.float32).astype(np.float64) for k, v in t.items()}
+             for i, t in P.init_dense_params(net, 0, std=0.01).items()}
+    x, y = synthetic_rows(1000, 1, net.input_shape, 3, np.arange(8) * 113)
+    x = x.astype(np.float64)
+    fab = P.spawn(2, precision=precision)
+    P.setup_workers(fab, plan, cs, dense, P.SgdState())
+    res = P.hybrid_step(fab, plan, cs, x, y)
+    of, oloss, _, _ = oracle_replay(net, plan, dense, x, y, fab)
+    assert abs(res.loss - oloss) / oloss < loss_tol
+    for j in range(2):
+        got = column_params(fab, j)
+        start = split_params(dense, cs, j)
+        for i in got:
+            d_got = got[i]["w"] - start[i]["w"]
+            d_ref = of.params[j][i]["w"] - start[i]["w"]
+            assert rel_l2(d_got, d_ref) < upd_tol, (j, i)
