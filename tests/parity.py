@@ -93,10 +93,10 @@ def assert_near_ties(trace, forced, cs, tie_tol=1e-5):
 
 def oracle_replay(net, plan, dense, x, y, fab, tie_tol=None):
     """Oracle step with the device's pool decisions; returns (oracle, loss, trace, flips).
-    tie_tol: 1e-5 of the layer's max in fp32 mode; 2e-2 in bf16 mode (bf16 inputs
-    carry 2^-8 relative rounding, accumulated through the layers)."""
+    tie_tol: 1e-5 of the layer's max in fp32 mode; 2e-2 in the bf16 / tf32 modes
+    (2^-8 / 2^-11 relative operand rounding, accumulated through the layers)."""
     if tie_tol is None:
-        tie_tol = 2e-2 if fab.precision == "bf16" else 1e-5
+        tie_tol = 2e-2 if fab.precision in ("bf16", "tf32") else 1e-5
     forced = device_argmax(fab, plan)
     relu = device_relu_masks(fab, plan)
     trace = {}
