@@ -157,6 +157,12 @@ PC_API int pc_softmax_xent(int B, int K, const void* logits, const int32_t* labe
                     void* grad, double* row_loss, int* bad_label, int prec, pc_stream_t stream);
 /* out[0] = sum_i v[i] in ascending order (one block; deterministic). */
 PC_API int pc_sum_f64(int n, const double* v, double* out, pc_stream_t stream);
+/* pc_softmax_xent + pc_sum_f64 in one launch: the last block to finish (device
+ * ticket, zero-initialised, reset by the kernel) sums row_loss into *loss in
+ * pc_sum_f64's order (bit-identical). Falls back to the two launches for K > 1024. */
+PC_API int pc_softmax_xent_loss(int B, int K, const void* logits, const int32_t* labels, double scale, void* grad,
+                                double* row_loss, int* bad_label, double* loss, unsigned* ticket, int prec,
+                                pc_stream_t stream);
 
 /* Fused momentum-SGD epilogue for a weight gradient (single-replica plans, where
  * no cross-replica reduction sits between the gradient and the update): instead

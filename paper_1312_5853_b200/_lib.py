@@ -84,6 +84,7 @@ SIGNATURES = {
     "pc_im2col_ex": (_i, [_i, _i, _i, _i, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp]),
     "pc_enable_peer_access": (_i, [_i]),
     "pc_copy_async": (_i, [_vp, _vp, _sz, _vp]),
+    "pc_softmax_xent_loss": (_i, [_i, _i, _vp, _vp, _d, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
     "pc_synthetic_rows": (_i, [_i, _i, _ll, C.c_ulonglong, _i, _vp, _i, _f, _vp, _i, _vp]),
     "pc_gather_rows": (_i, [_i, _ll, _vp, _vp, _vp, _vp]),
     "pc_dropout": (_i, [_i, _i, _i, _i, _i, _i, _ll, C.c_ulonglong, _vp, _i, C.c_ulonglong, _f, _vp, _vp, _i, _vp]),

@@ -604,42 +604,72 @@ template <typename T, int KPL>
 __global__ void __launch_bounds__(256) softmax_xent_warp_k(int B, int K, const T* __restrict__ logits,
                                                           const int32_t* __restrict__ labels, double scale,
                                                           T* __restrict__ grad, double* __restrict__ row_loss,
-                                                          int* __restrict__ bad) {
+                                                          int* __restrict__ bad, double* __restrict__ loss_out,
+                                                          unsigned* __restrict__ ticket) {
   PC_PDL_TRIGGER();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= B) return;
-  const T* z = logits + (long long)row * K;
-  float x[KPL];
-  float mx = -INFINITY;
+  if (row < B) {
+    const T* z = logits + (long long)row * K;
+    float x[KPL];
+    float mx = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < KPL; ++j) {
-    const int i = lane + 32 * j;
-    x[j] = i < K ? ld(z + i) : -INFINITY;
-    mx = fmaxf(mx, x[j]);
+    for (int j = 0; j < KPL; ++j) {
+      const int i = lane + 32 * j;
+      x[j] = i < K ? ld(z + i) : -INFINITY;
+      mx = fmaxf(mx, x[j]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      x[j] = lane + 32 * j < K ? expf(x[j] - mx) : 0.f;
+      sum += x[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const int lab = labels[row];
+    const bool ok = lab >= 0 && lab < K;
+    const float inv = 1.f / sum, sc = (float)scale;
+    T* g = grad + (long long)row * K;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const int i = lane + 32 * j;
+      if (i < K) g[i] = cvt<T>((x[j] * inv - (i == lab ? 1.f : 0.f)) * sc);
+    }
+    if (lane == 0) {
+      if (!ok) {
+        *bad = 1;
+        row_loss[row] = 0.0;
+      } else {
+        const double logp = (double)(ld(z + lab) - mx) - log((double)sum);
+        row_loss[row] = -logp * scale;
+      }
+    }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float sum = 0.f;
-#pragma unroll
-  for (int j = 0; j < KPL; ++j) {
-    x[j] = lane + 32 * j < K ? expf(x[j] - mx) : 0.f;
-    sum += x[j];
+  if (loss_out == nullptr) return;
+  // the step loss in the last block to finish (ticket): sum_f64_k's order exactly
+  __shared__ unsigned last;
+  __shared__ double sh[8];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < B; i += 256) acc += __ldcg(row_loss + i);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  const int lab = labels[row];
-  const bool ok = lab >= 0 && lab < K;
-  const float inv = 1.f / sum, sc = (float)scale;
-  T* g = grad + (long long)row * K;
-#pragma unroll
-  for (int j = 0; j < KPL; ++j) {
-    const int i = lane + 32 * j;
-    if (i < K) g[i] = cvt<T>((x[j] * inv - (i == lab ? 1.f : 0.f)) * sc);
-  }
-  if (lane == 0) {
-    if (!ok) { *bad = 1; row_loss[row] = 0.0; return; }
-    const double logp = (double)(ld(z + lab) - mx) - log((double)sum);
-    row_loss[row] = -logp * scale;
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = sh[0];
+    for (int w = 1; w < 8; ++w) t += sh[w];
+    loss_out[0] = t;
+    *ticket = 0u;   // ready for the next step (graph replay)
   }
 }
 
@@ -1132,7 +1162,8 @@ extern "C" int pc_softmax_xent(int B, int K, const void* logits, const int32_t* 
   if (B == 0) return PC_OK;
   if (K <= 32 * 32) {
     DISPATCH_PREC(prec, T, softmax_xent_warp_k<T, 32><<<(B + 7) / 8, 256, 0, S(st)>>>(
-        B, K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label));
+        B, K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label, nullptr,
+        nullptr));
   } else {
     DISPATCH_PREC(prec, T, softmax_xent_k<T, 256><<<B, 256, 0, S(st)>>>(
         K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label));
@@ -1144,6 +1175,22 @@ extern "C" int pc_softmax_xent(int B, int K, const void* logits, const int32_t* 
 extern "C" int pc_sum_f64(int n, const double* v, double* out, pc_stream_t st) {
   sum_f64_k<<<1, 256, 0, S(st)>>>(n, v, out);
   PC_CUDA_CHECK_LAUNCH("sum_f64");
+  return PC_OK;
+}
+
+extern "C" int pc_softmax_xent_loss(int B, int K, const void* logits, const int32_t* labels, double scale, void* grad,
+                                    double* row_loss, int* bad_label, double* loss, unsigned* ticket, int prec,
+                                    pc_stream_t st) {
+  PC_REQUIRE(B >= 0 && K >= 2, PC_ESHAPE, "softmax_xent: bad extents B=%d K=%d", B, K);
+  if (B == 0) return pc_sum_f64(0, row_loss, loss, st);
+  if (K > 32 * 32 || ticket == nullptr) {
+    int rc = pc_softmax_xent(B, K, logits, labels, scale, grad, row_loss, bad_label, prec, st);
+    return rc ? rc : pc_sum_f64(B, row_loss, loss, st);
+  }
+  DISPATCH_PREC(prec, T, softmax_xent_warp_k<T, 32><<<(B + 7) / 8, 256, 0, S(st)>>>(
+      B, K, static_cast<const T*>(logits), labels, scale, static_cast<T*>(grad), row_loss, bad_label, loss,
+      ticket));
+  PC_CUDA_CHECK_LAUNCH("softmax_xent_loss");
   return PC_OK;
 }
 

@@ -2657,6 +2657,9 @@ __global__ void fc_reduce_epilogue_k(const float* __restrict__ part, int splits,
                                      const float* __restrict__ bias, int relu, const __nv_bfloat16* __restrict__ mask,
                                      __nv_bfloat16* __restrict__ out, long long o_ld, long long o_cb,
                                      long long o_bstride) {
+  // launched programmatically dependent on the split-K GEMM (which leaves SMs idle:
+  // 64 of 74 pairs for fc6): CTAs placed early wait here for the GEMM's partials
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   PC_PDL_TRIGGER();
   const int groups = N / 8;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -2693,13 +2696,33 @@ __global__ void fc_reduce_epilogue_k(const float* __restrict__ part, int splits,
   *reinterpret_cast<uint4*>(out + idx) = u;
 }
 
+// PC_FC_REDUCE_PDL=0: plain stream-ordered launch of the split-K reduction
+static bool fc_reduce_pdl() {
+  static const int on = [] {
+    const char* e = getenv("PC_FC_REDUCE_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0 && pdl_enabled();
+}
+
 static int fc_reduce_epilogue(const float* part, int splits, int M, int N, const float* bias, int relu,
                               const void* mask, void* out, long long o_ld, long long o_cb, long long o_bstride,
                               cudaStream_t st) {
   const long long work = (long long)M * (N / 8);
-  fc_reduce_epilogue_k<<<(int)((work + 255) / 256), 256, 0, st>>>(
-      part, splits, M, N, bias, relu, static_cast<const __nv_bfloat16*>(mask), static_cast<__nv_bfloat16*>(out),
-      o_ld, o_cb, o_bstride);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)((work + 255) / 256));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = fc_reduce_pdl() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fc_reduce_epilogue_k, part, splits, M, N, bias, relu,
+                                     static_cast<const __nv_bfloat16*>(mask), static_cast<__nv_bfloat16*>(out), o_ld,
+                                     o_cb, o_bstride);
+  PC_REQUIRE(e == cudaSuccess, PC_ECUDA, "fc_reduce_epilogue launch: %s", cudaGetErrorString(e));
   PC_CUDA_CHECK_LAUNCH("fc_reduce_epilogue");
   return PC_OK;
 }

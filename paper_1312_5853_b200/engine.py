@@ -102,6 +102,7 @@ class ColumnEngine:
         self.has_dropout = any(st.kind == "dropout" for st in self.layers)
         self.bad_label = torch.zeros(1, dtype=torch.int32, device=device)
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+        self.loss_ticket = torch.zeros(1, dtype=torch.int32, device=device)   # pc_softmax_xent_loss
         self.bias_side = None                # enable_bias_side
         self.wt_ready = False                # the step program prepared st.wt this step
 
@@ -674,10 +675,10 @@ class ColumnEngine:
                      st.inp.data_ptr(), st.out.data_ptr(), st.argmax.data_ptr(), self.prec, s)
         else:
             k = st.cl.layer.classes
-            self._call(st, "pc_softmax_xent", self.B, k, st.inp.data_ptr(), self.labels.data_ptr(),
-                     float(loss_scale), st.out.data_ptr(), st.row_loss.data_ptr(),
-                     self.bad_label.data_ptr(), self.prec, s)
-            self._call(st, "pc_sum_f64", self.B, st.row_loss.data_ptr(), self.loss.data_ptr(), s)
+            # loss + gradient + the step loss's fixed-order sum in one launch
+            self._call(st, "pc_softmax_xent_loss", self.B, k, st.inp.data_ptr(), self.labels.data_ptr(),
+                       float(loss_scale), st.out.data_ptr(), st.row_loss.data_ptr(), self.bad_label.data_ptr(),
+                       self.loss.data_ptr(), self.loss_ticket.data_ptr(), self.prec, s)
 
     def _dropout(self, st, src, dst):
         hh, ww, cc, cdense, coff, thresh = st.drop
