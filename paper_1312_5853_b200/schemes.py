@@ -645,7 +645,11 @@ def evaluation_errors(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, x,
     if wids:
         with torch.cuda.device(dev):
             engines = _eval_engines(fabric, cs, b, wids)
-            xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+            if isinstance(x, np.ndarray) and x.dtype == np.float64 and all(e.s2d and e.in_c == 3 for e in engines):
+                # float64 test images travel raw; the input kernel rounds them on the device
+                xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+            else:
+                xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
             yd = torch.zeros(b, dtype=torch.int32, device=dev)
             for e in engines:
                 e.load_batch(xd, yd)

@@ -38,7 +38,7 @@ train_set = Dataset(dev.cpu().numpy().astype(np.float64), np.arange(n) // 2, 100
 def run(device_data: bool):
     cfg = P.TrainConfig(net=net, plan=P.ParallelPlan(1, 1), epochs=epochs, batch=256, seed=0, train_data=train_set,
                         precision="bf16", device_data=device_data, record_wall_time=True,
-                        sgd=P.SgdState())
+                        sgd=P.SgdState(learning_rate=0.001))   # He init at lr 0.01 diverges (as in the reference)
     res = P.train(cfg)
     torch.cuda.synchronize()
     w = [r.wall_seconds for r in res.records]
