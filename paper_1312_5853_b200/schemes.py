@@ -646,8 +646,14 @@ def evaluation_errors(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, x,
         with torch.cuda.device(dev):
             engines = _eval_engines(fabric, cs, b, wids)
             if isinstance(x, np.ndarray) and x.dtype == np.float64 and all(e.s2d and e.in_c == 3 for e in engines):
-                # float64 test images travel raw; the input kernel rounds them on the device
-                xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+                # float64 test images travel raw (threaded copy into cached pinned memory); the
+                # input kernel rounds them on the device
+                pin = fabric.__dict__.get("_eval_pinned")
+                if pin is None or tuple(pin.shape) != tuple(x.shape):
+                    pin = torch.empty(tuple(x.shape), dtype=torch.float64).pin_memory()
+                    fabric._eval_pinned = pin
+                _parallel_copy(pin.numpy(), np.ascontiguousarray(x))
+                xd = pin.to(dev, non_blocking=True)
             else:
                 xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
             yd = torch.zeros(b, dtype=torch.int32, device=dev)
