@@ -94,6 +94,21 @@ def _parallel_copy(dst: np.ndarray, src: np.ndarray, parts: int = 8) -> None:
     list(_COPY_POOL.map(lambda b: np.copyto(dst[b[0]:b[1]], src[b[0]:b[1]]), bounds))
 
 
+def _parallel_take(dst: np.ndarray, src: np.ndarray, idx: np.ndarray, parts: int = 8) -> None:
+    """dst[...] = src[idx] (rows) in `parts` slices on the copy pool: the host-fed
+    trainer's batch gather straight into pinned staging memory."""
+    global _COPY_POOL
+    n = len(idx)
+    if n < parts or dst.nbytes < (16 << 20):
+        np.take(src, idx, axis=0, out=dst)
+        return
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _COPY_POOL = ThreadPoolExecutor(max_workers=parts, thread_name_prefix="pc-copy")
+    bounds = [(i * n // parts, (i + 1) * n // parts) for i in range(parts)]
+    list(_COPY_POOL.map(lambda b: np.take(src, idx[b[0]:b[1]], axis=0, out=dst[b[0]:b[1]]), bounds))
+
+
 class _Runner:
     """Engines of this process for one (plan, shard) plus the exchange wiring."""
 
@@ -218,8 +233,10 @@ class _Runner:
         # space-to-depth input layer travels as raw float64 — a multi-threaded copy into
         # pinned memory, no host-side conversion pass — and the input kernel rounds it
         # to float32 on the device (the value the float32 path uploads)
-        raw64 = isinstance(batch_x, np.ndarray) and batch_x.dtype == np.float64 and \
+        raw64 = (isinstance(batch_x, np.ndarray) and batch_x.dtype == np.float64 or
+                 isinstance(batch_x, torch.Tensor) and not batch_x.is_cuda and batch_x.dtype == torch.float64) and \
             all(e.s2d and e.in_c == 3 for e in self.engines.values())
+        pinned64 = raw64 and isinstance(batch_x, torch.Tensor) and batch_x.is_pinned() and batch_x.is_contiguous()
         xdt = torch.bfloat16 if keep_bf16 else torch.float64 if raw64 else torch.float32
         if isinstance(batch_x, torch.Tensor) and batch_x.is_cuda and batch_x.dtype == xdt:
             xs = batch_x.contiguous()
@@ -254,11 +271,13 @@ class _Runner:
                 xs.record_stream(cs)
             if y.is_cuda:
                 y.record_stream(cs)
-        if raw64:
-            _parallel_copy(self.x_host.numpy(), batch_x)
+        if raw64 and not pinned64:
+            _parallel_copy(self.x_host.numpy(), batch_x.numpy() if isinstance(batch_x, torch.Tensor) else batch_x)
         with torch.cuda.stream(cs):
             if xs is not None:
                 self.x_dev.copy_(xs)
+            elif pinned64:
+                self.x_dev.copy_(batch_x, non_blocking=True)
             elif raw64:
                 self.x_dev.copy_(self.x_host, non_blocking=True)
             elif x.is_pinned():
@@ -595,8 +614,12 @@ def _eval_engines(fabric: Fabric, cs: ColumnizedSpec, b: int, wids: list) -> lis
             eng.p32.copy_(src.p32)
             if eng.plow is not None:
                 eng.plow.copy_(src.plow)
+            eng._host_src = None
         else:
-            eng.load_params(dict.__getitem__(fabric._local[eng.wid], "host_params"))
+            hp = dict.__getitem__(fabric._local[eng.wid], "host_params")
+            if getattr(eng, "_host_src", None) is not hp:    # setup_workers' host copy, loaded once
+                eng.load_params(hp)
+                eng._host_src = hp
     return engines
 
 

@@ -395,13 +395,17 @@ def test_float64_numpy_batch_matches_float32_batch_bit_for_bit():
     x, y = synthetic_rows(1000, 1, net.input_shape, 2, np.arange(16) * 37)
     dense = P.init_dense_params(net, 1, std=0.01)
     out = []
-    for xb in (x.astype(np.float64), torch.from_numpy(x).pin_memory()):
+    x64 = torch.from_numpy(x.astype(np.float64))
+    # float64 numpy, float64 CPU tensor (pageable, pinned: the host-fed trainer's
+    # staging buffer), float32 pinned
+    for xb in (x.astype(np.float64), x64, x64.pin_memory(), torch.from_numpy(x).pin_memory()):
         fab = P.spawn(1, precision="bf16")
         P.setup_workers(fab, plan, cs, dense, P.SgdState())
         losses = [P.hybrid_step(fab, plan, cs, xb, y).loss for _ in range(3)]
         out.append((losses, fab._engines[0].p32.clone(), fab._runner.x_dev.dtype))
-    assert out[0][2] == torch.float64 and out[1][2] == torch.float32
-    assert out[0][0] == out[1][0] and torch.equal(out[0][1], out[1][1])
+    assert [o[2] for o in out] == [torch.float64] * 3 + [torch.float32]
+    for o in out[1:]:
+        assert out[0][0] == o[0] and torch.equal(out[0][1], o[1])
 
 
 @pytest.mark.parametrize("precision,loss_tol,upd_tol", [("bf16", 1e-2, 0.3), ("tf32", 5e-3, 0.1)])

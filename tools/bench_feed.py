@@ -61,4 +61,11 @@ t0 = time.perf_counter()
 for _ in range(10):
     P.evaluation_errors(fab, P.ParallelPlan(1, 1), cs, tx, ty)
 out["evaluation_images_per_s"] = 2560 / (time.perf_counter() - t0)
+P.hybrid_step(fab, P.ParallelPlan(1, 1), cs, tx, ty)     # after a step: parameters come from the engine
+P.evaluation_errors(fab, P.ParallelPlan(1, 1), cs, tx, ty)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(10):
+    P.evaluation_errors(fab, P.ParallelPlan(1, 1), cs, tx, ty)
+out["evaluation_after_step_images_per_s"] = 2560 / (time.perf_counter() - t0)
 print(json.dumps(out), flush=True)
