@@ -31,6 +31,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib as L
+from . import mailbox as _mb
 from .errors import CapacityError, ValidationError
 
 
@@ -135,11 +136,18 @@ class Worker:
     def assert_capacity(self) -> None:
         self.fabric.meter_assert(self.wid)
 
-    def send(self, *a, **k):
-        raise ValidationError("the device fabric moves data with collectives; point-to-point "
-                              "send/recv of the simulated fabric is not offered")
+    # messaging (mailbox.py): the reference's semantics, device tensors move GPU to GPU
+    def send(self, dst: int, tag, value) -> None:
+        self.fabric.mailbox.send(self.wid, dst, tag, value)
 
-    recv = send
+    def recv(self, src: int, tag):
+        return self.fabric.mailbox.recv(self.wid, src, tag)
+
+    def reduce_to_root(self, group, root: int, value, tag="reduce"):
+        return _mb.reduce_to_root(self, group, root, value, tag)
+
+    def broadcast_from_root(self, group, root: int, value, tag="bcast"):
+        return _mb.broadcast_from_root(self, group, root, value, tag)
 
 
 class Fabric:
@@ -176,21 +184,28 @@ class Fabric:
         else:
             self.rank = 0
             self.local_wids = list(range(n))
+        self.mailbox = _mb.Mailbox(self)
+        self._groups = {}
+        # without a CUDA device the fabric still runs worker programs (messaging,
+        # metering); every device use (setup_workers, the steps) raises
+        self._torch_device = None
+        self.multi = False
+        self._device_of = [None] * n
         if not torch.cuda.is_available():
-            raise ValidationError("the device fabric needs a CUDA device (B200); none is visible")
+            if devices is not None:
+                raise ValidationError("devices= given but no CUDA device is visible")
+            return
         idx = torch.cuda.current_device()
         if self.dist:
             import os
             idx = int(os.environ.get("LOCAL_RANK", self.rank % torch.cuda.device_count()))
             torch.cuda.set_device(idx)
-        self.torch_device = torch.device("cuda", idx)
-        self._groups = {}
+        self._torch_device = torch.device("cuda", idx)
         # single process, several workers: one host thread + stream per worker on its GPU
         # (multidev.PeerRunner), the workers spread over the visible GPUs in contiguous
         # blocks (the columns of a replica share a GPU when there are fewer GPUs than
         # workers). devices=[...] pins worker w to GPU devices[w] (repeats allowed: the
         # same machinery on one GPU, which is how a one-GPU box tests it).
-        self.multi = False
         self._device_of = [self.torch_device] * n
         if not self.dist and n > 1:
             if devices is not None:
@@ -208,7 +223,15 @@ class Fabric:
         elif devices is not None and list(devices) not in ([idx], [idx] * n):
             raise ValidationError("devices= applies to single-process fabrics")
 
+    @property
+    def torch_device(self) -> torch.device:
+        if self._torch_device is None:
+            raise ValidationError("the device fabric needs a CUDA device (B200); none is visible")
+        return self._torch_device
+
     def device_of(self, wid: int) -> torch.device:
+        if self._device_of[wid] is None:
+            raise ValidationError("the device fabric needs a CUDA device (B200); none is visible")
         return self._device_of[wid]
 
     @property
@@ -220,16 +243,14 @@ class Fabric:
             raise CapacityError(wid, self.meter.current[wid], self.device.memory_capacity)
 
     def run(self, program, args: list | None = None) -> list:
-        """program(ctx, *args[wid]) on every worker hosted by this process;
+        """program(ctx, *args[wid]) on every worker hosted by this process, one
+        host thread each, scheduled ``lockstep`` or ``threads`` (mailbox.py);
         other processes' entries are None. Lowest failing worker's error wins."""
         if args is None:
             args = [() for _ in range(self.n)]
         if len(args) != self.n:
             raise ValidationError(f"need args for {self.n} workers, got {len(args)}")
-        results = [None] * self.n
-        for wid in self.local_wids:
-            results[wid] = program(Worker(self, wid), *args[wid])
-        return results
+        return _mb.run_programs(self, program, args)
 
     # --------------------------------------------------------- process groups
     def groups(self, d: int, m: int):

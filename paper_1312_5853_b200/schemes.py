@@ -53,6 +53,7 @@ def setup_workers(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, dense_
     if fabric.n != plan.workers:
         raise ValidationError(f"plan grid {plan.describe()} needs {plan.workers} workers, "
                               f"fabric has {fabric.n}")
+    fabric.torch_device          # the device path: raises ValidationError when no CUDA device is visible
     m = plan.model_columns
     fabric._engines.clear()
     fabric._runner = None

@@ -171,3 +171,63 @@ def test_bucketed_gradient_allreduce_overlapped_with_backward():
                for r in range(world))
     for r in range(world):
         np.testing.assert_allclose(got[r], want, rtol=1e-6, atol=1e-6)
+
+
+def _ring_program(ctx):
+    """Ring exchange with out-of-order tags, then reduce + broadcast (the
+    reference's determinism program, `tests/test_fabric.py:219-240`)."""
+    acc = np.full(4, float(ctx.wid) + 0.25)
+    nxt, prv = (ctx.wid + 1) % ctx.n, (ctx.wid - 1) % ctx.n
+    for step in range(3):
+        ctx.send(nxt, ("late", step), acc * 2)
+        ctx.send(nxt, ("ring", step), acc)
+        acc = acc + ctx.recv(prv, ("ring", step))       # arrives behind the "late" message
+        acc = acc - 0.5 * ctx.recv(prv, ("late", step))
+    ctx.send(nxt, "t", torch.arange(3, dtype=torch.float32) + ctx.wid)
+    t = ctx.recv(prv, "t")
+    total = ctx.reduce_to_root(range(ctx.n), 0, acc)
+    out = ctx.broadcast_from_root(range(ctx.n), 0, total if ctx.wid == 0 else None)
+    return out, t
+
+
+def _mailbox_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1312_5853_b200.fabric import spawn
+        fab = spawn(world)
+        res = fab.run(_ring_program)
+        out, t = res[rank]
+        q.put((rank, out, t.numpy(), fab.ledger.snapshot()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fabric_run_messaging_across_ranks_matches_one_process():
+    """Fabric.run under a process group (one worker per rank): send/recv cross
+    ranks over torch.distributed, tags matched out of order, CPU tensors kept as
+    tensors; results equal the single-process run, and each rank books its own
+    sends."""
+    from paper_1312_5853_b200.fabric import spawn
+    world = 3
+    fab = spawn(world, scheduling="threads")
+    want = fab.run(_ring_program)
+    want_snap = fab.ledger.snapshot()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mailbox_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    booked = {}
+    for rank, out, t, snap in got:
+        assert np.array_equal(out, want[rank][0])
+        assert np.array_equal(t, want[rank][1].numpy())
+        for link, v in snap.items():
+            assert link[0] == rank
+            booked[link] = v
+    assert booked == want_snap

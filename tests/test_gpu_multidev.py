@@ -110,3 +110,37 @@ def test_peer_fabric_evaluation_and_errors():
     assert counts[0] == counts[1]
     with pytest.raises(P.ValidationError):
         P.spawn(4, devices=[0, 0])
+
+
+@pytest.mark.parametrize("sched", ["lockstep", "threads"])
+def test_fabric_run_moves_device_tensors_between_workers(sched):
+    """Fabric.run with CUDA tensor payloads (mailbox.py): the copy lands on the
+    receiver's GPU, ordered after the sender's stream; reduce_to_root sums on the
+    root's device in ascending worker order, bit-identical to the float64 host
+    program rounded the same way."""
+    import torch
+    import paper_1312_5853_b200 as P
+    n = 4
+    fab = P.spawn(n, scheduling=sched, devices=_devices(n))
+    rs = np.random.RandomState(7)
+    host = [rs.randn(1 << 16).astype(np.float32) for _ in range(n)]
+
+    def program(ctx):
+        dev = fab.device_of(ctx.wid)
+        x = torch.from_numpy(host[ctx.wid]).to(dev)
+        x = x * 2 + 1                               # produced on this worker's stream
+        ctx.send((ctx.wid + 1) % n, "ring", x)
+        y = ctx.recv((ctx.wid - 1) % n, "ring")
+        assert y.device == dev
+        tot = ctx.reduce_to_root(range(n), 0, x + y)
+        return ctx.broadcast_from_root(range(n), 0, tot if ctx.wid == 0 else None).cpu()
+
+    res = fab.run(program)
+    xs = [torch.from_numpy(h) * 2 + 1 for h in host]
+    want = None
+    for w in range(n):
+        v = xs[w] + xs[(w - 1) % n]
+        want = v.clone() if want is None else want.add_(v)
+    for r in res:
+        assert torch.equal(r, want)
+    assert fab.ledger.total_messages == n + (n - 1) * 2
