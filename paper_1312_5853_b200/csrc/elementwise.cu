@@ -892,6 +892,10 @@ __global__ void __launch_bounds__(256) s2d_k(int B, int C_, int H, int W, int s_
 // into SMEM with 16-byte loads (aligned down, the tail clamped to the tensor),
 // then each thread assembles one SS x SS block and writes its CS channels as
 // 16-byte stores. Rows/columns outside the image are zero.
+__device__ __forceinline__ float s2d_f(float v) { return v; }
+__device__ __forceinline__ float s2d_f(double v) { return __double2float_rn(v); }
+__device__ __forceinline__ float s2d_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
 template <int CS, int SS, int CC>
 __global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, int Ws, long long total,
                                                  const __nv_bfloat16* __restrict__ x,
@@ -963,6 +967,74 @@ __global__ void __launch_bounds__(64) s2d_rows_k(int H, int W, int p, int Hs, in
   for (int c = threadIdx.x; c < Ws * CS / 8; c += blockDim.x) {
     const int X = c / (CS / 8), q = c % (CS / 8);
     out[c] = src[X * (CS / 8) + ((q ^ (X & 7)) % (CS / 8))];
+  }
+}
+
+// float / float64 source (the float32 device-resident batch, a caller's float64
+// images), one CTA of 64 threads per output block row (b, Y): each of the SS*CC
+// input rows of the block row is staged, converted to float and shifted so that
+// block X's SS values are one aligned float4 in SMEM (scalar loads, coalesced
+// across the warp, 48 independent loads per lane in flight); each thread then
+// assembles its block from conflict-free float4 reads and the block row leaves as
+// coalesced 16-byte stores through a swizzled SMEM row (as s2d_rows_k).
+template <typename TS, int SS, int CC, int IT>
+__global__ void __launch_bounds__(64) s2d_rows_f_k(int H, int W, int p, int Hs, int Ws,
+                                                   const TS* __restrict__ x, __nv_bfloat16* __restrict__ dst,
+                                                   int ones) {
+  PC_PDL_TRIGGER();
+  constexpr int CS = 64, ROWS = SS * CC, RS = 32 * IT;  // staged row: RS >= SS * Ws values
+  static_assert(SS == 4 && ROWS % 2 == 0, "4 values per block, rows split over two warps");
+  // staged already rounded to bf16 (the output's rounding of the same float value)
+  __shared__ __align__(16) __nv_bfloat16 lin[ROWS * RS];
+  __shared__ __align__(16) __nv_bfloat16 lout[RS / SS * CS];
+  const int b = blockIdx.x / Hs, Y = blockIdx.x - b * Hs;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float val[ROWS / 2][IT];
+#pragma unroll
+  for (int rr = 0; rr < ROWS / 2; ++rr) {
+    const int r = warp * (ROWS / 2) + rr, c = r / SS, dy = r - c * SS;  // row r = (c, dy)
+    const int iy = Y * SS + dy - p;
+    const bool rok = iy >= 0 && iy < H;
+    const TS* src = x + (((long long)b * CC + c) * H + (rok ? iy : 0)) * W;
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int ix = lane + 32 * k - p;
+      val[rr][k] = rok && ix >= 0 && ix < W ? s2d_f(__ldg(src + ix)) : 0.f;
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < ROWS / 2; ++rr)
+#pragma unroll
+    for (int k = 0; k < IT; ++k) lin[(warp * (ROWS / 2) + rr) * RS + lane + 32 * k] = __float2bfloat16_rn(val[rr][k]);
+  __syncthreads();
+  for (int X = threadIdx.x; X < Ws; X += blockDim.x) {
+    float v[CS];
+#pragma unroll
+    for (int i = 0; i < CS; ++i) v[i] = i == ones ? 1.f : 0.f;
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int c = r / SS, dy = r - c * SS;
+      const uint2 f = *reinterpret_cast<const uint2*>(lin + r * RS + SS * X);
+      v[(dy * SS + 0) * CC + c] = __uint_as_float(f.x << 16);
+      v[(dy * SS + 1) * CC + c] = __uint_as_float(f.x & 0xFFFF0000u);
+      v[(dy * SS + 2) * CC + c] = __uint_as_float(f.y << 16);
+      v[(dy * SS + 3) * CC + c] = __uint_as_float(f.y & 0xFFFF0000u);
+    }
+#pragma unroll
+    for (int q = 0; q < CS / 8; ++q) {
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(lout + (X * CS + (q ^ (X & 7)) * 8)) = u;
+    }
+  }
+  __syncthreads();
+  uint4* out = reinterpret_cast<uint4*>(dst + (long long)blockIdx.x * Ws * CS);
+  const uint4* sm = reinterpret_cast<const uint4*>(lout);
+  for (int c = threadIdx.x; c < Ws * CS / 8; c += blockDim.x) {
+    const int X = c / (CS / 8), q = c % (CS / 8);
+    out[c] = sm[X * (CS / 8) + (q ^ (X & 7))];
   }
 }
 
@@ -1318,6 +1390,23 @@ extern "C" int pc_space_to_depth_ex(int B, int C, int H, int W, int s, int p, in
   if (n == 0) return PC_OK;
   const int g = grid_for(n, 256);
   auto* d = static_cast<__nv_bfloat16*>(dst);
+  static const int rows_f = [] {   // PC_S2D_ROWS=0: the per-block kernel for float / float64 sources
+    const char* e = getenv("PC_S2D_ROWS");
+    return e ? atoi(e) : 1;
+  }();
+  if (rows_f && Cs == 64 && s == 4 && C == 3 && Ws * 4 <= 256 &&
+      (src_prec == PC_FP32 || src_prec == PC_FP64 || (rows_f == 2 && src_prec == PC_BF16))) {
+    if (src_prec == PC_BF16)
+      s2d_rows_f_k<__nv_bfloat16, 4, 3, 8><<<B * Hs, 64, 0, S(st)>>>(H, W, p, Hs, Ws,
+                                                                     static_cast<const __nv_bfloat16*>(src), d, ones);
+    else if (src_prec == PC_FP32)
+      s2d_rows_f_k<float, 4, 3, 8><<<B * Hs, 64, 0, S(st)>>>(H, W, p, Hs, Ws, static_cast<const float*>(src), d, ones);
+    else
+      s2d_rows_f_k<double, 4, 3, 8><<<B * Hs, 64, 0, S(st)>>>(H, W, p, Hs, Ws, static_cast<const double*>(src), d,
+                                                             ones);
+    PC_CUDA_CHECK_LAUNCH("space_to_depth");
+    return PC_OK;
+  }
   if (src_prec == PC_BF16 && Cs == 64 && s == 4 && C == 3 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
     const size_t smem = (size_t)C * (((size_t)s * W + 7) / 8 + 1) * 8 * 2 + (size_t)Ws * 64 * 2;
     if (smem <= 48 * 1024) {  // AlexNet conv1: row-staged
