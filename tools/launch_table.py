@@ -17,7 +17,7 @@ def main(path, out_path, peak=6544.0):
     for r in data:
         per.setdefault(r[idi], {"name": r[ki]})[r[mi]] = (float(r[vi].replace(",", "")), r[ui])
     items = list(per.values())
-    starts = [i for i, it in enumerate(items) if "s2d_k<" in it["name"] or "s2d_rows_k" in it["name"]]
+    starts = [i for i, it in enumerate(items) if "s2d_k<" in it["name"] or "s2d_rows_" in it["name"]]
     step = items[starts[-1]:]
     out = ["# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none",
