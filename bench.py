@@ -441,7 +441,9 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if plan.model_columns == 1 and plan.data_shards > 1 else "weak",
+        # dp (global 256 sharded) and mp (the same 256 over two columns) divide a fixed batch;
+        # hybrid keeps 256 per replica group, so the total grows with the replicas
+        "scaling": "weak" if plan.data_shards > 1 and plan.model_columns > 1 or plan.workers == 1 else "strong",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic (gen_synthetic blobs, 1000 classes, "
         "3x227x227; Gaussian std 0.01 init, seed 0)",
         "config": {"workload": f"AlexNet-227 {label} train step", "global_batch": gbatch,

@@ -28,7 +28,9 @@ wsb = lib.raw("pc_conv2d_backward_workspace")(C.byref(g), L.PC_BF16)
 ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream().cuda_stream
 flops = 2 * B * ho * ho * n * c * k * k
-def fwd(): lib.call("pc_conv2d_forward", C.byref(g), x.data_ptr(), w.data_ptr(), bias.data_ptr(), y.data_ptr(), L.PC_BF16, 1, st)
+import os
+FWD_FLAGS = 1 | (L.PC_ZERO_TAIL16 if os.environ.get("PROF_ZERO_TAIL") == "1" else 0)   # PC_RELU (+ zero tail)
+def fwd(): lib.call("pc_conv2d_forward", C.byref(g), x.data_ptr(), w.data_ptr(), bias.data_ptr(), y.data_ptr(), L.PC_BF16, FWD_FLAGS, st)
 def dgrad(): lib.call("pc_conv2d_backward", C.byref(g), x.data_ptr(), w.data_ptr(), gy.data_ptr(), gx.data_ptr(), None, gw.data_ptr(), gb.data_ptr(), L.PC_BF16, L.PC_WANT_DX, ws.data_ptr(), wsb, st)
 def wgrad(): lib.call("pc_conv2d_backward", C.byref(g), x.data_ptr(), w.data_ptr(), gy.data_ptr(), gx.data_ptr(), None, gw.data_ptr(), gb.data_ptr(), L.PC_BF16, L.PC_WANT_DW, ws.data_ptr(), wsb, st)
 for fn_name, fn in (("fwd", fwd), ("dgrad", dgrad), ("wgrad", wgrad)):
