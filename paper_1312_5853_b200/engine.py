@@ -39,6 +39,19 @@ ALIGN = 32  # elements; every flat-buffer slice starts 128-byte aligned in fp32
 PROFILE: list | None = None  # set to a list to record per-call CUDA events
 
 
+def _wg_ctas() -> dict:
+    """PC_WG_CTAS: grid caps of the side-stream conv weight gradients, "N" for all
+    layers or "layer:N,layer:N" (e.g. "3:100"); empty = uncapped."""
+    out = {}
+    for part in filter(None, os.environ.get("PC_WG_CTAS", "").split(",")):
+        k, _, v = part.rpartition(":")
+        out[int(k) if k else -1] = int(v)
+    return out
+
+
+WG_CTAS = _wg_ctas()
+
+
 def torch_dtype(prec: int):
     return torch.bfloat16 if prec == L.PC_BF16 else torch.float32
 
@@ -727,9 +740,16 @@ class ColumnEngine:
                                   st.gout.data_ptr(), st.gin.data_ptr(), st.inp.data_ptr() if st.mask_dx else None,
                                   None, None, self.cprec, flags & ~L.PC_WANT_DW, None, 0, None, s)
                 self._fork(wg)
-                self.lib.call("pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
-                              st.gout.data_ptr(), None, None, self.g32[st.w_off:].data_ptr(), gb, self.cprec,
-                              L.PC_WANT_DW, self.ws_wg.data_ptr(), self.ws_bytes, C.byref(upd), wg.cuda_stream)
+                cap = WG_CTAS.get(st.cl.index, WG_CTAS.get(-1, 0))
+                if cap:
+                    self.lib.call("pc_set_grid_cap", cap)
+                try:
+                    self.lib.call("pc_conv2d_backward_ex", C.byref(st.geom), st.inp.data_ptr(), w_ptr,
+                                  st.gout.data_ptr(), None, None, self.g32[st.w_off:].data_ptr(), gb, self.cprec,
+                                  L.PC_WANT_DW, self.ws_wg.data_ptr(), self.ws_bytes, C.byref(upd), wg.cuda_stream)
+                finally:
+                    if cap:
+                        self.lib.call("pc_set_grid_cap", 0)
                 if st.keep is not None:   # (not reached: the input layer's update is not fused)
                     raise RuntimeError("weight-gradient side stream: masked layer")
                 return

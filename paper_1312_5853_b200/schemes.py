@@ -201,8 +201,8 @@ class _Runner:
             for eng in self.engines.values():
                 if getattr(eng, "fuse_sgd", False):
                     eng.enable_wgrad_side(self.wg_side)
-                    if fc_too:   # FC weight gradients + updates on the same stream, no grid caps
-                        eng.enable_fc_side(self.wg_side, 0, 0, 0)
+                    if fc_too:   # FC weight gradients + updates on the same stream (PC_FC_WG_CTAS: grid cap)
+                        eng.enable_fc_side(self.wg_side, int(os.environ.get("PC_FC_WG_CTAS", "0")), 0, 0)
         # conv filters in the data-gradient layout, prepared on a side stream at the
         # start of every step (beside the forward) instead of inside each backward
         self.wt_side = None
