@@ -104,3 +104,64 @@ def test_lrn_dropout_net_fp32_matches_oracle(d, m, cross):
             for k in ("w", "b"):
                 start = P.split_params(dense, cs, j)[i][k]
                 assert rel(params[i][k] - start, of.params[j][i][k] - start) < 1e-4, (j, i, k)
+
+
+@pytest.mark.parametrize("plan_args", [(1, 1, ()), (1, 2, (8,))])   # 8: conv3 (LRN shifts the indices)
+def test_alexnet_lrn_dropout_bf16_bench_config_matches_oracle(plan_args):
+    """The bench's second configuration (configs/alexnet_lrn_dropout.net, bf16, every
+    default switch) at batch 16, single column and Krizhevsky's two columns: step 1
+    against the float64 oracle replaying the device's pool and ReLU decisions (the
+    dropout masks come from the same SplitMix64 stream) — loss <= 1e-2, every layer's
+    update <= 0.3 rel-L2 — and steps 2-3 (graph captured, replayed) equal to the
+    same steps run eagerly."""
+    import torch
+    import paper_1312_5853_b200 as P
+    from oracle.ref_engine import OracleFabric
+    from parity import (assert_near_ties, assert_relu_near_ties, device_argmax, device_relu_masks,
+                        rel_l2)
+    from paper_1312_5853_b200.data import synthetic_rows
+    from paper_1312_5853_b200.plan import plan_columnized
+    from paper_1312_5853_b200.schemes import column_params
+    net = P.load_network(CONFIGS / "alexnet_lrn_dropout.net")
+    plan = P.ParallelPlan(*plan_args)
+    cs = plan_columnized(net, plan)
+    dense = {i: {k: v.astype(np.float32).astype(np.float64) for k, v in t.items()}
+             for i, t in P.init_dense_params(net, 0, std=0.01).items()}
+    x, y = synthetic_rows(1000, 1, net.input_shape, 4, np.arange(16) * 61)
+    x = x.astype(np.float64)
+    runs = []
+    for graph in ("1", "0"):
+        import os
+        old = os.environ.get("PC_GRAPH")
+        os.environ["PC_GRAPH"] = graph
+        try:
+            fab = P.spawn(plan.workers, precision="bf16")
+            P.setup_workers(fab, plan, cs, dense, P.SgdState())
+            losses, snap = [], None
+            for s in range(3):
+                losses.append(P.hybrid_step(fab, plan, cs, x, y).loss)
+                if s == 0 and graph == "1":
+                    forced, relu = device_argmax(fab, plan), device_relu_masks(fab, plan)
+                    snap = [column_params(fab, j) for j in range(plan.model_columns)]
+            runs.append((losses, [e.p32.clone() for _, e in sorted(fab._engines.items())], snap, forced if snap else None,
+                         relu if snap else None))
+        finally:
+            if old is None:
+                os.environ.pop("PC_GRAPH", None)
+            else:
+                os.environ["PC_GRAPH"] = old
+    (lg, pg, snap, forced, relu), (le, pe, _, _, _) = runs
+    assert lg == le
+    for a, b in zip(pg, pe):
+        assert torch.equal(a, b)
+    of, trace = OracleFabric(net, plan, dense), {}
+    oloss = of.step(x, y, trace=trace, force_argmax=forced, force_relu=relu)
+    assert_near_ties(trace, forced, of.cs, 2e-2)
+    assert_relu_near_ties(trace, relu, 2e-2)
+    assert abs(lg[0] - oloss) / abs(oloss) < 1e-2, (lg[0], oloss)
+    for j in range(plan.model_columns):
+        start = P.split_params(dense, cs, j)
+        for i in snap[j]:
+            for k in ("w", "b"):
+                err = rel_l2(snap[j][i][k] - start[i][k], of.params[j][i][k] - start[i][k])
+                assert err < 0.3, (j, i, k, err)
