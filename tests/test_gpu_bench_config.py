@@ -127,6 +127,24 @@ def test_alexnet_b256_fp32_one_step_matches_oracle(alexnet, monkeypatch):
             assert rel(vel[i][k], ovel[i][k]) < 1e-5, (i, k, flips)
 
 
+def test_alexnet_b256_tf32_one_step_matches_oracle(alexnet, monkeypatch):
+    """The bench's `--precision tf32` line (float storage, tcgen05 kind::tf32) at its
+    batch 256: one step vs the oracle at the TF32 bounds of test_gpu_tf32.py (loss
+    <= 5e-3, update <= 0.1 rel-L2), on the tf32 kernels."""
+    from paper_1312_5853_b200._lib import lib
+    net, dense, x, y = alexnet
+    n0 = lib().dll.pc_tf32_contractions()
+    _, steps, _ = run_steps(net, dense, x, y, "tf32", 1, True, monkeypatch)
+    assert lib().dll.pc_tf32_contractions() > n0
+    snap = steps[0]
+    oloss, ovel, flips = _oracle_first_step(net, dense, x, y, snap, 2e-2)
+    assert abs(snap["loss"] - oloss) / abs(oloss) < 5e-3, (snap["loss"], oloss)
+    vel = snap["velocity"]
+    for i in vel:
+        for k in ("w", "b"):
+            assert rel_l2(vel[i][k], ovel[i][k]) < 0.1, (i, k, flips)
+
+
 @pytest.mark.parametrize("precision,loss_tol,upd_tol", [("fp32", 1e-5, 1e-5), ("bf16", 1e-2, 0.3)])
 def test_small64_config1_b32_two_steps(precision, loss_tol, upd_tol):
     """BASELINE configs[0]: alexnet_small64, gen_synthetic(100, 4, (3, 64, 64), 0), B=32, d1m1.
