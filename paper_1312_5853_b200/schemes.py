@@ -665,11 +665,19 @@ def evaluation_errors(fabric: Fabric, plan: ParallelPlan, cs: ColumnizedSpec, x,
     if fabric.multi:
         from .multidev import evaluate
         engines = _eval_engines(fabric, cs, b, wids)
+        if isinstance(x, torch.Tensor) and x.is_cuda:
+            x = x.float().cpu().numpy()
         return evaluate(fabric, plan, cs, x, labels, {e.wid: e for e in engines})
     if wids:
         with torch.cuda.device(dev):
             engines = _eval_engines(fabric, cs, b, wids)
-            if isinstance(x, np.ndarray) and x.dtype == np.float64 and all(e.s2d and e.in_c == 3 for e in engines):
+            if isinstance(x, torch.Tensor) and x.is_cuda:
+                # a device-resident test split (train() with device_data): used in place
+                xd = x.to(dev).contiguous()
+                if xd.dtype not in (torch.float32, torch.bfloat16) or \
+                        (xd.dtype == torch.bfloat16 and not all(e.s2d and e.prec == L.PC_BF16 for e in engines)):
+                    xd = xd.float()
+            elif isinstance(x, np.ndarray) and x.dtype == np.float64 and all(e.s2d and e.in_c == 3 for e in engines):
                 # float64 test images travel raw (threaded copy into cached pinned memory); the
                 # input kernel rounds them on the device
                 pin = fabric.__dict__.get("_eval_pinned")

@@ -124,3 +124,30 @@ def test_gather_rows_matches_index_select():
         src = torch.randn((37,) + row, device="cuda")
         idx = np.array([5, 0, 36, 5, 17, 2])
         assert torch.equal(_gather(src, idx), src.index_select(0, torch.as_tensor(idx).cuda()))
+
+
+@pytest.mark.parametrize("plan_args", [(1, 1, ()), (2, 1, ()), (1, 2, (6,))])
+def test_train_device_resident_test_split_matches_host(plan_args):
+    """train() with device_data evaluates the test split from HBM (evaluation_errors
+    on device tensors): the per-epoch test errors and losses equal the host-fed run's,
+    and evaluation_errors on a CUDA tensor equals the numpy call."""
+    import torch
+    import paper_1312_5853_b200 as P
+    net = P.load_network(CONFIGS / "alexnet_small64.net")
+    train_set, test_set = P.gen_synthetic(100, 2, net.input_shape, seed=4)
+    plan = P.ParallelPlan(*plan_args)
+    runs = []
+    for dev in (True, False):
+        cfg = P.TrainConfig(net=net, plan=plan, epochs=2, batch=32, seed=3, train_data=train_set, test_data=test_set,
+                            precision="bf16", device_data=dev, sgd=P.SgdState(learning_rate=0.001))
+        res = P.train(cfg)
+        runs.append([(r.train_loss, r.test_error) for r in res.records])
+        if dev:
+            fab = res.fabric
+            cs = P.columnize(net, plan.model_columns, plan.cross_layers)
+            xd = torch.as_tensor(np.ascontiguousarray(test_set.images[:50], dtype=np.float32)).cuda()
+            a = P.evaluation_errors(fab, plan, cs, xd, test_set.labels[:50])
+            b = P.evaluation_errors(fab, plan, cs, test_set.images[:50], test_set.labels[:50])
+            assert a == b
+    assert runs[0] == runs[1]
+    assert any(e is not None for _, e in runs[0])

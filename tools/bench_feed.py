@@ -68,4 +68,11 @@ t0 = time.perf_counter()
 for _ in range(10):
     P.evaluation_errors(fab, P.ParallelPlan(1, 1), cs, tx, ty)
 out["evaluation_after_step_images_per_s"] = 2560 / (time.perf_counter() - t0)
+txd = torch.as_tensor(np.ascontiguousarray(tx, dtype=np.float32)).cuda()   # device-resident test split
+P.evaluation_errors(fab, P.ParallelPlan(1, 1), cs, txd, ty)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(10):
+    P.evaluation_errors(fab, P.ParallelPlan(1, 1), cs, txd, ty)
+out["evaluation_device_split_images_per_s"] = 2560 / (time.perf_counter() - t0)
 print(json.dumps(out), flush=True)
