@@ -2120,7 +2120,7 @@ static bool halo_wanted(int N, int k) {
 // hsub > 1 (A_HALO_KR2): a CTA tile is hsub vertically adjacent sub-tiles of R rows;
 // the window box spans hsub * R + k - 1 rows and halo_tpi counts CTA tiles.
 static bool setup_halo(Params& p, const void* in, int B, int Hi, int Wi, int Ci, int k, int lo, int Ho, int Wo,
-                       int hsub = 1) {
+                       int hsub = 1, int chans = 64) {
   const int Wv = (Wo + 7) / 8 * 8;
   if (Wv > 128 || Ci % 8 || Ci < 64 || (reinterpret_cast<uintptr_t>(in) & 15) || !get_encode()) return false;
   const int R = BM / Wv;
@@ -2128,7 +2128,9 @@ static bool setup_halo(Params& p, const void* in, int B, int Hi, int Wi, int Ci,
   if (hsub > 1 && (hsub * R + k - 1) * Wv * 128 > HALO_R2_SLOT_BYTES) return false;
   cuuint64_t dims[4] = {(cuuint64_t)Ci, (cuuint64_t)Wi, (cuuint64_t)Hi, (cuuint64_t)B};
   cuuint64_t strides[3] = {(cuuint64_t)Ci * 2, (cuuint64_t)Wi * Ci * 2, (cuuint64_t)Hi * Wi * Ci * 2};
-  cuuint32_t box[4] = {64u, (cuuint32_t)Wv, (cuuint32_t)(hsub * R + k - 1), 1u};
+  // chans = 48: the input layer's structural-zero channels 48..63 are not loaded (the
+  // forward skips their k16 step; the rows keep the 128-byte swizzled pitch)
+  cuuint32_t box[4] = {(cuuint32_t)chans, (cuuint32_t)Wv, (cuuint32_t)(hsub * R + k - 1), 1u};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   if (g_encode(&p.tma_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(in), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -2138,7 +2140,7 @@ static bool setup_halo(Params& p, const void* in, int B, int Hi, int Wi, int Ci,
   p.halo_tpi = (Ho + hsub * R - 1) / (hsub * R);
   p.halo_Wv = Wv;
   p.halo_lo = lo;
-  p.halo_bytes = 64 * Wv * (hsub * R + k - 1) * 2;
+  p.halo_bytes = chans * Wv * (hsub * R + k - 1) * 2;
   p.M = B * p.halo_tpi * BM * hsub;  // virtual rows: hsub 128-row sub-tiles per halo tile
   p.i2c_k = k;
   p.i2c_C = Ci;
@@ -2247,7 +2249,12 @@ int umma_conv_forward(const pc_conv_geom& g, const void* x, const void* w, const
       return e ? atoi(e) : 1;
     }();
     Params q = p;
-    if (kr2 && setup_halo(q, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo, 2) && halo_res_fits(q, g.N)) {
+    static const int h48 = [] {  // PC_HALO48=0: load all 64 channels of the input-layer windows
+      const char* e = getenv("PC_HALO48");
+      return e ? atoi(e) : 1;
+    }();
+    const int wch = h48 && (flags & PC_ZERO_TAIL16) && g.C == BK ? 48 : 64;
+    if (kr2 && setup_halo(q, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo, 2, wch) && halo_res_fits(q, g.N)) {
       p = q;
       halo = res = res2 = true;
     } else if (setup_halo(q, x, g.B, g.H, g.W, g.C, g.k, -g.pad, g.Ho, g.Wo) && halo_res_fits(q, g.N)) {
